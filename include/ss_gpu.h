@@ -1,0 +1,173 @@
+/*
+ * ss_gpu.h — the drop-in GPU boundary: one stall-free hybrid batch through a
+ * Llama-style decoder on B200 (sm_100a), tensor-parallel over tp_size ranks.
+ *
+ * Replaces the reference's model step
+ *     double iteration_time(const Batch&, const CostModelParams&, int tp, int pp)
+ *     (reference proj/include/servesim/costmodel.hpp:60-61, called from
+ *      Engine::try_issue, proj/src/engine.cpp:227)
+ * with a real bf16 forward of the batch's T packed tokens. The measured device
+ * time comes back in *elapsed_ms and goes through the same
+ * max(1, llround(ms*1000)) conversion (engine.cpp:228, core.cpp:8).
+ *
+ * Batch composition (entry order = packed token order), token positions and
+ * KV block tables are produced on the host by the restated scheduler
+ * (ss_host.h); this library never makes scheduling decisions.
+ *
+ * Ownership: the caller owns every descriptor array for the duration of the
+ * call (they are staged into pinned memory and copied to the device before the
+ * call returns control on the stream). The library owns weights, the paged KV
+ * pool and workspaces. Output buffers (logits, next tokens) are owned by the
+ * caller. One ss_ctx per GPU rank, driven by one host thread; not reentrant.
+ */
+#ifndef SS_GPU_H
+#define SS_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include "ss_status.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ss_ctx ss_ctx;
+
+/* Model shape. The reference carries only hidden/ffn (presets.cpp:8-66); the
+ * head geometry comes from the public model configs. */
+typedef struct {
+    int32_t num_layers;
+    int32_t hidden;
+    int32_t num_q_heads;  /* global */
+    int32_t num_kv_heads; /* global */
+    int32_t head_dim;
+    int32_t ffn;          /* global intermediate size */
+    int32_t vocab;
+    float rope_theta;
+    float rms_eps;
+    int32_t max_positions; /* RoPE table length (>= longest prompt + output) */
+} ss_model_cfg;
+
+/* Descriptor of one hybrid batch (E entries, T packed tokens). Entry e owns
+ * packed tokens [cu_q[e], cu_q[e+1]); token t sits at absolute position pos[t]
+ * of its request and writes its K/V to paged slot slot[t] =
+ * block_table[e][pos/bs]*bs + pos%bs. After the iteration the entry's KV
+ * length is ctx_len[e] = prefix + chunk (engine.cpp:211-216). Logits are
+ * produced for the packed rows listed in out_rows (every decode entry and every
+ * chunk that completes its prompt, core.cpp:103-134). */
+typedef struct {
+    int32_t num_entries;
+    int32_t num_tokens;
+    const int32_t* cu_q;        /* [E+1] */
+    const int32_t* ctx_len;     /* [E]   */
+    const int32_t* pos;         /* [T]   */
+    const int32_t* token_ids;   /* [T]   */
+    const int64_t* slot;        /* [T]   */
+    const int32_t* block_table; /* [E * max_blocks], -1 padded */
+    int32_t max_blocks;
+    const int32_t* out_rows;    /* [n_out] */
+    int32_t n_out;
+} ss_batch_desc;
+
+/* Creates the per-rank context on `device`: allocates and initialises this
+ * rank's weight shard from the counter-based generator (ss_synth.h), so every
+ * rank and the CPU oracle see identical values. nccl_id is the 128-byte
+ * ncclUniqueId from ss_nccl_unique_id on rank 0 (ignored when tp_size == 1). */
+ss_status ss_create(const ss_model_cfg* cfg, int32_t tp_rank, int32_t tp_size,
+                    const void* nccl_id, uint64_t weight_seed, int32_t device, ss_ctx** out);
+void ss_destroy(ss_ctx* ctx);
+ss_status ss_model_config(const ss_ctx* ctx, ss_model_cfg* out, int32_t* tp_rank, int32_t* tp_size);
+ss_status ss_nccl_unique_id(void* out_128_bytes);
+
+/* Paged KV pool: num_blocks blocks of block_size tokens for every layer and
+ * this rank's KV heads. Layout per layer: [num_blocks][kv_heads_local][bs][hd]
+ * bf16 for K and for V. */
+ss_status ss_kv_alloc(ss_ctx* ctx, int64_t num_blocks, int32_t block_size);
+
+/* Synchronous forward of one hybrid batch from HOST descriptor arrays.
+ * logits_out (nullable): [n_out][vocab] fp32. next_tokens_out (nullable):
+ * [n_out] greedy argmax. elapsed_ms (nullable): device time of the forward. */
+ss_status ss_forward_hybrid(ss_ctx* ctx, const ss_batch_desc* desc, float* logits_out,
+                            int32_t* next_tokens_out, float* elapsed_ms);
+
+/* Device-resident batches for steady-state timing: upload once, then enqueue
+ * forwards on the context stream without host synchronisation. */
+typedef struct ss_batch ss_batch;
+ss_status ss_batch_upload(ss_ctx* ctx, const ss_batch_desc* desc, ss_batch** out);
+ss_status ss_forward_enqueue(ss_ctx* ctx, const ss_batch* batch);
+/* Copies the last enqueued forward's outputs to host (synchronises). */
+ss_status ss_read_outputs(ss_ctx* ctx, const ss_batch* batch, float* logits_out,
+                          int32_t* next_tokens_out);
+void ss_batch_free(ss_ctx* ctx, ss_batch* batch);
+/* cudaStream_t of the context, for external event timing. */
+void* ss_stream(ss_ctx* ctx);
+ss_status ss_synchronize(ss_ctx* ctx);
+
+/* Fills KV positions [0, n_tokens) of one request (given its block table)
+ * with the synthetic cache values of ss_synth.h, for every layer. Used to
+ * stand up canonical batches whose decodes sit at a 4k context. */
+ss_status ss_kv_fill_synthetic(ss_ctx* ctx, const int32_t* block_table, int32_t n_blocks,
+                               int32_t request_id, int32_t n_tokens, uint64_t kv_seed);
+
+/* Per-kernel-class device time accounting (CUDA events around every launch on
+ * the context stream). Classes: see ss_kernel_class_name. */
+enum {
+    SS_K_EMBED = 0,
+    SS_K_RMSNORM = 1,
+    SS_K_GEMM_QKV = 2,
+    SS_K_ROPE_APPEND = 3,
+    SS_K_ATTN = 4,
+    SS_K_ATTN_COMBINE = 5,
+    SS_K_GEMM_O = 6,
+    SS_K_GEMM_GATEUP = 7,
+    SS_K_GEMM_DOWN = 8,
+    SS_K_ALLREDUCE = 9,
+    SS_K_LMHEAD = 10,
+    SS_K_ARGMAX = 11,
+    SS_K_NUM_CLASSES = 12
+};
+ss_status ss_set_profiling(ss_ctx* ctx, int32_t enabled);
+/* ms_out/launches_out: SS_K_NUM_CLASSES entries accumulated since reset. */
+ss_status ss_kernel_times(ss_ctx* ctx, double* ms_out, int64_t* launches_out, int32_t reset);
+const char* ss_kernel_class_name(int32_t k);
+/* Total kernel launches issued by this library on ctx since creation. */
+int64_t ss_launch_count(ss_ctx* ctx);
+
+const char* ss_last_error(ss_ctx* ctx); /* ctx may be NULL (creation errors) */
+
+/* ---- single-kernel entry points (device pointers, ctx stream) ---------------
+ * Used by the per-kernel parity tests; each is exactly the launch the fused
+ * forward makes. */
+/* K3: D[M,N] = A[M,K] . B[N,K]^T, bf16 in, fp32 accumulate (tcgen05/TMEM/TMA).
+ * epilogue: 0 store bf16 D; 1 out_f32 += D; 2 SwiGLU over 32-column
+ * gate/up interleave -> bf16 [M, N/2]; 3 store fp32 D. */
+ss_status ss_k_gemm(ss_ctx* ctx, const void* A, const void* B, void* D, int32_t M, int32_t N,
+                    int32_t K, int32_t epilogue);
+/* K4: out_bf16[M,h] = rmsnorm(x_f32[M,h]) * w_bf16[h]; rows gathered through
+ * row_idx when non-null. */
+ss_status ss_k_rmsnorm(ss_ctx* ctx, const float* x, const void* w, void* out,
+                       const int32_t* row_idx, int32_t M, int32_t h, float eps);
+/* K2 (+K4 RoPE): rope q/k of qkv[T][(nq+2nkv)*hd] in place-free fashion,
+ * q -> q_out[T][nq][hd], k/v -> paged cache of `layer` at slot[t]. Device
+ * pointers for pos/slot. */
+ss_status ss_k_rope_append(ss_ctx* ctx, const void* qkv, void* q_out, const int32_t* pos,
+                           const int64_t* slot, int32_t T, int32_t layer);
+/* K1: mixed paged attention for a device-resident batch of `layer`:
+ * q[T][nq][hd] -> o[T][nq][hd]. */
+ss_status ss_k_attention(ss_ctx* ctx, const ss_batch* batch, const void* q, void* o,
+                         int32_t layer);
+/* Reads back / writes raw KV of one layer ([num_blocks][kvh][bs][hd] bf16
+ * each for K and V) for tests. */
+ss_status ss_kv_layer_ptrs(ss_ctx* ctx, int32_t layer, void** k_ptr, void** v_ptr);
+/* Device pointer of a weight tensor of this rank's shard: name in {"wqkv",
+ * "wo", "wgu", "wdown", "attn_norm", "mlp_norm", "final_norm", "embed",
+ * "lm_head"}; layer ignored for the global ones. rows/cols describe its
+ * [rows][cols] bf16 layout. */
+ss_status ss_weight_ptr(ss_ctx* ctx, const char* name, int32_t layer, void** ptr, int64_t* rows,
+                        int64_t* cols);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SS_GPU_H */
