@@ -86,7 +86,6 @@ SS_HD uint16_t ss_synth_kv(uint64_t seed, int layer, int which, int64_t rid, int
                          1.7320508075688772f);
 }
 
-#if !defined(__CUDA_ARCH__)
 #include <math.h>
 /* Per-tensor scale: uniform[-s, s) has variance s^2/3, so s = sqrt(3/fan_in)
  * gives N(0, 1/fan_in)-matched variance; O and down projections are further
@@ -98,6 +97,14 @@ static inline float ss_weight_scale(int tensor_id, int64_t fan_in, int num_layer
     return (float)s;
 }
 static inline float ss_embed_scale(void) { return 1.7320508075688772f; }
-#endif
+/* RoPE (rotate-half, HF Llama convention) table entry for position p and
+ * pair index i < hd/2: angle = p * theta^(-2i/hd), evaluated in double and
+ * rounded once; the GPU path and the oracle share these exact values. */
+static inline void ss_rope_cs(double theta, int hd, int64_t p, int i, float* c, float* s) {
+    const double inv = pow(theta, -2.0 * (double)i / (double)hd);
+    const double a = (double)p * inv;
+    *c = (float)cos(a);
+    *s = (float)sin(a);
+}
 
 #endif /* SS_SYNTH_H */

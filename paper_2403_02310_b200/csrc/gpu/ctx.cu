@@ -1,0 +1,914 @@
+// The ss_gpu.h C ABI: per-rank context (weights, paged KV pool, workspaces,
+// NCCL communicator) and the hybrid-batch forward that replaces the
+// reference's iteration_time() model step (reference costmodel.cpp:39-56,
+// called at engine.cpp:227).
+//
+// Per layer, on one stream (T packed tokens, this rank's head/column shard):
+//   rmsnorm(x) -> xn                                   K4
+//   GEMM xn . Wqkv^T -> qkv                            K3 (tcgen05)
+//   RoPE(q,k) ; append k,v to paged blocks at slot[t] K2 (+K4)
+//   mixed paged attention (+ split-KV combine)        K1
+//   GEMM o . Wo^T, fused residual add                  K3 (+ NCCL all-reduce when tp > 1)
+//   rmsnorm(x) -> xn                                   K4
+//   GEMM xn . Wgu^T, fused SiLU(gate) * up             K3
+//   GEMM act . Wdown^T, fused residual add             K3 (+ NCCL all-reduce when tp > 1)
+// then final norm + LM head on the logit rows only, vocab all-gather, argmax.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../../include/ss_gpu.h"
+#include "../../../include/ss_synth.h"
+#include "common.cuh"
+#include "kernels.cuh"
+
+#define SS_API extern "C" __attribute__((visibility("default")))
+
+using namespace ssk;
+using bf16 = __nv_bfloat16;
+
+namespace {
+
+thread_local std::string g_create_err;
+
+// ---------------------------------------------------------------- NCCL (dlopen)
+struct Nccl {
+    void* h = nullptr;
+    ncclResult_t (*get_id)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                               cudaStream_t) = nullptr;
+    ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*destroy)(ncclComm_t) = nullptr;
+    const char* (*err)(ncclResult_t) = nullptr;
+    bool load(std::string& why) {
+        if (h) return true;
+        // Prefer an NCCL already mapped into the process (torch's), else the system one.
+        h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+        if (!h) {
+            why = std::string("cannot dlopen libnccl.so.2: ") + dlerror();
+            return false;
+        }
+        get_id = reinterpret_cast<decltype(get_id)>(dlsym(h, "ncclGetUniqueId"));
+        init_rank = reinterpret_cast<decltype(init_rank)>(dlsym(h, "ncclCommInitRank"));
+        all_reduce = reinterpret_cast<decltype(all_reduce)>(dlsym(h, "ncclAllReduce"));
+        all_gather = reinterpret_cast<decltype(all_gather)>(dlsym(h, "ncclAllGather"));
+        destroy = reinterpret_cast<decltype(destroy)>(dlsym(h, "ncclCommDestroy"));
+        err = reinterpret_cast<decltype(err)>(dlsym(h, "ncclGetErrorString"));
+        if (!get_id || !init_rank || !all_reduce || !all_gather || !destroy || !err) {
+            why = "libnccl.so.2 lacks required symbols";
+            return false;
+        }
+        return true;
+    }
+};
+Nccl g_nccl;
+
+struct Layer {
+    bf16 *wqkv, *wo, *wgu, *wdown, *attn_norm, *mlp_norm;
+    CUtensorMap tb_qkv[2], tb_o[2], tb_gu[2], tb_down[2];  // B maps for BN = 128, 256
+};
+
+struct Prof {
+    int cls;
+    cudaEvent_t a, b;
+};
+
+}  // namespace
+
+struct ss_batch {
+    int E = 0, T = 0, n_out = 0, max_blocks = 0;
+    size_t dev_cap = 0;
+    uint8_t* dev = nullptr;  // one allocation, sub-arrays below
+    int32_t *cu_q = nullptr, *ctx_len = nullptr, *pos = nullptr, *tokens = nullptr, *bt = nullptr,
+            *out_rows = nullptr;
+    int64_t* slot = nullptr;
+    AttnItem* items = nullptr;
+    AttnCombine* combs = nullptr;
+    int n_items = 0, n_combs = 0, part_rows = 0;
+};
+
+struct ss_ctx {
+    ss_model_cfg cfg{};
+    int rank = 0, tp = 1, device = 0, num_sms = 148;
+    uint64_t seed = 0;
+    int h = 0, L = 0, hd = 0, nq_l = 0, nkv_l = 0, G = 1, ffn_l = 0, vocab_l = 0;
+    cudaStream_t st = nullptr;
+    std::string err;
+
+    uint8_t* wmem = nullptr;
+    std::vector<Layer> layers;
+    bf16 *embed = nullptr, *lm_head = nullptr, *final_norm = nullptr;
+    CUtensorMap tb_lm[2];
+    float2* rope = nullptr;
+
+    bf16 *kc = nullptr, *vc = nullptr;
+    int64_t nblocks = 0, layer_stride = 0;
+    int bs = 16;
+
+    // workspaces, capacity T_cap tokens / O_cap logit rows / P_cap partial rows
+    int T_cap = 0, O_cap = 0, P_cap = 0;
+    float* x = nullptr;
+    bf16 *xn = nullptr, *qkv = nullptr, *q = nullptr, *o = nullptr, *act = nullptr, *part = nullptr, *xo = nullptr;
+    float *logits_l = nullptr, *logits_g = nullptr, *logits = nullptr;
+    int32_t* next_tok = nullptr;
+    float *part_o = nullptr, *part_ml = nullptr;
+    CUtensorMap ta_xn, ta_o, ta_act, ta_xo;
+
+    uint8_t* pinned = nullptr;
+    size_t pinned_cap = 0;
+    ss_batch scratch;  // batch buffers reused by ss_forward_hybrid
+    const ss_batch* last = nullptr;
+
+    ncclComm_t comm = nullptr;
+
+    bool prof = false;
+    std::vector<Prof> pend;
+    std::vector<cudaEvent_t> free_ev;
+    double ms[SS_K_NUM_CLASSES] = {};
+    int64_t launches[SS_K_NUM_CLASSES] = {};
+    int64_t total_launches = 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+namespace {
+
+ss_status fail(ss_ctx* c, ss_status s, const std::string& msg) {
+    if (c) c->err = msg;
+    else g_create_err = msg;
+    return s;
+}
+
+#define CK(call)                                                                                    \
+    do {                                                                                            \
+        cudaError_t e_ = (call);                                                                    \
+        if (e_ != cudaSuccess)                                                                      \
+            return fail(ctx, e_ == cudaErrorMemoryAllocation ? SS_OUT_OF_MEMORY : SS_CUDA_ERROR,    \
+                        std::string(#call) + ": " + cudaGetErrorString(e_));                        \
+    } while (0)
+
+#define NK(call)                                                                                    \
+    do {                                                                                            \
+        ncclResult_t r_ = (call);                                                                   \
+        if (r_ != ncclSuccess) return fail(ctx, SS_NCCL_ERROR, std::string(#call) + ": " + g_nccl.err(r_)); \
+    } while (0)
+
+cudaEvent_t get_ev(ss_ctx* c) {
+    if (!c->free_ev.empty()) {
+        cudaEvent_t e = c->free_ev.back();
+        c->free_ev.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+// Runs one launch (or a short fixed group) with optional per-class timing.
+template <class F>
+ss_status launch(ss_ctx* ctx, int cls, int nkernels, F&& f) {
+    cudaEvent_t a = nullptr, b = nullptr;
+    if (ctx->prof) {
+        a = get_ev(ctx);
+        b = get_ev(ctx);
+        cudaEventRecord(a, ctx->st);
+    }
+    cudaError_t e = f();
+    if (e != cudaSuccess)
+        return fail(ctx, SS_CUDA_ERROR, std::string("kernel launch (") + ss_kernel_class_name(cls) +
+                                            "): " + cudaGetErrorString(e));
+    if (ctx->prof) {
+        cudaEventRecord(b, ctx->st);
+        ctx->pend.push_back(Prof{cls, a, b});
+    }
+    ctx->launches[cls] += nkernels;
+    ctx->total_launches += nkernels;
+    return SS_OK;
+}
+
+template <class T>
+T* carve(uint8_t*& p, size_t n) {
+    T* r = reinterpret_cast<T*>(p);
+    p += (n * sizeof(T) + 255) & ~size_t(255);
+    return r;
+}
+
+ss_status init_weight(ss_ctx* ctx, bf16* w, int kind, int layer, int64_t rows, int64_t cols, float sa, float sb,
+                      float sc) {
+    WeightInit wi{};
+    wi.kind = kind;
+    wi.layer = layer;
+    wi.rank = ctx->rank;
+    wi.rows = rows;
+    wi.cols = cols;
+    wi.nq_l = ctx->nq_l;
+    wi.nkv_l = ctx->nkv_l;
+    wi.hd = ctx->hd;
+    wi.ffn_l = ctx->ffn_l;
+    wi.vocab_l = ctx->vocab_l;
+    wi.seed = ctx->seed;
+    wi.scale_a = sa;
+    wi.scale_b = sb;
+    wi.scale_c = sc;
+    return init_weight_launch(w, wi, ctx->st) == cudaSuccess ? SS_OK : fail(ctx, SS_CUDA_ERROR, "weight init launch");
+}
+
+bool bmaps(CUtensorMap (&m)[2], const bf16* w, int64_t rows, int64_t cols) {
+    return make_tmap_2d(&m[0], w, uint64_t(rows), uint64_t(cols), 128, 64) &&
+           make_tmap_2d(&m[1], w, uint64_t(rows), uint64_t(cols), 256, 64);
+}
+
+ss_status ensure_workspace(ss_ctx* ctx, int T, int n_out, int part_rows) {
+    if (T > ctx->T_cap) {
+        const int cap = std::max(T, std::max(2 * ctx->T_cap, 64));
+        cudaFree(ctx->x);
+        cudaFree(ctx->xn);
+        cudaFree(ctx->qkv);
+        cudaFree(ctx->q);
+        cudaFree(ctx->o);
+        cudaFree(ctx->act);
+        cudaFree(ctx->part);
+        const size_t h = size_t(ctx->h), qd = size_t(ctx->nq_l) * ctx->hd;
+        const size_t qkvd = size_t(ctx->nq_l + 2 * ctx->nkv_l) * ctx->hd;
+        CK(cudaMalloc(&ctx->x, size_t(cap) * h * 4));
+        CK(cudaMalloc(&ctx->xn, size_t(cap) * h * 2));
+        CK(cudaMalloc(&ctx->qkv, size_t(cap) * qkvd * 2));
+        CK(cudaMalloc(&ctx->q, size_t(cap) * qd * 2));
+        CK(cudaMalloc(&ctx->o, size_t(cap) * qd * 2));
+        CK(cudaMalloc(&ctx->act, size_t(cap) * ctx->ffn_l * 2));
+        CK(cudaMalloc(&ctx->part, size_t(cap) * h * 2));
+        ctx->T_cap = cap;
+        if (!make_tmap_2d(&ctx->ta_xn, ctx->xn, cap, h, 128, 64) ||
+            !make_tmap_2d(&ctx->ta_o, ctx->o, cap, qd, 128, 64) ||
+            !make_tmap_2d(&ctx->ta_act, ctx->act, cap, ctx->ffn_l, 128, 64))
+            return fail(ctx, SS_CUDA_ERROR, "cuTensorMapEncodeTiled failed (activation maps)");
+    }
+    if (n_out > ctx->O_cap) {
+        const int cap = std::max(n_out, std::max(2 * ctx->O_cap, 64));
+        cudaFree(ctx->xo);
+        cudaFree(ctx->logits_l);
+        cudaFree(ctx->logits_g);
+        cudaFree(ctx->logits);
+        cudaFree(ctx->next_tok);
+        CK(cudaMalloc(&ctx->xo, size_t(cap) * ctx->h * 2));
+        CK(cudaMalloc(&ctx->logits_l, size_t(cap) * ctx->vocab_l * 4));
+        if (ctx->tp > 1) {
+            CK(cudaMalloc(&ctx->logits_g, size_t(cap) * ctx->vocab_l * ctx->tp * 4));
+            CK(cudaMalloc(&ctx->logits, size_t(cap) * ctx->cfg.vocab * 4));
+        }
+        CK(cudaMalloc(&ctx->next_tok, size_t(cap) * 4));
+        ctx->O_cap = cap;
+        if (!make_tmap_2d(&ctx->ta_xo, ctx->xo, cap, ctx->h, 128, 64))
+            return fail(ctx, SS_CUDA_ERROR, "cuTensorMapEncodeTiled failed (logit rows)");
+    }
+    if (part_rows > ctx->P_cap) {
+        const int cap = std::max(part_rows, 2 * ctx->P_cap);
+        cudaFree(ctx->part_o);
+        cudaFree(ctx->part_ml);
+        CK(cudaMalloc(&ctx->part_o, size_t(cap) * ctx->hd * 4));
+        CK(cudaMalloc(&ctx->part_ml, size_t(cap) * 2 * 4));
+        ctx->P_cap = cap;
+    }
+    return SS_OK;
+}
+
+// Work list of the mixed attention launch (see attention.cu).
+void build_items(const ss_ctx* ctx, const ss_batch_desc* d, std::vector<AttnItem>& items,
+                 std::vector<AttnCombine>& combs, int& part_rows) {
+    const int G = ctx->G;
+    struct Tile {
+        int e, row0, nr, extent;
+    };
+    std::vector<Tile> tiles;
+    int prefill_items = 0;
+    for (int e = 0; e < d->num_entries; ++e) {
+        const int ntok = d->cu_q[e + 1] - d->cu_q[e];
+        const int prefix = d->ctx_len[e] - ntok;
+        const int rows = ntok * G;
+        for (int row0 = 0; row0 < rows; row0 += 64) {
+            const int nr = std::min(64, rows - row0);
+            tiles.push_back(Tile{e, row0, nr, prefix + (row0 + nr - 1) / G + 1});
+            if (nr > 16) prefill_items += ctx->nkv_l;
+        }
+    }
+    const int long_split = prefill_items < ctx->num_sms ? 2048 : (1 << 30);
+    part_rows = 0;
+    for (const Tile& t : tiles) {
+        const int split = t.nr <= 16 ? 512 : long_split;
+        const int ns = (t.extent + split - 1) / split;
+        for (int h = 0; h < ctx->nkv_l; ++h) {
+            if (ns <= 1) {
+                items.push_back(AttnItem{t.e, h, t.row0, t.nr, 0, t.extent, -1, 0});
+                continue;
+            }
+            const int base = part_rows;
+            for (int s = 0; s < ns; ++s)
+                items.push_back(AttnItem{t.e, h, t.row0, t.nr, s * split, std::min(t.extent, (s + 1) * split),
+                                         base + s * t.nr, 0});
+            combs.push_back(AttnCombine{t.e, h, t.row0, t.nr, ns, base, t.nr, 0});
+            part_rows += ns * t.nr;
+        }
+    }
+    // longest items first so the tail of the launch is short
+    std::stable_sort(items.begin(), items.end(), [](const AttnItem& a, const AttnItem& b) {
+        const long ca = long(a.key1 - a.key0) * (a.nrows <= 16 ? 16 : 64);
+        const long cb = long(b.key1 - b.key0) * (b.nrows <= 16 ? 16 : 64);
+        return ca > cb;
+    });
+}
+
+ss_status validate(ss_ctx* ctx, const ss_batch_desc* d) {
+    if (!d || d->num_entries < 1 || d->num_tokens < 1 || !d->cu_q || !d->ctx_len || !d->pos || !d->token_ids ||
+        !d->slot || !d->block_table || d->max_blocks < 1 || d->n_out < 0 || (d->n_out > 0 && !d->out_rows))
+        return fail(ctx, SS_INVALID_ARG, "malformed batch descriptor");
+    if (d->cu_q[0] != 0 || d->cu_q[d->num_entries] != d->num_tokens)
+        return fail(ctx, SS_INVALID_ARG, "cu_q must start at 0 and end at num_tokens");
+    if (ctx->nblocks == 0) return fail(ctx, SS_INVALID_ARG, "KV pool not allocated (ss_kv_alloc)");
+    for (int e = 0; e < d->num_entries; ++e) {
+        const int n = d->cu_q[e + 1] - d->cu_q[e];
+        if (n < 1 || d->ctx_len[e] < n) return fail(ctx, SS_INVALID_ARG, "entry with no tokens or ctx < tokens");
+        if (d->ctx_len[e] > int64_t(d->max_blocks) * ctx->bs || d->ctx_len[e] > ctx->cfg.max_positions)
+            return fail(ctx, SS_INVALID_ARG, "context longer than block table / RoPE table");
+        const int nb = (d->ctx_len[e] + ctx->bs - 1) / ctx->bs;
+        for (int b = 0; b < nb; ++b) {
+            const int32_t id = d->block_table[size_t(e) * d->max_blocks + b];
+            if (id < 0 || id >= ctx->nblocks)
+                return fail(ctx, SS_OUT_OF_KV, "block id " + std::to_string(id) + " outside the KV pool of " +
+                                                   std::to_string(ctx->nblocks) + " blocks");
+        }
+        for (int t = d->cu_q[e]; t < d->cu_q[e + 1]; ++t) {
+            const int p = d->pos[t];
+            if (p != d->ctx_len[e] - n + (t - d->cu_q[e]))
+                return fail(ctx, SS_INVALID_ARG, "positions must be prefix .. prefix+chunk-1 per entry");
+            const int64_t want = int64_t(d->block_table[size_t(e) * d->max_blocks + p / ctx->bs]) * ctx->bs + p % ctx->bs;
+            if (d->slot[t] != want) return fail(ctx, SS_INVALID_ARG, "slot disagrees with the block table");
+            if (d->token_ids[t] < 0 || d->token_ids[t] >= ctx->cfg.vocab)
+                return fail(ctx, SS_INVALID_ARG, "token id outside the vocabulary");
+        }
+    }
+    for (int i = 0; i < d->n_out; ++i)
+        if (d->out_rows[i] < 0 || d->out_rows[i] >= d->num_tokens) return fail(ctx, SS_INVALID_ARG, "bad out_rows");
+    return SS_OK;
+}
+
+ss_status upload(ss_ctx* ctx, const ss_batch_desc* d, ss_batch* b) {
+    if (ss_status s = validate(ctx, d)) return s;
+    std::vector<AttnItem> items;
+    std::vector<AttnCombine> combs;
+    int part_rows = 0;
+    build_items(ctx, d, items, combs, part_rows);
+    const int E = d->num_entries, T = d->num_tokens;
+    struct Seg {
+        const void* src;
+        size_t bytes;
+    };
+    const Seg segs[] = {
+        {d->cu_q, size_t(E + 1) * 4},        {d->ctx_len, size_t(E) * 4},   {d->pos, size_t(T) * 4},
+        {d->token_ids, size_t(T) * 4},       {d->block_table, size_t(E) * d->max_blocks * 4},
+        {d->out_rows, size_t(d->n_out) * 4}, {d->slot, size_t(T) * 8},
+        {items.data(), items.size() * sizeof(AttnItem)}, {combs.data(), combs.size() * sizeof(AttnCombine)},
+    };
+    size_t total = 0;
+    for (const Seg& s : segs) total += (s.bytes + 255) & ~size_t(255);
+    if (total > ctx->pinned_cap) {
+        cudaFreeHost(ctx->pinned);
+        ctx->pinned = nullptr;
+        CK(cudaMallocHost(&ctx->pinned, total * 2));
+        ctx->pinned_cap = total * 2;
+    }
+    if (total > b->dev_cap) {
+        cudaFree(b->dev);
+        b->dev = nullptr;
+        CK(cudaMalloc(&b->dev, total * 2));
+        b->dev_cap = total * 2;
+    }
+    // previous users of the pinned staging buffer must be done before overwrite
+    CK(cudaStreamSynchronize(ctx->st));
+    size_t off = 0;
+    uint8_t* dptrs[9];
+    for (int i = 0; i < 9; ++i) {
+        if (segs[i].bytes) std::memcpy(ctx->pinned + off, segs[i].src, segs[i].bytes);
+        dptrs[i] = b->dev + off;
+        off += (segs[i].bytes + 255) & ~size_t(255);
+    }
+    CK(cudaMemcpyAsync(b->dev, ctx->pinned, total, cudaMemcpyHostToDevice, ctx->st));
+    b->cu_q = reinterpret_cast<int32_t*>(dptrs[0]);
+    b->ctx_len = reinterpret_cast<int32_t*>(dptrs[1]);
+    b->pos = reinterpret_cast<int32_t*>(dptrs[2]);
+    b->tokens = reinterpret_cast<int32_t*>(dptrs[3]);
+    b->bt = reinterpret_cast<int32_t*>(dptrs[4]);
+    b->out_rows = reinterpret_cast<int32_t*>(dptrs[5]);
+    b->slot = reinterpret_cast<int64_t*>(dptrs[6]);
+    b->items = reinterpret_cast<AttnItem*>(dptrs[7]);
+    b->combs = reinterpret_cast<AttnCombine*>(dptrs[8]);
+    b->E = E;
+    b->T = T;
+    b->n_out = d->n_out;
+    b->max_blocks = d->max_blocks;
+    b->n_items = int(items.size());
+    b->n_combs = int(combs.size());
+    b->part_rows = part_rows;
+    return ensure_workspace(ctx, T, std::max(d->n_out, 1), part_rows);
+}
+
+AttnParams attn_params(const ss_ctx* ctx, const ss_batch* b, const bf16* q, bf16* o, int layer) {
+    AttnParams p{};
+    p.q = q;
+    p.o = o;
+    p.kc = ctx->kc + size_t(layer) * ctx->layer_stride;
+    p.vc = ctx->vc + size_t(layer) * ctx->layer_stride;
+    p.cu_q = b->cu_q;
+    p.ctx_len = b->ctx_len;
+    p.block_table = b->bt;
+    p.max_blocks = b->max_blocks;
+    p.items = b->items;
+    p.n_items = b->n_items;
+    p.part_o = ctx->part_o;
+    p.part_ml = ctx->part_ml;
+    p.combines = b->combs;
+    p.n_combines = b->n_combs;
+    p.nq_l = ctx->nq_l;
+    p.nkv_l = ctx->nkv_l;
+    p.group = ctx->G;
+    p.head_dim = ctx->hd;
+    p.block_size = ctx->bs;
+    p.scale_log2 = float(1.0 / std::sqrt(double(ctx->hd)) * 1.4426950408889634);
+    return p;
+}
+
+ss_status gemm(ss_ctx* ctx, int cls, const CUtensorMap& ta, const CUtensorMap (&tb)[2], int M, int N, int K,
+               void* out, int ldo, int epi) {
+    GemmPlan p;
+    p.M = M;
+    p.N = N;
+    p.K = K;
+    p.out = out;
+    p.ldo = ldo;
+    p.epi = epi;
+    p.num_sms = ctx->num_sms;
+    p.bn = gemm_pick_bn(M, N, ctx->num_sms);
+    if (epi == EPI_SWIGLU && p.bn % 64) p.bn = 256;
+    p.tmA = ta;
+    p.tmB = tb[p.bn == 256 ? 1 : 0];
+    return launch(ctx, cls, 1, [&] { return gemm_launch(p, ctx->st); });
+}
+
+ss_status allreduce_bf16(ss_ctx* ctx, bf16* buf, size_t n) {
+    return launch(ctx, SS_K_ALLREDUCE, 1, [&]() -> cudaError_t {
+        return g_nccl.all_reduce(buf, buf, n, ncclBfloat16, ncclSum, ctx->comm, ctx->st) == ncclSuccess
+                   ? cudaSuccess
+                   : cudaErrorUnknown;
+    });
+}
+
+ss_status enqueue_forward(ss_ctx* ctx, const ss_batch* b) {
+    const int T = b->T, h = ctx->h;
+    const int qkvN = (ctx->nq_l + 2 * ctx->nkv_l) * ctx->hd, qd = ctx->nq_l * ctx->hd;
+    const float eps = ctx->cfg.rms_eps;
+    ss_status s;
+#define RUN(x)                 \
+    if ((s = (x)) != SS_OK) \
+        return s;
+    RUN(launch(ctx, SS_K_EMBED, 1, [&] { return embed_launch(b->tokens, ctx->embed, ctx->x, T, h, ctx->st); }));
+    for (int l = 0; l < ctx->L; ++l) {
+        const Layer& W = ctx->layers[size_t(l)];
+        RUN(launch(ctx, SS_K_RMSNORM, 1,
+                   [&] { return rmsnorm_launch(ctx->x, W.attn_norm, ctx->xn, nullptr, T, h, eps, ctx->st); }));
+        RUN(gemm(ctx, SS_K_GEMM_QKV, ctx->ta_xn, W.tb_qkv, T, qkvN, h, ctx->qkv, qkvN, EPI_BF16));
+        RUN(launch(ctx, SS_K_ROPE_APPEND, 1, [&] {
+            return rope_append_launch(ctx->qkv, ctx->q, b->pos, b->slot, ctx->rope, T, ctx->nq_l, ctx->nkv_l, ctx->hd,
+                                      ctx->bs, ctx->kc + size_t(l) * ctx->layer_stride,
+                                      ctx->vc + size_t(l) * ctx->layer_stride, ctx->st);
+        }));
+        const AttnParams ap = attn_params(ctx, b, ctx->q, ctx->o, l);
+        RUN(launch(ctx, SS_K_ATTN, 1, [&] { return attention_launch(ap, ctx->st); }));
+        if (b->n_combs) RUN(launch(ctx, SS_K_ATTN_COMBINE, 1, [&] { return attention_combine_launch(ap, ctx->st); }));
+        if (ctx->tp == 1) {
+            RUN(gemm(ctx, SS_K_GEMM_O, ctx->ta_o, W.tb_o, T, h, qd, ctx->x, h, EPI_RESADD));
+        } else {
+            RUN(gemm(ctx, SS_K_GEMM_O, ctx->ta_o, W.tb_o, T, h, qd, ctx->part, h, EPI_BF16));
+            RUN(allreduce_bf16(ctx, ctx->part, size_t(T) * h));
+            RUN(launch(ctx, SS_K_ALLREDUCE, 1,
+                       [&] { return residual_add_launch(ctx->x, ctx->part, int64_t(T) * h, ctx->st); }));
+        }
+        RUN(launch(ctx, SS_K_RMSNORM, 1,
+                   [&] { return rmsnorm_launch(ctx->x, W.mlp_norm, ctx->xn, nullptr, T, h, eps, ctx->st); }));
+        RUN(gemm(ctx, SS_K_GEMM_GATEUP, ctx->ta_xn, W.tb_gu, T, 2 * ctx->ffn_l, h, ctx->act, ctx->ffn_l, EPI_SWIGLU));
+        if (ctx->tp == 1) {
+            RUN(gemm(ctx, SS_K_GEMM_DOWN, ctx->ta_act, W.tb_down, T, h, ctx->ffn_l, ctx->x, h, EPI_RESADD));
+        } else {
+            RUN(gemm(ctx, SS_K_GEMM_DOWN, ctx->ta_act, W.tb_down, T, h, ctx->ffn_l, ctx->part, h, EPI_BF16));
+            RUN(allreduce_bf16(ctx, ctx->part, size_t(T) * h));
+            RUN(launch(ctx, SS_K_ALLREDUCE, 1,
+                       [&] { return residual_add_launch(ctx->x, ctx->part, int64_t(T) * h, ctx->st); }));
+        }
+    }
+    if (b->n_out > 0) {
+        RUN(launch(ctx, SS_K_RMSNORM, 1, [&] {
+            return rmsnorm_launch(ctx->x, ctx->final_norm, ctx->xo, b->out_rows, b->n_out, h, eps, ctx->st);
+        }));
+        RUN(gemm(ctx, SS_K_LMHEAD, ctx->ta_xo, ctx->tb_lm, b->n_out, ctx->vocab_l, h, ctx->logits_l, ctx->vocab_l,
+                 EPI_F32));
+        const float* full = ctx->logits_l;
+        if (ctx->tp > 1) {
+            RUN(launch(ctx, SS_K_ALLREDUCE, 1, [&]() -> cudaError_t {
+                return g_nccl.all_gather(ctx->logits_l, ctx->logits_g, size_t(b->n_out) * ctx->vocab_l, ncclFloat32,
+                                         ctx->comm, ctx->st) == ncclSuccess
+                           ? cudaSuccess
+                           : cudaErrorUnknown;
+            }));
+            RUN(launch(ctx, SS_K_ARGMAX, 1, [&] {
+                return gather_vocab_launch(ctx->logits_g, ctx->logits, ctx->tp, b->n_out, ctx->vocab_l, ctx->st);
+            }));
+            full = ctx->logits;
+        }
+        RUN(launch(ctx, SS_K_ARGMAX, 1, [&] {
+            return argmax_launch(full, b->n_out, ctx->cfg.vocab, ctx->cfg.vocab, ctx->next_tok, ctx->st);
+        }));
+    }
+#undef RUN
+    ctx->last = b;
+    return SS_OK;
+}
+
+ss_status read_outputs(ss_ctx* ctx, const ss_batch* b, float* logits, int32_t* next) {
+    if (b->n_out == 0) return SS_OK;
+    const float* full = ctx->tp > 1 ? ctx->logits : ctx->logits_l;
+    if (logits)
+        CK(cudaMemcpyAsync(logits, full, size_t(b->n_out) * ctx->cfg.vocab * 4, cudaMemcpyDeviceToHost, ctx->st));
+    if (next) CK(cudaMemcpyAsync(next, ctx->next_tok, size_t(b->n_out) * 4, cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    return SS_OK;
+}
+
+void collect_prof(ss_ctx* ctx) {
+    for (const Prof& p : ctx->pend) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) ctx->ms[p.cls] += ms;
+        ctx->free_ev.push_back(p.a);
+        ctx->free_ev.push_back(p.b);
+    }
+    ctx->pend.clear();
+}
+
+}  // namespace
+
+// ============================================================================ C ABI
+
+SS_API const char* ss_kernel_class_name(int32_t k) {
+    static const char* names[SS_K_NUM_CLASSES] = {"embed",   "rmsnorm", "gemm_qkv",    "rope_kv_append",
+                                                  "attention", "attn_combine", "gemm_o", "gemm_gate_up",
+                                                  "gemm_down", "nccl_allreduce", "lm_head", "argmax"};
+    return (k >= 0 && k < SS_K_NUM_CLASSES) ? names[k] : "unknown";
+}
+
+SS_API const char* ss_last_error(ss_ctx* ctx) { return ctx ? ctx->err.c_str() : g_create_err.c_str(); }
+
+SS_API ss_status ss_nccl_unique_id(void* out) {
+    ss_ctx* ctx = nullptr;
+    std::string why;
+    if (!g_nccl.load(why)) return fail(ctx, SS_NCCL_ERROR, why);
+    ncclUniqueId id;
+    NK(g_nccl.get_id(&id));
+    std::memcpy(out, &id, sizeof(id));
+    return SS_OK;
+}
+
+SS_API ss_status ss_create(const ss_model_cfg* cfg, int32_t tp_rank, int32_t tp_size, const void* nccl_id,
+                           uint64_t weight_seed, int32_t device, ss_ctx** out) {
+    ss_ctx* ctx = nullptr;
+    if (!cfg || !out) return fail(ctx, SS_INVALID_ARG, "null argument");
+    const ss_model_cfg& c = *cfg;
+    if (tp_size < 1 || tp_rank < 0 || tp_rank >= tp_size) return fail(ctx, SS_INVALID_ARG, "bad tp rank/size");
+    if (c.num_layers < 1 || c.hidden % 64 || c.num_q_heads % tp_size || c.num_kv_heads % tp_size ||
+        c.num_q_heads % c.num_kv_heads || (c.head_dim != 64 && c.head_dim != 128) || c.ffn % (32 * tp_size) ||
+        c.vocab % tp_size || (c.vocab / tp_size) % 32 || c.max_positions < 1)
+        return fail(ctx, SS_INVALID_ARG,
+                    "unsupported model shape (need hidden%64, heads%tp, hd in {64,128}, ffn%(32tp), vocab/tp%32)");
+    if ((c.ffn / tp_size) % 64)
+        return fail(ctx, SS_INVALID_ARG, "ffn shard must be a multiple of 64 (K tiling of the down projection)");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(ctx, SS_CUDA_ERROR, "no CUDA device visible: this library has no CPU fallback");
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return fail(ctx, SS_CUDA_ERROR, "bad device");
+    if (prop.major != 10) return fail(ctx, SS_CUDA_ERROR, "needs an sm_100 (B200) device");
+
+    ctx = new ss_ctx();
+    ctx->cfg = c;
+    ctx->rank = tp_rank;
+    ctx->tp = tp_size;
+    ctx->device = device;
+    ctx->num_sms = prop.multiProcessorCount;
+    ctx->h = c.hidden;
+    ctx->L = c.num_layers;
+    ctx->hd = c.head_dim;
+    ctx->nq_l = c.num_q_heads / tp_size;
+    ctx->nkv_l = c.num_kv_heads / tp_size;
+    ctx->G = ctx->nq_l / ctx->nkv_l;
+    ctx->ffn_l = c.ffn / tp_size;
+    ctx->vocab_l = c.vocab / tp_size;
+    ctx->seed = weight_seed;
+    auto bail = [&](ss_status s) {
+        std::string m = ctx->err;
+        ss_destroy(ctx);
+        g_create_err = m;
+        return s;
+    };
+    if (cudaSetDevice(device) != cudaSuccess) return bail(fail(ctx, SS_CUDA_ERROR, "cudaSetDevice"));
+    if (cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking) != cudaSuccess)
+        return bail(fail(ctx, SS_CUDA_ERROR, "stream create"));
+    cudaEventCreate(&ctx->ev0);
+    cudaEventCreate(&ctx->ev1);
+
+    // ---- weights: one allocation
+    const int64_t h = c.hidden, hd = c.head_dim;
+    const int64_t qkv_rows = int64_t(ctx->nq_l + 2 * ctx->nkv_l) * hd, qd = int64_t(ctx->nq_l) * hd;
+    const int64_t per_layer = qkv_rows * h + h * qd + 2 * int64_t(ctx->ffn_l) * h + h * ctx->ffn_l + 2 * h;
+    size_t bytes = size_t(per_layer + 256 * 6) * 2 * size_t(c.num_layers) +
+                   size_t(int64_t(c.vocab) * h + int64_t(ctx->vocab_l) * h + h) * 2 + 4096;
+    if (cudaMalloc(&ctx->wmem, bytes) != cudaSuccess) return bail(fail(ctx, SS_OUT_OF_MEMORY, "weights allocation"));
+    uint8_t* p = ctx->wmem;
+    ctx->layers.resize(size_t(c.num_layers));
+    const float s_qkv = ss_weight_scale(SS_T_Q, h, c.num_layers);
+    const float s_o = ss_weight_scale(SS_T_O, int64_t(c.num_q_heads) * hd, c.num_layers);
+    const float s_gu = ss_weight_scale(SS_T_GATE, h, c.num_layers);
+    const float s_dn = ss_weight_scale(SS_T_DOWN, c.ffn, c.num_layers);
+    for (int l = 0; l < c.num_layers; ++l) {
+        Layer& W = ctx->layers[size_t(l)];
+        W.wqkv = carve<bf16>(p, size_t(qkv_rows * h));
+        W.wo = carve<bf16>(p, size_t(h * qd));
+        W.wgu = carve<bf16>(p, size_t(2 * ctx->ffn_l * h));
+        W.wdown = carve<bf16>(p, size_t(h * ctx->ffn_l));
+        W.attn_norm = carve<bf16>(p, size_t(h));
+        W.mlp_norm = carve<bf16>(p, size_t(h));
+        ss_status s;
+        if ((s = init_weight(ctx, W.wqkv, W_QKV, l, qkv_rows, h, s_qkv, s_qkv, s_qkv)) ||
+            (s = init_weight(ctx, W.wo, W_O, l, h, qd, s_o, s_o, s_o)) ||
+            (s = init_weight(ctx, W.wgu, W_GU, l, 2 * ctx->ffn_l, h, s_gu, s_gu, s_gu)) ||
+            (s = init_weight(ctx, W.wdown, W_DOWN, l, h, ctx->ffn_l, s_dn, s_dn, s_dn)) ||
+            (s = init_weight(ctx, W.attn_norm, W_ONES, l, 1, h, 1, 1, 1)) ||
+            (s = init_weight(ctx, W.mlp_norm, W_ONES, l, 1, h, 1, 1, 1)))
+            return bail(s);
+        if (!bmaps(W.tb_qkv, W.wqkv, qkv_rows, h) || !bmaps(W.tb_o, W.wo, h, qd) ||
+            !bmaps(W.tb_gu, W.wgu, 2 * ctx->ffn_l, h) || !bmaps(W.tb_down, W.wdown, h, ctx->ffn_l))
+            return bail(fail(ctx, SS_CUDA_ERROR, "cuTensorMapEncodeTiled failed (weights)"));
+    }
+    ctx->embed = carve<bf16>(p, size_t(int64_t(c.vocab) * h));
+    ctx->lm_head = carve<bf16>(p, size_t(int64_t(ctx->vocab_l) * h));
+    ctx->final_norm = carve<bf16>(p, size_t(h));
+    {
+        ss_status s;
+        if ((s = init_weight(ctx, ctx->embed, W_EMBED, 0, c.vocab, h, ss_embed_scale(), 0, 0)) ||
+            (s = init_weight(ctx, ctx->lm_head, W_LMHEAD, 0, ctx->vocab_l, h, ss_weight_scale(-1, h, c.num_layers), 0,
+                             0)) ||
+            (s = init_weight(ctx, ctx->final_norm, W_ONES, 0, 1, h, 1, 1, 1)))
+            return bail(s);
+        if (!bmaps(ctx->tb_lm, ctx->lm_head, ctx->vocab_l, h))
+            return bail(fail(ctx, SS_CUDA_ERROR, "cuTensorMapEncodeTiled failed (lm head)"));
+    }
+    // ---- RoPE table (host, double precision; shared with the oracle via ss_synth.h)
+    {
+        const int half = c.head_dim / 2;
+        std::vector<float2> tab(size_t(c.max_positions) * half);
+        for (int64_t pp = 0; pp < c.max_positions; ++pp)
+            for (int i = 0; i < half; ++i) {
+                float cc, ss;
+                ss_rope_cs(double(c.rope_theta), c.head_dim, pp, i, &cc, &ss);
+                tab[size_t(pp) * half + i] = make_float2(cc, ss);
+            }
+        if (cudaMalloc(&ctx->rope, tab.size() * sizeof(float2)) != cudaSuccess)
+            return bail(fail(ctx, SS_OUT_OF_MEMORY, "rope table"));
+        cudaMemcpy(ctx->rope, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice);
+    }
+    if (tp_size > 1) {
+        std::string why;
+        if (!nccl_id) return bail(fail(ctx, SS_INVALID_ARG, "tp_size > 1 needs an NCCL unique id"));
+        if (!g_nccl.load(why)) return bail(fail(ctx, SS_NCCL_ERROR, why));
+        ncclUniqueId id;
+        std::memcpy(&id, nccl_id, sizeof(id));
+        ncclResult_t r = g_nccl.init_rank(&ctx->comm, tp_size, id, tp_rank);
+        if (r != ncclSuccess) return bail(fail(ctx, SS_NCCL_ERROR, std::string("ncclCommInitRank: ") + g_nccl.err(r)));
+    }
+    if (cudaStreamSynchronize(ctx->st) != cudaSuccess)
+        return bail(fail(ctx, SS_CUDA_ERROR, std::string("init: ") + cudaGetErrorString(cudaGetLastError())));
+    *out = ctx;
+    return SS_OK;
+}
+
+SS_API void ss_destroy(ss_ctx* ctx) {
+    if (!ctx) return;
+    if (ctx->st) cudaStreamSynchronize(ctx->st);
+    if (ctx->comm) g_nccl.destroy(ctx->comm);
+    cudaFree(ctx->wmem);
+    cudaFree(ctx->rope);
+    cudaFree(ctx->kc);
+    cudaFree(ctx->vc);
+    for (void* q : {(void*)ctx->x, (void*)ctx->xn, (void*)ctx->qkv, (void*)ctx->q, (void*)ctx->o, (void*)ctx->act,
+                    (void*)ctx->part, (void*)ctx->xo, (void*)ctx->logits_l, (void*)ctx->logits_g, (void*)ctx->logits,
+                    (void*)ctx->next_tok, (void*)ctx->part_o, (void*)ctx->part_ml, (void*)ctx->scratch.dev})
+        cudaFree(q);
+    cudaFreeHost(ctx->pinned);
+    for (const Prof& p : ctx->pend) {
+        cudaEventDestroy(p.a);
+        cudaEventDestroy(p.b);
+    }
+    for (cudaEvent_t e : ctx->free_ev) cudaEventDestroy(e);
+    if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+    if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    if (ctx->st) cudaStreamDestroy(ctx->st);
+    delete ctx;
+}
+
+SS_API ss_status ss_model_config(const ss_ctx* ctx, ss_model_cfg* out, int32_t* tp_rank, int32_t* tp_size) {
+    if (!ctx || !out) return SS_INVALID_ARG;
+    *out = ctx->cfg;
+    if (tp_rank) *tp_rank = ctx->rank;
+    if (tp_size) *tp_size = ctx->tp;
+    return SS_OK;
+}
+
+SS_API ss_status ss_kv_alloc(ss_ctx* ctx, int64_t num_blocks, int32_t block_size) {
+    if (!ctx || num_blocks < 1 || block_size != 16)
+        return fail(ctx, SS_INVALID_ARG, "KV pool needs num_blocks >= 1 and block_size 16 (reference default)");
+    cudaFree(ctx->kc);
+    cudaFree(ctx->vc);
+    ctx->kc = ctx->vc = nullptr;
+    ctx->nblocks = 0;
+    ctx->bs = block_size;
+    ctx->layer_stride = num_blocks * ctx->nkv_l * block_size * ctx->hd;
+    const size_t bytes = size_t(ctx->layer_stride) * ctx->L * 2;
+    CK(cudaMalloc(&ctx->kc, bytes));
+    CK(cudaMalloc(&ctx->vc, bytes));
+    CK(cudaMemsetAsync(ctx->kc, 0, bytes, ctx->st));
+    CK(cudaMemsetAsync(ctx->vc, 0, bytes, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    ctx->nblocks = num_blocks;
+    return SS_OK;
+}
+
+SS_API ss_status ss_batch_upload(ss_ctx* ctx, const ss_batch_desc* desc, ss_batch** out) {
+    if (!ctx || !out) return SS_INVALID_ARG;
+    ss_batch* b = new ss_batch();
+    if (ss_status s = upload(ctx, desc, b)) {
+        cudaFree(b->dev);
+        delete b;
+        return s;
+    }
+    CK(cudaStreamSynchronize(ctx->st));
+    *out = b;
+    return SS_OK;
+}
+
+SS_API void ss_batch_free(ss_ctx* ctx, ss_batch* b) {
+    if (!b) return;
+    if (ctx) {
+        cudaStreamSynchronize(ctx->st);
+        if (ctx->last == b) ctx->last = nullptr;
+    }
+    cudaFree(b->dev);
+    delete b;
+}
+
+SS_API ss_status ss_forward_enqueue(ss_ctx* ctx, const ss_batch* b) {
+    if (!ctx || !b) return SS_INVALID_ARG;
+    if (ss_status s = ensure_workspace(ctx, b->T, std::max(b->n_out, 1), b->part_rows)) return s;
+    return enqueue_forward(ctx, b);
+}
+
+SS_API ss_status ss_read_outputs(ss_ctx* ctx, const ss_batch* b, float* logits, int32_t* next) {
+    if (!ctx || !b) return SS_INVALID_ARG;
+    return read_outputs(ctx, b, logits, next);
+}
+
+SS_API ss_status ss_forward_hybrid(ss_ctx* ctx, const ss_batch_desc* desc, float* logits, int32_t* next,
+                                   float* elapsed_ms) {
+    if (!ctx) return SS_INVALID_ARG;
+    CK(cudaEventRecord(ctx->ev0, ctx->st));
+    if (ss_status s = upload(ctx, desc, &ctx->scratch)) return s;
+    if (ss_status s = enqueue_forward(ctx, &ctx->scratch)) return s;
+    CK(cudaEventRecord(ctx->ev1, ctx->st));
+    if (ss_status s = read_outputs(ctx, &ctx->scratch, logits, next)) return s;
+    CK(cudaEventSynchronize(ctx->ev1));
+    if (elapsed_ms) CK(cudaEventElapsedTime(elapsed_ms, ctx->ev0, ctx->ev1));
+    return SS_OK;
+}
+
+SS_API void* ss_stream(ss_ctx* ctx) { return ctx ? static_cast<void*>(ctx->st) : nullptr; }
+
+SS_API ss_status ss_synchronize(ss_ctx* ctx) {
+    if (!ctx) return SS_INVALID_ARG;
+    CK(cudaStreamSynchronize(ctx->st));
+    return SS_OK;
+}
+
+SS_API ss_status ss_kv_fill_synthetic(ss_ctx* ctx, const int32_t* block_table, int32_t n_blocks, int32_t rid,
+                                      int32_t n_tokens, uint64_t seed) {
+    if (!ctx || !block_table || n_tokens < 0 || int64_t(n_blocks) * ctx->bs < n_tokens)
+        return fail(ctx, SS_INVALID_ARG, "bad synthetic fill arguments");
+    for (int b = 0; b < n_blocks; ++b)
+        if (block_table[b] < 0 || block_table[b] >= ctx->nblocks) return fail(ctx, SS_OUT_OF_KV, "block outside pool");
+    int32_t* d = nullptr;
+    CK(cudaMalloc(&d, size_t(std::max(n_blocks, 1)) * 4));
+    CK(cudaMemcpy(d, block_table, size_t(n_blocks) * 4, cudaMemcpyHostToDevice));
+    cudaError_t e = kv_fill_launch(ctx->kc, ctx->vc, ctx->layer_stride, ctx->L, d, n_tokens, rid, ctx->nkv_l,
+                                   ctx->rank * ctx->nkv_l, ctx->cfg.num_kv_heads, ctx->hd, ctx->bs, seed, ctx->st);
+    cudaError_t e2 = cudaStreamSynchronize(ctx->st);
+    cudaFree(d);
+    if (e != cudaSuccess || e2 != cudaSuccess) return fail(ctx, SS_CUDA_ERROR, "synthetic KV fill failed");
+    return SS_OK;
+}
+
+SS_API ss_status ss_set_profiling(ss_ctx* ctx, int32_t enabled) {
+    if (!ctx) return SS_INVALID_ARG;
+    ctx->prof = enabled != 0;
+    return SS_OK;
+}
+
+SS_API ss_status ss_kernel_times(ss_ctx* ctx, double* ms_out, int64_t* launches_out, int32_t reset) {
+    if (!ctx) return SS_INVALID_ARG;
+    CK(cudaStreamSynchronize(ctx->st));
+    collect_prof(ctx);
+    for (int k = 0; k < SS_K_NUM_CLASSES; ++k) {
+        if (ms_out) ms_out[k] = ctx->ms[k];
+        if (launches_out) launches_out[k] = ctx->launches[k];
+        if (reset) {
+            ctx->ms[k] = 0;
+            ctx->launches[k] = 0;
+        }
+    }
+    return SS_OK;
+}
+
+SS_API int64_t ss_launch_count(ss_ctx* ctx) { return ctx ? ctx->total_launches : 0; }
+
+// ---------------------------------------------------------------- single kernels
+
+SS_API ss_status ss_k_gemm(ss_ctx* ctx, const void* A, const void* B, void* D, int32_t M, int32_t N, int32_t K,
+                           int32_t epi) {
+    if (!ctx || epi < 0 || epi > 3) return fail(ctx, SS_INVALID_ARG, "bad gemm arguments");
+    GemmPlan p;
+    const int ldo = epi == EPI_SWIGLU ? N / 2 : N;
+    if (!gemm_prepare(p, A, uint64_t(M), B, M, N, K, D, ldo, epi, ctx->num_sms))
+        return fail(ctx, SS_INVALID_ARG, "gemm shape unsupported (N%32, K%8, SwiGLU N%64) or tensor map failed");
+    return launch(ctx, SS_K_GEMM_QKV, 1, [&] { return gemm_launch(p, ctx->st); });
+}
+
+SS_API ss_status ss_k_rmsnorm(ss_ctx* ctx, const float* x, const void* w, void* out, const int32_t* rows, int32_t M,
+                              int32_t h, float eps) {
+    if (!ctx || h % 8) return fail(ctx, SS_INVALID_ARG, "rmsnorm needs h % 8 == 0");
+    return launch(ctx, SS_K_RMSNORM, 1, [&] {
+        return rmsnorm_launch(x, static_cast<const bf16*>(w), static_cast<bf16*>(out), rows, M, h, eps, ctx->st);
+    });
+}
+
+SS_API ss_status ss_k_rope_append(ss_ctx* ctx, const void* qkv, void* q_out, const int32_t* pos, const int64_t* slot,
+                                  int32_t T, int32_t layer) {
+    if (!ctx || layer < 0 || layer >= ctx->L || !ctx->kc) return fail(ctx, SS_INVALID_ARG, "bad rope/append args");
+    return launch(ctx, SS_K_ROPE_APPEND, 1, [&] {
+        return rope_append_launch(static_cast<const bf16*>(qkv), static_cast<bf16*>(q_out), pos, slot, ctx->rope, T,
+                                  ctx->nq_l, ctx->nkv_l, ctx->hd, ctx->bs, ctx->kc + size_t(layer) * ctx->layer_stride,
+                                  ctx->vc + size_t(layer) * ctx->layer_stride, ctx->st);
+    });
+}
+
+SS_API ss_status ss_k_attention(ss_ctx* ctx, const ss_batch* b, const void* q, void* o, int32_t layer) {
+    if (!ctx || !b || layer < 0 || layer >= ctx->L) return fail(ctx, SS_INVALID_ARG, "bad attention args");
+    if (ss_status s = ensure_workspace(ctx, b->T, std::max(b->n_out, 1), b->part_rows)) return s;
+    const AttnParams ap = attn_params(ctx, b, static_cast<const bf16*>(q), static_cast<bf16*>(o), layer);
+    if (ss_status s = launch(ctx, SS_K_ATTN, 1, [&] { return attention_launch(ap, ctx->st); })) return s;
+    if (b->n_combs) return launch(ctx, SS_K_ATTN_COMBINE, 1, [&] { return attention_combine_launch(ap, ctx->st); });
+    return SS_OK;
+}
+
+SS_API ss_status ss_kv_layer_ptrs(ss_ctx* ctx, int32_t layer, void** k, void** v) {
+    if (!ctx || layer < 0 || layer >= ctx->L || !ctx->kc) return SS_INVALID_ARG;
+    *k = ctx->kc + size_t(layer) * ctx->layer_stride;
+    *v = ctx->vc + size_t(layer) * ctx->layer_stride;
+    return SS_OK;
+}
+
+SS_API ss_status ss_weight_ptr(ss_ctx* ctx, const char* name, int32_t layer, void** ptr, int64_t* rows,
+                               int64_t* cols) {
+    if (!ctx || !name) return SS_INVALID_ARG;
+    const std::string n(name);
+    const int64_t h = ctx->h, qkv = int64_t(ctx->nq_l + 2 * ctx->nkv_l) * ctx->hd, qd = int64_t(ctx->nq_l) * ctx->hd;
+    if (n == "embed") { *ptr = ctx->embed; *rows = ctx->cfg.vocab; *cols = h; return SS_OK; }
+    if (n == "lm_head") { *ptr = ctx->lm_head; *rows = ctx->vocab_l; *cols = h; return SS_OK; }
+    if (n == "final_norm") { *ptr = ctx->final_norm; *rows = 1; *cols = h; return SS_OK; }
+    if (layer < 0 || layer >= ctx->L) return fail(ctx, SS_INVALID_ARG, "layer out of range");
+    const Layer& W = ctx->layers[size_t(layer)];
+    if (n == "wqkv") { *ptr = W.wqkv; *rows = qkv; *cols = h; return SS_OK; }
+    if (n == "wo") { *ptr = W.wo; *rows = h; *cols = qd; return SS_OK; }
+    if (n == "wgu") { *ptr = W.wgu; *rows = 2 * ctx->ffn_l; *cols = h; return SS_OK; }
+    if (n == "wdown") { *ptr = W.wdown; *rows = h; *cols = ctx->ffn_l; return SS_OK; }
+    if (n == "attn_norm") { *ptr = W.attn_norm; *rows = 1; *cols = h; return SS_OK; }
+    if (n == "mlp_norm") { *ptr = W.mlp_norm; *rows = 1; *cols = h; return SS_OK; }
+    return fail(ctx, SS_INVALID_ARG, "unknown weight name " + n);
+}

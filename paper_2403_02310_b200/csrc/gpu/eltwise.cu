@@ -1,0 +1,301 @@
+// K2 (paged KV append) and K4 (RMSNorm, RoPE, residual, argmax) plus the
+// synthetic initialisers. All are HBM-bound: 16-byte vector accesses along the
+// contiguous hidden / head dimension, warp-shuffle reductions.
+#include "../../../include/ss_synth.h"
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace ssk {
+
+namespace {
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__global__ void embed_kernel(const int32_t* __restrict__ tokens, const __nv_bfloat16* __restrict__ table,
+                             float* __restrict__ x, int h) {
+    const int t = blockIdx.x;
+    const uint4* src = reinterpret_cast<const uint4*>(table + size_t(tokens[t]) * h);
+    float4* dst = reinterpret_cast<float4*>(x + size_t(t) * h);
+    for (int i = threadIdx.x; i < h / 8; i += blockDim.x) {
+        const uint4 v = src[i];
+        dst[2 * i] = make_float4(bf16_lo(v.x), bf16_hi(v.x), bf16_lo(v.y), bf16_hi(v.y));
+        dst[2 * i + 1] = make_float4(bf16_lo(v.z), bf16_hi(v.z), bf16_lo(v.w), bf16_hi(v.w));
+    }
+}
+
+// One CTA per row: out = bf16(x * rsqrt(mean(x^2) + eps) * w).
+__global__ void rmsnorm_kernel(const float* __restrict__ x, const __nv_bfloat16* __restrict__ w,
+                               __nv_bfloat16* __restrict__ out, const int32_t* __restrict__ rows, int h, float eps) {
+    __shared__ float red[32];
+    const int r = blockIdx.x;
+    const int src_row = rows ? rows[r] : r;
+    const float4* xr = reinterpret_cast<const float4*>(x + size_t(src_row) * h);
+    float ss = 0.f;
+    for (int i = threadIdx.x; i < h / 4; i += blockDim.x) {
+        const float4 v = xr[i];
+        ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+    }
+    ss = warp_sum(ss);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+        v = warp_sum(v);
+        if (threadIdx.x == 0) red[0] = rsqrtf(v / float(h) + eps);
+    }
+    __syncthreads();
+    const float inv = red[0];
+    const uint2* wr = reinterpret_cast<const uint2*>(w);
+    uint2* o = reinterpret_cast<uint2*>(out + size_t(r) * h);
+    for (int i = threadIdx.x; i < h / 4; i += blockDim.x) {
+        const float4 v = xr[i];
+        const uint2 ww = wr[i];
+        o[i] = make_uint2(pack_bf16(v.x * inv * bf16_lo(ww.x), v.y * inv * bf16_hi(ww.x)),
+                          pack_bf16(v.z * inv * bf16_lo(ww.y), v.w * inv * bf16_hi(ww.y)));
+    }
+}
+
+// One CTA per token. Thread handles 2 rotation pairs (i, i + hd/2) x2 lanes of
+// 4 B; q heads -> q_out, k heads -> K page, v heads copied to V page.
+__global__ void rope_append_kernel(const __nv_bfloat16* __restrict__ qkv, __nv_bfloat16* __restrict__ q_out,
+                                   const int32_t* __restrict__ pos, const int64_t* __restrict__ slot,
+                                   const float2* __restrict__ cs, int nq, int nkv, int hd, int bs,
+                                   __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc) {
+    const int t = blockIdx.x;
+    const int half = hd / 2;
+    const int p = pos[t];
+    const int64_t sl = slot[t];
+    const int64_t blk = sl / bs, off = sl % bs;
+    const __nv_bfloat16* row = qkv + size_t(t) * (nq + 2 * nkv) * hd;
+    const float2* c = cs + size_t(p) * half;
+    // rotate q and k heads: pairs (i, i + half), two consecutive i per thread
+    const int pairs = (nq + nkv) * (half / 2);
+    for (int idx = threadIdx.x; idx < pairs; idx += blockDim.x) {
+        const int hh = idx / (half / 2);
+        const int i = (idx % (half / 2)) * 2;
+        const __nv_bfloat16* src = row + size_t(hh) * hd;
+        const uint32_t lo = *reinterpret_cast<const uint32_t*>(src + i);
+        const uint32_t hi = *reinterpret_cast<const uint32_t*>(src + i + half);
+        const float2 c0 = c[i], c1 = c[i + 1];  // (cos, sin)
+        const float x0 = bf16_lo(lo), x1 = bf16_hi(lo), y0 = bf16_lo(hi), y1 = bf16_hi(hi);
+        const uint32_t nlo = pack_bf16(x0 * c0.x - y0 * c0.y, x1 * c1.x - y1 * c1.y);
+        const uint32_t nhi = pack_bf16(y0 * c0.x + x0 * c0.y, y1 * c1.x + x1 * c1.y);
+        __nv_bfloat16* dst;
+        if (hh < nq) {
+            dst = q_out + (size_t(t) * nq + hh) * hd;
+        } else {
+            dst = kc + ((size_t(blk) * nkv + (hh - nq)) * bs + off) * hd;
+        }
+        *reinterpret_cast<uint32_t*>(dst + i) = nlo;
+        *reinterpret_cast<uint32_t*>(dst + i + half) = nhi;
+    }
+    // v heads: straight copy, 16 B per thread
+    const int vchunks = nkv * hd / 8;
+    const __nv_bfloat16* vsrc = row + size_t(nq + nkv) * hd;
+    for (int idx = threadIdx.x; idx < vchunks; idx += blockDim.x) {
+        const int hh = idx / (hd / 8), c8 = (idx % (hd / 8)) * 8;
+        *reinterpret_cast<uint4*>(vc + ((size_t(blk) * nkv + hh) * bs + off) * hd + c8) =
+            *reinterpret_cast<const uint4*>(vsrc + size_t(hh) * hd + c8);
+    }
+}
+
+__global__ void residual_add_kernel(float* __restrict__ x, const __nv_bfloat16* __restrict__ part, int64_t n8) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n8; i += int64_t(gridDim.x) * blockDim.x) {
+        const uint4 v = reinterpret_cast<const uint4*>(part)[i];
+        float4* d = reinterpret_cast<float4*>(x) + 2 * i;
+        float4 a = d[0], b = d[1];
+        a.x += bf16_lo(v.x); a.y += bf16_hi(v.x); a.z += bf16_lo(v.y); a.w += bf16_hi(v.y);
+        b.x += bf16_lo(v.z); b.y += bf16_hi(v.z); b.z += bf16_lo(v.w); b.w += bf16_hi(v.w);
+        d[0] = a;
+        d[1] = b;
+    }
+}
+
+// Greedy argmax per row; ties resolve to the lowest index.
+__global__ void argmax_kernel(const float* __restrict__ logits, int V, int ld, int32_t* __restrict__ out) {
+    __shared__ float sv[32];
+    __shared__ int si[32];
+    const float* r = logits + size_t(blockIdx.x) * ld;
+    float best = -INFINITY;
+    int bi = 0x7fffffff;
+    for (int i = threadIdx.x; i < V; i += blockDim.x) {
+        const float v = r[i];
+        if (v > best || (v == best && i < bi)) {
+            best = v;
+            bi = i;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > best || (ov == best && oi < bi)) {
+            best = ov;
+            bi = oi;
+        }
+    }
+    if ((threadIdx.x & 31) == 0) {
+        sv[threadIdx.x >> 5] = best;
+        si[threadIdx.x >> 5] = bi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < int(blockDim.x >> 5); ++w)
+            if (sv[w] > best || (sv[w] == best && si[w] < bi)) {
+                best = sv[w];
+                bi = si[w];
+            }
+        out[blockIdx.x] = bi;
+    }
+}
+
+__global__ void gather_vocab_kernel(const float* __restrict__ in, float* __restrict__ out, int tp, int rows, int vl) {
+    const int64_t n = int64_t(tp) * rows * vl;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t r = (i / vl) % rows, k = i / (int64_t(vl) * rows), c = i % vl;
+        out[r * int64_t(tp) * vl + k * vl + c] = in[i];
+    }
+}
+
+// Element (i, j) of this rank's shard -> (tag, global row, global col, scale).
+__global__ void init_weight_kernel(__nv_bfloat16* __restrict__ w, const WeightInit wi) {
+    const int64_t n = wi.rows * wi.cols;
+    for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < n;
+         idx += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t i = idx / wi.cols, j = idx % wi.cols;
+        uint32_t tag = 0;
+        uint64_t gr = 0, gc = uint64_t(j);
+        float sc = wi.scale_a;
+        switch (wi.kind) {
+            case W_QKV: {
+                const int64_t qr = int64_t(wi.nq_l) * wi.hd, kr = int64_t(wi.nkv_l) * wi.hd;
+                if (i < qr) {
+                    tag = SS_TAG_LAYER(wi.layer, SS_T_Q);
+                    gr = uint64_t(wi.rank * qr + i);
+                } else if (i < qr + kr) {
+                    tag = SS_TAG_LAYER(wi.layer, SS_T_K);
+                    gr = uint64_t(wi.rank * kr + (i - qr));
+                    sc = wi.scale_b;
+                } else {
+                    tag = SS_TAG_LAYER(wi.layer, SS_T_V);
+                    gr = uint64_t(wi.rank * kr + (i - qr - kr));
+                    sc = wi.scale_c;
+                }
+                break;
+            }
+            case W_O:
+                tag = SS_TAG_LAYER(wi.layer, SS_T_O);
+                gr = uint64_t(i);
+                gc = uint64_t(int64_t(wi.rank) * wi.cols + j);
+                break;
+            case W_GU: {
+                const int64_t b = i / 64, r = i % 64;
+                const bool gate = r < 32;
+                tag = SS_TAG_LAYER(wi.layer, gate ? SS_T_GATE : SS_T_UP);
+                gr = uint64_t(int64_t(wi.rank) * wi.ffn_l + b * 32 + (gate ? r : r - 32));
+                sc = gate ? wi.scale_a : wi.scale_b;
+                break;
+            }
+            case W_DOWN:
+                tag = SS_TAG_LAYER(wi.layer, SS_T_DOWN);
+                gr = uint64_t(i);
+                gc = uint64_t(int64_t(wi.rank) * wi.cols + j);
+                break;
+            case W_EMBED:
+                tag = SS_TAG_EMBED;
+                gr = uint64_t(i);
+                break;
+            case W_LMHEAD:
+                tag = SS_TAG_LMHEAD;
+                gr = uint64_t(int64_t(wi.rank) * wi.vocab_l + i);
+                break;
+            default: {
+                w[idx] = __ushort_as_bfloat16(uint16_t(0x3F80));  // 1.0
+                continue;
+            }
+        }
+        w[idx] = __ushort_as_bfloat16(ss_synth_bf16(wi.seed, tag, gr, gc, sc));
+    }
+}
+
+__global__ void kv_fill_kernel(__nv_bfloat16* __restrict__ kb, __nv_bfloat16* __restrict__ vb, int64_t lstride,
+                               int L, const int32_t* __restrict__ bt, int n_tokens, int rid, int nkv_l, int kv_off,
+                               int nkv_g, int hd, int bs, uint64_t seed) {
+    const int64_t per_layer = int64_t(n_tokens) * nkv_l * hd;
+    const int64_t n = per_layer * L * 2;
+    for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < n;
+         idx += int64_t(gridDim.x) * blockDim.x) {
+        const int which = int(idx / (per_layer * L));
+        const int64_t rem = idx % (per_layer * L);
+        const int layer = int(rem / per_layer);
+        const int64_t e = rem % per_layer;
+        const int pos = int(e / (int64_t(nkv_l) * hd));
+        const int h = int((e / hd) % nkv_l), d = int(e % hd);
+        const uint16_t v = ss_synth_kv(seed, layer, which, rid, pos, kv_off + h, d, nkv_g, hd);
+        const int64_t blk = bt[pos / bs];
+        const int64_t off = layer * lstride + ((blk * nkv_l + h) * bs + pos % bs) * hd + d;
+        (which ? vb : kb)[off] = __ushort_as_bfloat16(v);
+    }
+}
+
+int grid_for(int64_t n, int threads) {
+    int64_t g = (n + threads - 1) / threads;
+    return int(g < 148 * 16 ? (g < 1 ? 1 : g) : 148 * 16);
+}
+
+}  // namespace
+
+cudaError_t embed_launch(const int32_t* tokens, const __nv_bfloat16* table, float* x, int T, int h, cudaStream_t st) {
+    if (T > 0) embed_kernel<<<T, 256, 0, st>>>(tokens, table, x, h);
+    return cudaGetLastError();
+}
+
+cudaError_t rmsnorm_launch(const float* x, const __nv_bfloat16* w, __nv_bfloat16* out, const int32_t* rows, int M,
+                           int h, float eps, cudaStream_t st) {
+    if (M > 0) rmsnorm_kernel<<<M, h >= 4096 ? 512 : 256, 0, st>>>(x, w, out, rows, h, eps);
+    return cudaGetLastError();
+}
+
+cudaError_t rope_append_launch(const __nv_bfloat16* qkv, __nv_bfloat16* q_out, const int32_t* pos, const int64_t* slot,
+                               const float2* cs, int T, int nq, int nkv, int hd, int bs, __nv_bfloat16* kc,
+                               __nv_bfloat16* vc, cudaStream_t st) {
+    if (T > 0) rope_append_kernel<<<T, 256, 0, st>>>(qkv, q_out, pos, slot, cs, nq, nkv, hd, bs, kc, vc);
+    return cudaGetLastError();
+}
+
+cudaError_t residual_add_launch(float* x, const __nv_bfloat16* part, int64_t n, cudaStream_t st) {
+    if (n > 0) residual_add_kernel<<<grid_for(n / 8, 256), 256, 0, st>>>(x, part, n / 8);
+    return cudaGetLastError();
+}
+
+cudaError_t argmax_launch(const float* logits, int rows, int V, int ld, int32_t* out, cudaStream_t st) {
+    if (rows > 0) argmax_kernel<<<rows, 512, 0, st>>>(logits, V, ld, out);
+    return cudaGetLastError();
+}
+
+cudaError_t gather_vocab_launch(const float* in, float* out, int tp, int rows, int vl, cudaStream_t st) {
+    const int64_t n = int64_t(tp) * rows * vl;
+    if (n > 0) gather_vocab_kernel<<<grid_for(n, 256), 256, 0, st>>>(in, out, tp, rows, vl);
+    return cudaGetLastError();
+}
+
+cudaError_t init_weight_launch(__nv_bfloat16* w, const WeightInit& wi, cudaStream_t st) {
+    init_weight_kernel<<<grid_for(wi.rows * wi.cols, 256), 256, 0, st>>>(w, wi);
+    return cudaGetLastError();
+}
+
+cudaError_t kv_fill_launch(__nv_bfloat16* kb, __nv_bfloat16* vb, int64_t lstride, int L, const int32_t* bt,
+                           int n_tokens, int rid, int nkv_l, int kv_off, int nkv_g, int hd, int bs, uint64_t seed,
+                           cudaStream_t st) {
+    const int64_t n = int64_t(n_tokens) * nkv_l * hd * L * 2;
+    if (n > 0)
+        kv_fill_kernel<<<grid_for(n, 256), 256, 0, st>>>(kb, vb, lstride, L, bt, n_tokens, rid, nkv_l, kv_off, nkv_g,
+                                                         hd, bs, seed);
+    return cudaGetLastError();
+}
+
+}  // namespace ssk

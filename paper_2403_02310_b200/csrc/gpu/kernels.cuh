@@ -1,0 +1,104 @@
+// Launch interfaces of the sm_100a kernels (K1..K4) used by ctx.cu.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ssk {
+
+// ------------------------------------------------------------------ K3 GEMM
+enum { EPI_BF16 = 0, EPI_RESADD = 1, EPI_SWIGLU = 2, EPI_F32 = 3 };
+
+struct GemmPlan {
+    CUtensorMap tmA, tmB;  // 64-byte aligned members of a 64-aligned struct
+    int M = 0, N = 0, K = 0;
+    void* out = nullptr;
+    int ldo = 0;
+    int epi = 0;
+    int bn = 256;
+    int num_sms = 148;
+} __attribute__((aligned(64)));
+
+bool make_tmap_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
+                  uint32_t box_cols);
+int gemm_pick_bn(int M, int N, int num_sms);
+// A is [a_rows >= M][K] bf16; B is [N][K] bf16; out row stride ldo elements.
+bool gemm_prepare(GemmPlan& p, const void* A, uint64_t a_rows, const void* B, int M, int N, int K, void* out,
+                  int ldo, int epi, int num_sms, int bn = 0);
+cudaError_t gemm_launch(const GemmPlan& p, cudaStream_t st);
+
+// ------------------------------------------------------------------ K1 attention
+// One work item = (entry, kv head, row tile, key range). Rows of an entry for
+// kv head h are (token j, head-in-group i) pairs, row = j * G + i.
+struct AttnItem {
+    int32_t entry;
+    int32_t kv_head;
+    int32_t row0;      // first row of the tile
+    int32_t nrows;     // rows in the tile (<= 64)
+    int32_t key0;      // key range [key0, key1)
+    int32_t key1;
+    int32_t part;      // -1: final output; else partial slot base (rows)
+    int32_t pad;
+};
+struct AttnCombine {  // one split group: partial slots base + s * nrows_pad
+    int32_t entry;
+    int32_t kv_head;
+    int32_t row0;
+    int32_t nrows;
+    int32_t nsplit;
+    int32_t part;
+    int32_t stride;  // rows between consecutive splits' partial slots
+    int32_t pad;
+};
+struct AttnParams {
+    const __nv_bfloat16* q;      // [T][nq_l][hd]
+    __nv_bfloat16* o;            // [T][nq_l][hd]
+    const __nv_bfloat16* kc;     // layer K cache [nblocks][nkv_l][bs][hd]
+    const __nv_bfloat16* vc;
+    const int32_t* cu_q;         // [E+1]
+    const int32_t* ctx_len;      // [E]
+    const int32_t* block_table;  // [E][max_blocks]
+    int32_t max_blocks;
+    const AttnItem* items;
+    int32_t n_items;
+    float* part_o;               // [slots][hd] fp32 (unnormalised)
+    float* part_ml;              // [slots][2]   (running max in log2 units, sum)
+    const AttnCombine* combines;
+    int32_t n_combines;
+    int32_t nq_l, nkv_l, group, head_dim, block_size;
+    float scale_log2;            // softmax scale * log2(e)
+};
+cudaError_t attention_launch(const AttnParams& p, cudaStream_t st);
+cudaError_t attention_combine_launch(const AttnParams& p, cudaStream_t st);
+
+// ------------------------------------------------------------------ K2/K4 elementwise
+cudaError_t embed_launch(const int32_t* tokens, const __nv_bfloat16* table, float* x, int T, int h,
+                         cudaStream_t st);
+cudaError_t rmsnorm_launch(const float* x, const __nv_bfloat16* w, __nv_bfloat16* out, const int32_t* rows, int M,
+                           int h, float eps, cudaStream_t st);
+// RoPE (rotate-half) of q and k heads + paged KV append of k and v.
+cudaError_t rope_append_launch(const __nv_bfloat16* qkv, __nv_bfloat16* q_out, const int32_t* pos,
+                               const int64_t* slot, const float2* rope_cs, int T, int nq_l, int nkv_l, int hd,
+                               int bs, __nv_bfloat16* kc, __nv_bfloat16* vc, cudaStream_t st);
+cudaError_t residual_add_launch(float* x, const __nv_bfloat16* part, int64_t n, cudaStream_t st);
+cudaError_t argmax_launch(const float* logits, int rows, int V, int ld, int32_t* out, cudaStream_t st);
+// logits gathered [tp][rows][V_l] -> [rows][tp * V_l]
+cudaError_t gather_vocab_launch(const float* in, float* out, int tp, int rows, int vl, cudaStream_t st);
+
+// Synthetic initialisers (ss_synth.h).
+enum WeightKind { W_QKV = 0, W_O = 1, W_GU = 2, W_DOWN = 3, W_EMBED = 4, W_LMHEAD = 5, W_ONES = 6 };
+struct WeightInit {
+    int kind, layer, rank;
+    int64_t rows, cols;
+    int nq_l, nkv_l, hd, ffn_l, vocab_l;
+    uint64_t seed;
+    float scale_a, scale_b, scale_c;  // per-tag scales (q/k/v or gate/up)
+};
+cudaError_t init_weight_launch(__nv_bfloat16* w, const WeightInit& wi, cudaStream_t st);
+cudaError_t kv_fill_launch(__nv_bfloat16* kbase, __nv_bfloat16* vbase, int64_t layer_stride, int L,
+                           const int32_t* bt_dev, int n_tokens, int rid, int nkv_l, int kv_off, int nkv_g, int hd,
+                           int bs, uint64_t seed, cudaStream_t st);
+
+}  // namespace ssk
