@@ -47,8 +47,12 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
+// Bounded wait: a pipeline bug surfaces as a trapped launch (an error the host
+// reports) instead of a hung GPU. The bound is seconds of spinning.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t spins = 0;
     while (!mbar_try_wait(bar, parity)) {
+        if (++spins == (1u << 28)) __trap();
     }
 }
 

@@ -219,16 +219,28 @@ class HybridForward:
         mk = lambda p: torch.as_tensor(_Dev(p, shp, "<i2"), device="cuda").view(torch.bfloat16)
         return mk(k.value), mk(v.value)
 
+    # The single-kernel entry points run on the library stream; torch work that
+    # produced their inputs runs on torch's stream, so order the two explicitly.
+    @staticmethod
+    def _fence():
+        import torch
+
+        torch.cuda.synchronize()
+
     def k_gemm(self, A, B, D, M: int, N: int, K: int, epilogue: int):
+        self._fence()
         self._check(gpu_lib().ss_k_gemm(self._h, A.data_ptr(), B.data_ptr(), D.data_ptr(), M, N, K, epilogue))
 
     def k_rmsnorm(self, x, w, out, rows, M: int, h: int, eps: float):
+        self._fence()
         self._check(gpu_lib().ss_k_rmsnorm(self._h, x.data_ptr(), w.data_ptr(), out.data_ptr(),
                                            rows.data_ptr() if rows is not None else None, M, h, eps))
 
     def k_rope_append(self, qkv, q_out, pos, slot, T: int, layer: int):
+        self._fence()
         self._check(gpu_lib().ss_k_rope_append(self._h, qkv.data_ptr(), q_out.data_ptr(), pos.data_ptr(),
                                                slot.data_ptr(), T, layer))
 
     def k_attention(self, batch: Batch, q, o, layer: int):
+        self._fence()
         self._check(gpu_lib().ss_k_attention(self._h, batch.handle, q.data_ptr(), o.data_ptr(), layer))
