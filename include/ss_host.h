@@ -165,6 +165,22 @@ const ss_batch_desc* ssh_desc_view(const ssh_desc* d);
 int64_t ssh_desc_pool_blocks(const ssh_desc* d);
 void ssh_desc_free(ssh_desc* d);
 
+/* Replay session: a persistent KV ledger + block tables for executing an
+ * externally given micro-batch stream (e.g. the reference's golden batch
+ * stream) on the GPU or the oracle. Each step grows every entry's request to
+ * prefix + tokens in entry order (admitting requests on first sight), exactly
+ * as Engine::try_issue does (engine.cpp:207-221); ssh_session_release returns
+ * a finished request's blocks (engine.cpp:283-286). Token ids use the real
+ * request ids. prompt_lens[e] marks chunk entries that complete their prompt. */
+typedef struct ssh_session ssh_session;
+ss_status ssh_session_create(int64_t kv_blocks, int32_t block_size, int32_t vocab, uint64_t token_seed,
+                             ssh_session** out);
+ss_status ssh_session_step(ssh_session* s, const ssh_entry* entries, int32_t n, const int32_t* prompt_lens,
+                           ssh_desc** out);
+ss_status ssh_session_release(ssh_session* s, int32_t request_id);
+int64_t ssh_session_peak_blocks(const ssh_session* s);
+void ssh_session_free(ssh_session* s);
+
 const char* ssh_last_error(void);
 
 #ifdef __cplusplus

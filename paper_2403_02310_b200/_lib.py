@@ -179,6 +179,11 @@ def host_lib():
         _sig(lib, "ssh_desc_view", C.POINTER(BatchDesc), [P])
         _sig(lib, "ssh_desc_pool_blocks", I64, [P])
         _sig(lib, "ssh_desc_free", None, [P])
+        _sig(lib, "ssh_session_create", I32, [I64, I32, I32, C.c_uint64, C.POINTER(P)])
+        _sig(lib, "ssh_session_step", I32, [P, C.POINTER(EntryRow), I32, P, C.POINTER(P)])
+        _sig(lib, "ssh_session_release", I32, [P, I32])
+        _sig(lib, "ssh_session_peak_blocks", I64, [P])
+        _sig(lib, "ssh_session_free", None, [P])
         _sig(lib, "ssh_last_error", C.c_char_p, [])
         _host = lib
     return _host
@@ -201,5 +206,6 @@ HOST_EXPORTS = [
     "ssh_report_event_log", "ssh_report_summary", "ssh_report_num_microbatches", "ssh_report_microbatch",
     "ssh_report_peak_blocks", "ssh_report_free", "ssh_iteration_time", "ssh_decode_reference_time",
     "ssh_compute_token_budget", "ssh_next_chunk_size", "ssh_percentile", "ssh_desc_build", "ssh_desc_canonical",
-    "ssh_desc_view", "ssh_desc_pool_blocks", "ssh_desc_free", "ssh_last_error",
+    "ssh_desc_view", "ssh_desc_pool_blocks", "ssh_desc_free", "ssh_session_create", "ssh_session_step",
+    "ssh_session_release", "ssh_session_peak_blocks", "ssh_session_free", "ssh_last_error",
 ]

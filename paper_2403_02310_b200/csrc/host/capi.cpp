@@ -18,6 +18,13 @@ struct ssh_report {
     bool jsonl_ready = false;
 };
 
+struct ssh_session {
+    ss::KvLedger kv;
+    int32_t vocab;
+    std::uint64_t seed;
+    ssh_session(std::int64_t blocks, std::int32_t bs, std::int32_t v, std::uint64_t sd) : kv(blocks, bs), vocab(v), seed(sd) {}
+};
+
 struct ssh_desc {
     ss::HostDesc d;
     ss_batch_desc view;
@@ -301,6 +308,40 @@ ss_status ssh_desc_canonical(int32_t tau, int32_t n_dec, int64_t kv_each, int64_
         *out = make_desc(b, std::vector<bool>(b.entries.size(), true), bs, vocab, seed);
     });
 }
+
+ss_status ssh_session_create(int64_t kv_blocks, int32_t bs, int32_t vocab, uint64_t seed, ssh_session** out) {
+    return guarded([&] {
+        if (vocab < 1) throw ss::ContractViolation("vocab must be >= 1");
+        *out = new ssh_session(kv_blocks, bs, vocab, seed);
+    });
+}
+
+ss_status ssh_session_step(ssh_session* s, const ssh_entry* entries, int32_t n, const int32_t* prompt_lens,
+                           ssh_desc** out) {
+    return guarded([&] {
+        if (!s || !entries || n < 1 || !prompt_lens || !out) throw ss::ContractViolation("null argument");
+        ss::Batch b = to_batch(entries, n);
+        std::vector<bool> completes;
+        for (int32_t i = 0; i < n; ++i) {
+            const ss::Entry& e = b.entries[std::size_t(i)];
+            if (!s->kv.live(e.rid)) s->kv.admit(e.rid, prompt_lens[i]);
+            s->kv.grow(e.rid, e.prefix + e.tokens);
+            completes.push_back(e.kind == ss::Kind::Chunk && e.prefix + e.tokens == prompt_lens[i]);
+        }
+        auto d = std::make_unique<ssh_desc>();
+        d->d = ss::build_desc(b, s->kv, completes, s->seed, s->vocab);
+        d->view = d->d.view();
+        d->pool_blocks = s->kv.peak_allocated();
+        *out = d.release();
+    });
+}
+
+ss_status ssh_session_release(ssh_session* s, int32_t rid) {
+    return guarded([&] { s->kv.release(rid); });
+}
+
+int64_t ssh_session_peak_blocks(const ssh_session* s) { return s ? s->kv.peak_allocated() : 0; }
+void ssh_session_free(ssh_session* s) { delete s; }
 
 const ss_batch_desc* ssh_desc_view(const ssh_desc* d) { return d ? &d->view : nullptr; }
 int64_t ssh_desc_pool_blocks(const ssh_desc* d) { return d ? d->pool_blocks : 0; }

@@ -135,9 +135,12 @@ class SimReport:
         self._h = C.c_void_p(handle)
 
     def __del__(self):
-        if getattr(self, "_h", None) is not None and self._h.value:
-            host_lib().ssh_report_free(self._h)
-            self._h = None
+        try:
+            if getattr(self, "_h", None) is not None and self._h.value:
+                host_lib().ssh_report_free(self._h)
+                self._h = None
+        except Exception:  # interpreter shutdown
+            pass
 
     def event_log_jsonl(self) -> str:
         n = C.c_size_t()
@@ -239,9 +242,12 @@ class Descriptor:
         return cls(h.value)
 
     def __del__(self):
-        if getattr(self, "_h", None) is not None and self._h.value:
-            host_lib().ssh_desc_free(self._h)
-            self._h = None
+        try:
+            if getattr(self, "_h", None) is not None and self._h.value:
+                host_lib().ssh_desc_free(self._h)
+                self._h = None
+        except Exception:  # interpreter shutdown
+            pass
 
     @property
     def view(self) -> _lib.BatchDesc:
@@ -264,3 +270,50 @@ class Descriptor:
             "block_table": a(v.block_table, E * v.max_blocks, np.int32).reshape(E, v.max_blocks),
             "out_rows": a(v.out_rows, v.n_out, np.int32),
         }
+
+
+class Session:
+    """Persistent ledger + block tables for replaying a micro-batch stream
+    (ssh_session_*): entries keep their real request ids across steps."""
+
+    def __init__(self, kv_blocks: int, *, block_size: int = 16, vocab: int, token_seed: int = 0):
+        h = C.c_void_p()
+        host_check(host_lib().ssh_session_create(kv_blocks, block_size, vocab, token_seed, C.byref(h)))
+        self._h = h
+
+    def step(self, entries: Sequence[BatchEntry], prompt_lens: Sequence[int]) -> Descriptor:
+        arr = (_lib.EntryRow * len(entries))(*[e._c() for e in entries])
+        pl = (C.c_int32 * len(entries))(*prompt_lens)
+        h = C.c_void_p()
+        host_check(host_lib().ssh_session_step(self._h, arr, len(entries), pl, C.byref(h)))
+        return Descriptor(h.value)
+
+    def release(self, request_id: int):
+        host_check(host_lib().ssh_session_release(self._h, request_id))
+
+    @property
+    def peak_blocks(self) -> int:
+        return host_lib().ssh_session_peak_blocks(self._h)
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None) is not None and self._h.value:
+                host_lib().ssh_session_free(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+
+def replay_plan(report: SimReport, trace: Sequence[Request]):
+    """Yields (microbatch, prompt_lens, finished_ids) for executing a simulated
+    stream in issue order: finished_ids are released after that step (pp = 1)."""
+    for mb in report.microbatches():
+        pl = [trace[e.request_id].prompt_tokens for e in mb.entries]
+        done = []
+        for e in mb.entries:
+            r = trace[e.request_id]
+            if e.kind == "prefill" and e.prefix_tokens + e.chunk_tokens == r.prompt_tokens and r.output_tokens == 1:
+                done.append(e.request_id)
+            elif e.kind == "decode" and e.prefix_tokens == r.prompt_tokens + r.output_tokens - 2:
+                done.append(e.request_id)
+        yield mb, pl, done
