@@ -36,6 +36,7 @@ namespace {
 constexpr int kWarps = 4;
 constexpr int kKeysPerTile = 64;
 constexpr int kRowsPerTile = 64;
+constexpr int kStages = 3;  // 2 CTAs/SM x 2 tiles in flight = 128 KB of K/V outstanding per SM
 
 template <int HD>
 struct AttnSmem {
@@ -44,7 +45,7 @@ struct AttnSmem {
     static constexpr int Q_BYTES = kRowsPerTile * ROW_BYTES;
     static constexpr int KV_TILE = kKeysPerTile * ROW_BYTES;
     static constexpr int STAGE = 2 * KV_TILE;  // K + V
-    static constexpr int TOTAL = Q_BYTES + 2 * STAGE;
+    static constexpr int TOTAL = Q_BYTES + kStages * STAGE;
 };
 
 // byte offset of (row, 16B chunk c) in an XOR-swizzled tile
@@ -108,18 +109,25 @@ __device__ __forceinline__ void attend(const AttnParams& p, const AttnItem& it, 
     for (int dt = 0; dt < HD / 8; ++dt) O[dt][0] = O[dt][1] = O[dt][2] = O[dt][3] = 0.f;
 
     const int ntiles = (it.key1 - it.key0 + kKeysPerTile - 1) / kKeysPerTile;
-    load_kv_tile<HD>(p, smem + S::Q_BYTES, smem + S::Q_BYTES + S::KV_TILE, e, it.kv_head, it.key0, it.key1);
-    cp_async_commit();
-    for (int t = 0; t < ntiles; ++t) {
-        const int kbase = it.key0 + t * kKeysPerTile;
-        uint8_t* sK = smem + S::Q_BYTES + (t & 1) * S::STAGE;
-        uint8_t* sV = sK + S::KV_TILE;
-        if (t + 1 < ntiles) {
-            uint8_t* nK = smem + S::Q_BYTES + ((t + 1) & 1) * S::STAGE;
-            load_kv_tile<HD>(p, nK, nK + S::KV_TILE, e, it.kv_head, kbase + kKeysPerTile, it.key1);
+    // kStages-deep cp.async ring: kStages-1 tiles stay in flight while one is consumed
+#pragma unroll
+    for (int s = 0; s < kStages - 1; ++s) {
+        if (s < ntiles) {
+            uint8_t* nK = smem + S::Q_BYTES + s * S::STAGE;
+            load_kv_tile<HD>(p, nK, nK + S::KV_TILE, e, it.kv_head, it.key0 + s * kKeysPerTile, it.key1);
         }
         cp_async_commit();
-        cp_async_wait<1>();
+    }
+    for (int t = 0; t < ntiles; ++t) {
+        const int kbase = it.key0 + t * kKeysPerTile;
+        uint8_t* sK = smem + S::Q_BYTES + (t % kStages) * S::STAGE;
+        uint8_t* sV = sK + S::KV_TILE;
+        if (t + kStages - 1 < ntiles) {
+            uint8_t* nK = smem + S::Q_BYTES + ((t + kStages - 1) % kStages) * S::STAGE;
+            load_kv_tile<HD>(p, nK, nK + S::KV_TILE, e, it.kv_head, kbase + (kStages - 1) * kKeysPerTile, it.key1);
+        }
+        cp_async_commit();
+        cp_async_wait<kStages - 1>();
         __syncthreads();
 
         // S = Q K^T for this warp's key slice
@@ -191,7 +199,7 @@ __device__ __forceinline__ void attend(const AttnParams& p, const AttnItem& it, 
                 mma_bf16_16816(O[dt + 1], a, b2, b3);
             }
         }
-        __syncthreads();  // stage (t & 1) is refilled by the next iteration's prefetch
+        __syncthreads();  // this stage is refilled by a later iteration's prefetch
     }
     cp_async_wait<0>();
 #pragma unroll

@@ -18,6 +18,7 @@
 //   EPI_SWIGLU  gate/up rows interleaved in 32-row groups: out = silu(g) * u
 //   EPI_F32     store fp32 D (LM head logits)
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -268,6 +269,10 @@ bool make_tmap_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols
 }
 
 int gemm_pick_bn(int M, int N, int num_sms) {
+    if (const char* f = getenv("SS_GEMM_BN")) {  // tuning override (dev only)
+        const int bn = atoi(f);
+        if (bn == 128 || bn == 256) return bn;
+    }
     auto cost = [&](int bn) {
         const long tiles = long((M + BM - 1) / BM) * ((N + bn - 1) / bn);
         const long waves = (tiles + num_sms - 1) / num_sms;
