@@ -14,17 +14,20 @@
 //
 // Item modes (CTA-uniform, 4 warps):
 //   row mode  (rows > 16, prefill tiles): warp w owns rows [16w, 16w+16) and
-//             walks the whole key range; classic flash-attention-2 loop.
+//             walks the whole key range; flash-attention-2 style loop.
 //   key mode  (rows <= 16, decodes):      all warps share the rows; each warp
 //             takes a 16-key slice of every 64-key tile, and the four partial
 //             softmax states are merged in shared memory at the end.
 // Long key ranges are split across CTAs (split-KV); partial (m, l, O) go to a
 // workspace and attention_combine merges them in a fixed order (deterministic).
 //
-// K/V pages ([block][kv_head][16][hd], 4 KB contiguous per page at hd=128) are
-// streamed with cp.async into an XOR-swizzled double buffer; S = QK^T and
-// O += PV use mma.sync m16n8k16 (bf16 in, fp32 accumulate).
+// K/V pages ([block][kv_head][16][hd], 4 KB contiguous at hd=128) are moved by
+// TMA (cp.async.bulk.tensor, SWIZZLE_128B) into a kStages-deep ring, issued by
+// one thread: no per-thread address math or block-table loads in the stream.
+// S = QK^T and O += PV use mma.sync m16n8k16 (bf16 in, fp32 accumulate); the
+// decode path is HBM-bound, so the MMA flavour does not limit it.
 #include <cfloat>
+#include <climits>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -40,50 +43,56 @@ constexpr int kStages = 3;  // 2 CTAs/SM x 2 tiles in flight = 128 KB of K/V out
 
 template <int HD>
 struct AttnSmem {
-    static constexpr int ROW_BYTES = HD * 2;
-    static constexpr int CHUNKS = HD / 8;  // 16 B chunks per row
-    static constexpr int Q_BYTES = kRowsPerTile * ROW_BYTES;
-    static constexpr int KV_TILE = kKeysPerTile * ROW_BYTES;
-    static constexpr int STAGE = 2 * KV_TILE;  // K + V
-    static constexpr int TOTAL = Q_BYTES + kStages * STAGE;
+    static constexpr int Q_BYTES = kRowsPerTile * HD * 2;
+    static constexpr int KV_TILE = kKeysPerTile * HD * 2;  // [HD/64 halves][64 keys][128 B]
+    static constexpr int STAGE = 2 * KV_TILE;              // K + V
+    static constexpr int BAR_OFF = Q_BYTES + kStages * STAGE;
+    // 896 B of alignment slack (the dynamic window starts 1 KB-aligned in practice;
+    // checked at run time) keeps two CTAs per SM within 228 KB at hd = 128
+    static constexpr int TOTAL = BAR_OFF + 64 + 896;
 };
 
-// byte offset of (row, 16B chunk c) in an XOR-swizzled tile
+// Q tile: rows of HD*2 bytes, 16-byte chunks XOR-swizzled by row.
 template <int HD>
-__device__ __forceinline__ uint32_t swz(int row, int c) {
+__device__ __forceinline__ uint32_t swz_q(int row, int c) {
     return uint32_t(row * (HD * 2) + ((c ^ (row & 7)) << 4));
+}
+// K/V tile as written by TMA with SWIZZLE_128B: [c / 8 half][key][128 B].
+__device__ __forceinline__ uint32_t swz_kv(int key, int c) {
+    return uint32_t((c >> 3) * (kKeysPerTile * 128) + key * 128 + (((c & 7) ^ (key & 7)) << 4));
 }
 
 template <int HD>
-__device__ __forceinline__ void load_kv_tile(const AttnParams& p, uint8_t* sK, uint8_t* sV, int e, int h, int kbase,
-                                             int key1) {
-    constexpr int CH = HD / 8;
+__device__ __forceinline__ void issue_kv_tile(const AttnParams& p, const CUtensorMap* tmK, const CUtensorMap* tmV,
+                                              uint8_t* sK, uint8_t* sV, uint64_t* bar, int e, int h, int kbase) {
     const int32_t* bt = p.block_table + size_t(e) * p.max_blocks;
-    const size_t page = size_t(16) * HD;  // elements per (block, head) page
-    for (int idx = threadIdx.x; idx < kKeysPerTile * CH; idx += kWarps * 32) {
-        const int r = idx / CH, c = idx % CH;
-        const int key = kbase + r;
-        const uint32_t so = swz<HD>(r, c);
-        if (key < key1) {
-            const int32_t blk = bt[key >> 4];
-            const size_t off = (size_t(blk) * p.nkv_l + h) * page + size_t(key & 15) * HD + c * 8;
-            cp_async16(smem_u32(sK) + so, p.kc + off);
-            cp_async16(smem_u32(sV) + so, p.vc + off);
-        } else {
-            cp_async_zero16(smem_u32(sK) + so, p.kc);
-            cp_async_zero16(smem_u32(sV) + so, p.vc);
+    const int nvalid = (p.ctx_len[e] + 15) >> 4;
+    mbar_arrive_expect_tx(bar, 2 * AttnSmem<HD>::KV_TILE);
+#pragma unroll
+    for (int pg = 0; pg < kKeysPerTile / 16; ++pg) {
+        const int lb = (kbase >> 4) + pg;
+        // pages past the context are masked; point them at a valid (finite) page
+        const int32_t blk = bt[lb < nvalid ? lb : 0];
+        const int32_t row = int32_t(p.layer_row0 + (int64_t(blk) * p.nkv_l + h) * 16);
+#pragma unroll
+        for (int hh = 0; hh < HD / 64; ++hh) {
+            const uint32_t off = uint32_t(hh * (kKeysPerTile * 128) + pg * 16 * 128);
+            tma_load_2d(sK + off, tmK, hh * 64, row, bar);
+            tma_load_2d(sV + off, tmV, hh * 64, row, bar);
         }
     }
 }
 
 // KPW = keys handled per warp per 64-key tile (64: row mode, 16: key mode).
 template <int HD, int KPW>
-__device__ __forceinline__ void attend(const AttnParams& p, const AttnItem& it, uint8_t* smem, int qrow_base,
-                                       int kofs, float (&O)[HD / 8][4], float (&m)[2], float (&l)[2]) {
+__device__ __forceinline__ void attend(const AttnParams& p, const CUtensorMap* tmK, const CUtensorMap* tmV,
+                                       const AttnItem& it, uint8_t* smem, int qrow_base, int kofs,
+                                       float (&O)[HD / 8][4], float (&m)[2], float (&l)[2]) {
     using S = AttnSmem<HD>;
     constexpr int NT = KPW / 8;  // n8 tiles of S per warp
     const int lane = threadIdx.x & 31;
     uint8_t* sQ = smem;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
     const int e = it.entry;
     const int tok0 = p.cu_q[e];
     const int ntok = p.cu_q[e + 1] - tok0;
@@ -94,41 +103,44 @@ __device__ __forceinline__ void attend(const AttnParams& p, const AttnItem& it, 
 #pragma unroll
     for (int ks = 0; ks < HD / 16; ++ks) {
         const int r = qrow_base + (lane & 15);
-        ldsm_x4(smem_u32(sQ) + swz<HD>(r, ks * 2 + (lane >> 4)), qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3]);
+        ldsm_x4(smem_u32(sQ) + swz_q<HD>(r, ks * 2 + (lane >> 4)), qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3]);
     }
-    // causal limits of the two rows this thread holds
+    // causal limits of the two rows this thread holds (unused rows see everything:
+    // their Q is zero, so they stay finite and are never stored)
     int lim[2];
 #pragma unroll
     for (int hr = 0; hr < 2; ++hr) {
         const int r = qrow_base + (lane >> 2) + hr * 8;
-        lim[hr] = r < it.nrows ? prefix + (it.row0 + r) / p.group : -1;
+        lim[hr] = r < it.nrows ? prefix + (it.row0 + r) / p.group : INT_MAX;
     }
+    const int lim_lo = __reduce_min_sync(0xffffffffu, min(lim[0], lim[1]));
     m[0] = m[1] = -INFINITY;
     l[0] = l[1] = 0.f;
 #pragma unroll
     for (int dt = 0; dt < HD / 8; ++dt) O[dt][0] = O[dt][1] = O[dt][2] = O[dt][3] = 0.f;
 
     const int ntiles = (it.key1 - it.key0 + kKeysPerTile - 1) / kKeysPerTile;
-    // kStages-deep cp.async ring: kStages-1 tiles stay in flight while one is consumed
+    if (threadIdx.x == 0) {
 #pragma unroll
-    for (int s = 0; s < kStages - 1; ++s) {
-        if (s < ntiles) {
-            uint8_t* nK = smem + S::Q_BYTES + s * S::STAGE;
-            load_kv_tile<HD>(p, nK, nK + S::KV_TILE, e, it.kv_head, it.key0 + s * kKeysPerTile, it.key1);
-        }
-        cp_async_commit();
+        for (int s = 0; s < kStages - 1; ++s)
+            if (s < ntiles) {
+                uint8_t* sk = smem + S::Q_BYTES + s * S::STAGE;
+                issue_kv_tile<HD>(p, tmK, tmV, sk, sk + S::KV_TILE, &full[s], e, it.kv_head,
+                                  it.key0 + s * kKeysPerTile);
+            }
     }
     for (int t = 0; t < ntiles; ++t) {
         const int kbase = it.key0 + t * kKeysPerTile;
-        uint8_t* sK = smem + S::Q_BYTES + (t % kStages) * S::STAGE;
+        const int st = t % kStages;
+        uint8_t* sK = smem + S::Q_BYTES + st * S::STAGE;
         uint8_t* sV = sK + S::KV_TILE;
-        if (t + kStages - 1 < ntiles) {
-            uint8_t* nK = smem + S::Q_BYTES + ((t + kStages - 1) % kStages) * S::STAGE;
-            load_kv_tile<HD>(p, nK, nK + S::KV_TILE, e, it.kv_head, kbase + (kStages - 1) * kKeysPerTile, it.key1);
+        if (threadIdx.x == 0 && t + kStages - 1 < ntiles) {
+            const int ns = (t + kStages - 1) % kStages;
+            uint8_t* nk = smem + S::Q_BYTES + ns * S::STAGE;
+            issue_kv_tile<HD>(p, tmK, tmV, nk, nk + S::KV_TILE, &full[ns], e, it.kv_head,
+                              kbase + (kStages - 1) * kKeysPerTile);
         }
-        cp_async_commit();
-        cp_async_wait<kStages - 1>();
-        __syncthreads();
+        mbar_wait(&full[st], uint32_t((t / kStages) & 1));
 
         // S = Q K^T for this warp's key slice
         float s[NT][4];
@@ -140,47 +152,55 @@ __device__ __forceinline__ void attend(const AttnParams& p, const AttnItem& it, 
             for (int nt = 0; nt < NT; nt += 2) {
                 const int key = kofs + nt * 8 + ((lane >> 4) << 3) + (lane & 7);
                 uint32_t b0, b1, b2, b3;
-                ldsm_x4(smem_u32(sK) + swz<HD>(key, ks * 2 + ((lane >> 3) & 1)), b0, b1, b2, b3);
+                ldsm_x4(smem_u32(sK) + swz_kv(key, ks * 2 + ((lane >> 3) & 1)), b0, b1, b2, b3);
                 mma_bf16_16816(s[nt], qa[ks], b0, b1);
                 mma_bf16_16816(s[nt + 1], qa[ks], b2, b3);
             }
         }
-        // mask, online softmax (log2 domain)
+        // mask only where a row's causal limit or the range end cuts this slice
+        const int klast = kbase + kofs + KPW - 1;
+        if (klast > lim_lo || klast >= it.key1) {
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const int key = kbase + kofs + nt * 8 + 2 * (lane & 3) + (c & 1);
+                    if (key > lim[c >> 1] || key >= it.key1) s[nt][c] = -INFINITY;
+                }
+        }
         float mt[2] = {-INFINITY, -INFINITY};
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const int key = kbase + kofs + nt * 8 + 2 * (lane & 3) + (c & 1);
-                const int hr = c >> 1;
-                const bool vis = key <= lim[hr] && key < it.key1;
-                s[nt][c] = vis ? s[nt][c] * p.scale_log2 : -INFINITY;
-                mt[hr] = fmaxf(mt[hr], s[nt][c]);
-            }
+            mt[0] = fmaxf(mt[0], fmaxf(s[nt][0], s[nt][1]));
+            mt[1] = fmaxf(mt[1], fmaxf(s[nt][2], s[nt][3]));
         }
         float alpha[2], msub[2];
 #pragma unroll
         for (int hr = 0; hr < 2; ++hr) {
             mt[hr] = fmaxf(mt[hr], __shfl_xor_sync(0xffffffffu, mt[hr], 1));
             mt[hr] = fmaxf(mt[hr], __shfl_xor_sync(0xffffffffu, mt[hr], 2));
-            const float mn = fmaxf(m[hr], mt[hr]);
+            const float mn = fmaxf(m[hr], mt[hr] * p.scale_log2);
             msub[hr] = mn == -INFINITY ? 0.f : mn;
             alpha[hr] = exp2f(m[hr] - msub[hr]);
             m[hr] = mn;
             l[hr] *= alpha[hr];
         }
+        if (__any_sync(0xffffffffu, alpha[0] != 1.f || alpha[1] != 1.f)) {
 #pragma unroll
-        for (int dt = 0; dt < HD / 8; ++dt) {
-            O[dt][0] *= alpha[0];
-            O[dt][1] *= alpha[0];
-            O[dt][2] *= alpha[1];
-            O[dt][3] *= alpha[1];
+            for (int dt = 0; dt < HD / 8; ++dt) {
+                O[dt][0] *= alpha[0];
+                O[dt][1] *= alpha[0];
+                O[dt][2] *= alpha[1];
+                O[dt][3] *= alpha[1];
+            }
         }
         uint32_t pa[NT / 2][4];
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
-            const float p0 = exp2f(s[nt][0] - msub[0]), p1 = exp2f(s[nt][1] - msub[0]);
-            const float p2 = exp2f(s[nt][2] - msub[1]), p3 = exp2f(s[nt][3] - msub[1]);
+            const float p0 = exp2f(fmaf(s[nt][0], p.scale_log2, -msub[0]));
+            const float p1 = exp2f(fmaf(s[nt][1], p.scale_log2, -msub[0]));
+            const float p2 = exp2f(fmaf(s[nt][2], p.scale_log2, -msub[1]));
+            const float p3 = exp2f(fmaf(s[nt][3], p.scale_log2, -msub[1]));
             l[0] += p0 + p1;
             l[1] += p2 + p3;
             pa[nt >> 1][(nt & 1) * 2 + 0] = pack_bf16(p0, p1);
@@ -194,14 +214,13 @@ __device__ __forceinline__ void attend(const AttnParams& p, const AttnItem& it, 
 #pragma unroll
             for (int dt = 0; dt < HD / 8; dt += 2) {
                 uint32_t b0, b1, b2, b3;
-                ldsm_x4_t(smem_u32(sV) + swz<HD>(key, dt + (lane >> 4)), b0, b1, b2, b3);
+                ldsm_x4_t(smem_u32(sV) + swz_kv(key, dt + (lane >> 4)), b0, b1, b2, b3);
                 mma_bf16_16816(O[dt], a, b0, b1);
                 mma_bf16_16816(O[dt + 1], a, b2, b3);
             }
         }
-        __syncthreads();  // this stage is refilled by a later iteration's prefetch
+        __syncthreads();  // stage st is refilled by a later iteration's TMA
     }
-    cp_async_wait<0>();
 #pragma unroll
     for (int hr = 0; hr < 2; ++hr) {
         l[hr] += __shfl_xor_sync(0xffffffffu, l[hr], 1);
@@ -221,24 +240,31 @@ __device__ __forceinline__ void emit_pair(const AttnParams& p, const AttnItem& i
         const float inv = ll > 0.f ? 1.f / ll : 0.f;
         *reinterpret_cast<uint32_t*>(p.o + (size_t(tok) * p.nq_l + hq) * HD + d) = pack_bf16(o0 * inv, o1 * inv);
     } else {
-        float* po = p.part_o + size_t(it.part + r) * HD + d;
-        po[0] = o0;
-        po[1] = o1;
-        if (d == 0) {
-            p.part_ml[size_t(it.part + r) * 2 + 0] = mm;
-            p.part_ml[size_t(it.part + r) * 2 + 1] = ll;
-        }
+        *reinterpret_cast<float2*>(p.part_o + size_t(it.part + r) * HD + d) = make_float2(o0, o1);
+        if (d == 0) *reinterpret_cast<float2*>(p.part_ml + size_t(it.part + r) * 2) = make_float2(mm, ll);
     }
 }
 
 template <int HD>
-__global__ void __launch_bounds__(kWarps * 32) attention_kernel(const AttnParams p) {
+__global__ void __launch_bounds__(kWarps * 32) attention_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmK,
+                                                                const __grid_constant__ CUtensorMap tmV) {
     using S = AttnSmem<HD>;
-    extern __shared__ __align__(128) uint8_t smem[];
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t pad = ((raw + 1023u) & ~1023u) - raw;
+    if (pad > 896u) __trap();  // SWIZZLE_128B tiles need 1 KB alignment
+    uint8_t* smem = smem_raw + pad;
     const AttnItem it = p.items[blockIdx.x];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool key_mode = it.nrows <= 16;
 
+    if (threadIdx.x == 0) {
+        tma_prefetch(&tmK);
+        tma_prefetch(&tmV);
+        uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
+        for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+        mbar_fence_init();
+    }
     // stage the Q tile (rows beyond nrows are zero)
     {
         constexpr int CH = HD / 8;
@@ -246,7 +272,7 @@ __global__ void __launch_bounds__(kWarps * 32) attention_kernel(const AttnParams
         const int nr = key_mode ? 16 : kRowsPerTile;
         for (int idx = threadIdx.x; idx < nr * CH; idx += kWarps * 32) {
             const int r = idx / CH, c = idx % CH;
-            const uint32_t so = smem_u32(smem) + swz<HD>(r, c);
+            const uint32_t so = smem_u32(smem) + swz_q<HD>(r, c);
             if (r < it.nrows) {
                 const int gr = it.row0 + r;
                 const __nv_bfloat16* src =
@@ -263,7 +289,7 @@ __global__ void __launch_bounds__(kWarps * 32) attention_kernel(const AttnParams
 
     float O[HD / 8][4], m[2], l[2];
     if (!key_mode) {
-        attend<HD, 64>(p, it, smem, warp * 16, 0, O, m, l);
+        attend<HD, 64>(p, &tmK, &tmV, it, smem, warp * 16, 0, O, m, l);
         const int r0 = warp * 16 + (lane >> 2);
 #pragma unroll
         for (int dt = 0; dt < HD / 8; ++dt) {
@@ -274,9 +300,8 @@ __global__ void __launch_bounds__(kWarps * 32) attention_kernel(const AttnParams
         return;
     }
 
-    attend<HD, 16>(p, it, smem, 0, warp * 16, O, m, l);
-    // merge the four warps' partial softmax states (smem reused after the loop)
-    __syncthreads();
+    attend<HD, 16>(p, &tmK, &tmV, it, smem, 0, warp * 16, O, m, l);
+    // merge the four warps' partial softmax states (K/V stages reused as scratch)
     float* sO = reinterpret_cast<float*>(smem + S::Q_BYTES);  // [4][16][HD]
     float* sML = sO + kWarps * 16 * HD;                        // [4][16][2]
     {
@@ -284,10 +309,8 @@ __global__ void __launch_bounds__(kWarps * 32) attention_kernel(const AttnParams
 #pragma unroll
         for (int dt = 0; dt < HD / 8; ++dt) {
             const int d = dt * 8 + 2 * (lane & 3);
-            sO[(warp * 16 + r0) * HD + d] = O[dt][0];
-            sO[(warp * 16 + r0) * HD + d + 1] = O[dt][1];
-            sO[(warp * 16 + r0 + 8) * HD + d] = O[dt][2];
-            sO[(warp * 16 + r0 + 8) * HD + d + 1] = O[dt][3];
+            *reinterpret_cast<float2*>(&sO[(warp * 16 + r0) * HD + d]) = make_float2(O[dt][0], O[dt][1]);
+            *reinterpret_cast<float2*>(&sO[(warp * 16 + r0 + 8) * HD + d]) = make_float2(O[dt][2], O[dt][3]);
         }
         if ((lane & 3) == 0) {
             sML[(warp * 16 + r0) * 2] = m[0];
@@ -308,8 +331,9 @@ __global__ void __launch_bounds__(kWarps * 32) attention_kernel(const AttnParams
         for (int w = 0; w < kWarps; ++w) {
             const float f = exp2f(sML[(w * 16 + r) * 2] - Ms);
             L += sML[(w * 16 + r) * 2 + 1] * f;
-            o0 += sO[(w * 16 + r) * HD + d] * f;
-            o1 += sO[(w * 16 + r) * HD + d + 1] * f;
+            const float2 ov = *reinterpret_cast<const float2*>(&sO[(w * 16 + r) * HD + d]);
+            o0 += ov.x * f;
+            o1 += ov.y * f;
         }
         emit_pair<HD>(p, it, r, d, o0, o1, M, L);
     }
@@ -338,7 +362,7 @@ __global__ void attention_combine_kernel(const AttnParams p) {
 }
 
 template <int HD>
-cudaError_t launch_hd(const AttnParams& p, cudaStream_t st) {
+cudaError_t launch_hd(const AttnParams& p, const CUtensorMap& tk, const CUtensorMap& tv, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(attention_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -346,17 +370,22 @@ cudaError_t launch_hd(const AttnParams& p, cudaStream_t st) {
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    if (p.n_items > 0) attention_kernel<HD><<<p.n_items, kWarps * 32, AttnSmem<HD>::TOTAL, st>>>(p);
+    if (p.n_items > 0) attention_kernel<HD><<<p.n_items, kWarps * 32, AttnSmem<HD>::TOTAL, st>>>(p, tk, tv);
     return cudaGetLastError();
 }
 
 }  // namespace
 
-cudaError_t attention_launch(const AttnParams& p, cudaStream_t st) {
-    static_assert(AttnSmem<128>::TOTAL >= AttnSmem<128>::Q_BYTES + kWarps * 16 * 128 * 4 + kWarps * 16 * 8,
-                  "key-mode merge scratch must fit in the KV stages");
-    if (p.head_dim == 128) return launch_hd<128>(p, st);
-    if (p.head_dim == 64) return launch_hd<64>(p, st);
+bool attention_tmaps(CUtensorMap* tk, CUtensorMap* tv, const void* kc, const void* vc, int64_t total_rows, int hd) {
+    return make_tmap_2d(tk, kc, uint64_t(total_rows), uint64_t(hd), 16, 64) &&
+           make_tmap_2d(tv, vc, uint64_t(total_rows), uint64_t(hd), 16, 64);
+}
+
+cudaError_t attention_launch(const AttnParams& p, const CUtensorMap& tk, const CUtensorMap& tv, cudaStream_t st) {
+    static_assert(AttnSmem<128>::BAR_OFF - AttnSmem<128>::Q_BYTES >= kWarps * 16 * 128 * 4 + kWarps * 16 * 8,
+                  "key-mode merge scratch must fit in the K/V stages");
+    if (p.head_dim == 128) return launch_hd<128>(p, tk, tv, st);
+    if (p.head_dim == 64) return launch_hd<64>(p, tk, tv, st);
     return cudaErrorInvalidValue;
 }
 

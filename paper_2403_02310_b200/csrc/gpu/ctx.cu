@@ -120,6 +120,7 @@ struct ss_ctx {
     int32_t* next_tok = nullptr;
     float *part_o = nullptr, *part_ml = nullptr;
     CUtensorMap ta_xn, ta_o, ta_act, ta_xo;
+    CUtensorMap tm_k, tm_v;  // 2D TMA views of the paged K/V pools
 
     uint8_t* pinned = nullptr;
     size_t pinned_cap = 0;
@@ -438,6 +439,7 @@ AttnParams attn_params(const ss_ctx* ctx, const ss_batch* b, const bf16* q, bf16
     p.group = ctx->G;
     p.head_dim = ctx->hd;
     p.block_size = ctx->bs;
+    p.layer_row0 = int64_t(layer) * ctx->nblocks * ctx->nkv_l * ctx->bs;
     p.scale_log2 = float(1.0 / std::sqrt(double(ctx->hd)) * 1.4426950408889634);
     return p;
 }
@@ -487,7 +489,7 @@ ss_status enqueue_forward(ss_ctx* ctx, const ss_batch* b) {
                                       ctx->vc + size_t(l) * ctx->layer_stride, ctx->st);
         }));
         const AttnParams ap = attn_params(ctx, b, ctx->q, ctx->o, l);
-        RUN(launch(ctx, SS_K_ATTN, 1, [&] { return attention_launch(ap, ctx->st); }));
+        RUN(launch(ctx, SS_K_ATTN, 1, [&] { return attention_launch(ap, ctx->tm_k, ctx->tm_v, ctx->st); }));
         if (b->n_combs) RUN(launch(ctx, SS_K_ATTN_COMBINE, 1, [&] { return attention_combine_launch(ap, ctx->st); }));
         if (ctx->tp == 1) {
             RUN(gemm(ctx, SS_K_GEMM_O, ctx->ta_o, W.tb_o, T, h, qd, ctx->x, h, EPI_RESADD));
@@ -749,6 +751,8 @@ SS_API ss_status ss_kv_alloc(ss_ctx* ctx, int64_t num_blocks, int32_t block_size
     CK(cudaMemsetAsync(ctx->kc, 0, bytes, ctx->st));
     CK(cudaMemsetAsync(ctx->vc, 0, bytes, ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
+    if (!attention_tmaps(&ctx->tm_k, &ctx->tm_v, ctx->kc, ctx->vc, num_blocks * ctx->nkv_l * block_size * ctx->L, ctx->hd))
+        return fail(ctx, SS_CUDA_ERROR, "cuTensorMapEncodeTiled failed (KV pool)");
     ctx->nblocks = num_blocks;
     return SS_OK;
 }
@@ -882,7 +886,7 @@ SS_API ss_status ss_k_attention(ss_ctx* ctx, const ss_batch* b, const void* q, v
     if (!ctx || !b || layer < 0 || layer >= ctx->L) return fail(ctx, SS_INVALID_ARG, "bad attention args");
     if (ss_status s = ensure_workspace(ctx, b->T, std::max(b->n_out, 1), b->part_rows)) return s;
     const AttnParams ap = attn_params(ctx, b, static_cast<const bf16*>(q), static_cast<bf16*>(o), layer);
-    if (ss_status s = launch(ctx, SS_K_ATTN, 1, [&] { return attention_launch(ap, ctx->st); })) return s;
+    if (ss_status s = launch(ctx, SS_K_ATTN, 1, [&] { return attention_launch(ap, ctx->tm_k, ctx->tm_v, ctx->st); })) return s;
     if (b->n_combs) return launch(ctx, SS_K_ATTN_COMBINE, 1, [&] { return attention_combine_launch(ap, ctx->st); });
     return SS_OK;
 }

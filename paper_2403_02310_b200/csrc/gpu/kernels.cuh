@@ -69,8 +69,11 @@ struct AttnParams {
     int32_t n_combines;
     int32_t nq_l, nkv_l, group, head_dim, block_size;
     float scale_log2;            // softmax scale * log2(e)
+    int64_t layer_row0;          // first row of this layer in the 2D [rows][hd] TMA view of the cache
 };
-cudaError_t attention_launch(const AttnParams& p, cudaStream_t st);
+// 2D TMA views [L * nblocks * nkv * 16][hd] of the K and V pools (box 16 x 64, SWIZZLE_128B).
+bool attention_tmaps(CUtensorMap* tk, CUtensorMap* tv, const void* kc, const void* vc, int64_t total_rows, int hd);
+cudaError_t attention_launch(const AttnParams& p, const CUtensorMap& tk, const CUtensorMap& tv, cudaStream_t st);
 cudaError_t attention_combine_launch(const AttnParams& p, cudaStream_t st);
 
 // ------------------------------------------------------------------ K2/K4 elementwise
