@@ -70,9 +70,24 @@ struct Nccl {
 };
 Nccl g_nccl;
 
+// TMA maps of one weight matrix, one per B-tile box height (rows staged per CTA),
+// encoded on first use.
+struct WMaps {
+    const bf16* w = nullptr;
+    int64_t rows = 0, cols = 0;
+    CUtensorMap m[17];
+    bool ok[17] = {};
+    const CUtensorMap* get(int box_rows) {
+        const int i = box_rows / 16;
+        if (box_rows % 16 || i < 1 || i > 16) return nullptr;
+        if (!ok[i]) ok[i] = make_tmap_2d(&m[i], w, uint64_t(rows), uint64_t(cols), uint32_t(box_rows), 64);
+        return ok[i] ? &m[i] : nullptr;
+    }
+};
+
 struct Layer {
     bf16 *wqkv, *wo, *wgu, *wdown, *attn_norm, *mlp_norm;
-    CUtensorMap tb_qkv[2], tb_o[2], tb_gu[2], tb_down[2];  // B maps for BN = 128, 256
+    WMaps tb_qkv, tb_o, tb_gu, tb_down;
 };
 
 struct Prof {
@@ -105,7 +120,7 @@ struct ss_ctx {
     uint8_t* wmem = nullptr;
     std::vector<Layer> layers;
     bf16 *embed = nullptr, *lm_head = nullptr, *final_norm = nullptr;
-    CUtensorMap tb_lm[2];
+    WMaps tb_lm;
     float2* rope = nullptr;
 
     bf16 *kc = nullptr, *vc = nullptr;
@@ -220,9 +235,11 @@ ss_status init_weight(ss_ctx* ctx, bf16* w, int kind, int layer, int64_t rows, i
     return init_weight_launch(w, wi, ctx->st) == cudaSuccess ? SS_OK : fail(ctx, SS_CUDA_ERROR, "weight init launch");
 }
 
-bool bmaps(CUtensorMap (&m)[2], const bf16* w, int64_t rows, int64_t cols) {
-    return make_tmap_2d(&m[0], w, uint64_t(rows), uint64_t(cols), 128, 64) &&
-           make_tmap_2d(&m[1], w, uint64_t(rows), uint64_t(cols), 256, 64);
+bool bmaps(WMaps& m, const bf16* w, int64_t rows, int64_t cols) {
+    m.w = w;
+    m.rows = rows;
+    m.cols = cols;
+    return m.get(128) != nullptr;  // validates the encode path once up front
 }
 
 ss_status ensure_workspace(ss_ctx* ctx, int T, int n_out, int part_rows) {
@@ -444,8 +461,8 @@ AttnParams attn_params(const ss_ctx* ctx, const ss_batch* b, const bf16* q, bf16
     return p;
 }
 
-ss_status gemm(ss_ctx* ctx, int cls, const CUtensorMap& ta, const CUtensorMap (&tb)[2], int M, int N, int K,
-               void* out, int ldo, int epi) {
+ss_status gemm(ss_ctx* ctx, int cls, const CUtensorMap& ta, WMaps& tb, int M, int N, int K, void* out, int ldo,
+               int epi) {
     GemmPlan p;
     p.M = M;
     p.N = N;
@@ -454,10 +471,13 @@ ss_status gemm(ss_ctx* ctx, int cls, const CUtensorMap& ta, const CUtensorMap (&
     p.ldo = ldo;
     p.epi = epi;
     p.num_sms = ctx->num_sms;
-    p.bn = gemm_pick_bn(M, N, ctx->num_sms);
-    if (epi == EPI_SWIGLU && p.bn % 64) p.bn = 256;
+    const GemmShape s = gemm_pick(M, N, epi, ctx->num_sms);
+    p.cg = s.cg;
+    p.bn = s.bn;
     p.tmA = ta;
-    p.tmB = tb[p.bn == 256 ? 1 : 0];
+    const CUtensorMap* mb = tb.get(p.bn / p.cg);
+    if (!mb) return fail(ctx, SS_CUDA_ERROR, "cuTensorMapEncodeTiled failed (weight tile map)");
+    p.tmB = *mb;
     return launch(ctx, cls, 1, [&] { return gemm_launch(p, ctx->st); });
 }
 
@@ -479,7 +499,7 @@ ss_status enqueue_forward(ss_ctx* ctx, const ss_batch* b) {
         return s;
     RUN(launch(ctx, SS_K_EMBED, 1, [&] { return embed_launch(b->tokens, ctx->embed, ctx->x, T, h, ctx->st); }));
     for (int l = 0; l < ctx->L; ++l) {
-        const Layer& W = ctx->layers[size_t(l)];
+        Layer& W = ctx->layers[size_t(l)];
         RUN(launch(ctx, SS_K_RMSNORM, 1,
                    [&] { return rmsnorm_launch(ctx->x, W.attn_norm, ctx->xn, nullptr, T, h, eps, ctx->st); }));
         RUN(gemm(ctx, SS_K_GEMM_QKV, ctx->ta_xn, W.tb_qkv, T, qkvN, h, ctx->qkv, qkvN, EPI_BF16));

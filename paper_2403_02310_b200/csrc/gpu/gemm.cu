@@ -3,14 +3,19 @@
 //   D[M, N] = A[M, K] . B[N, K]^T      A = activations (bf16, K-major)
 //                                      B = weight shard (bf16, K-major)
 //
-// Persistent, warp-specialised tcgen05 kernel (one CTA per SM):
+// Persistent, warp-specialised tcgen05 kernel, one CTA per SM:
 //   warp 0       TMA producer: A/B tiles (SWIZZLE_128B) into a STAGES-deep ring
-//   warp 1       TMEM allocator + single-thread tcgen05.mma issuer (M=128,
-//                N=BN, K=16 per instruction, fp32 accumulators in TMEM)
+//   warp 1       TMEM allocator + single-thread tcgen05.mma issuer (fp32
+//                accumulators in TMEM, K = 16 per instruction)
 //   warps 2..5   epilogue: tcgen05.ld -> registers -> fused epilogue -> HBM
-// Accumulators are double-buffered in TMEM so tile i's epilogue overlaps tile
-// i+1's MMAs. The M tail (T = 481, 2017, ...) is handled by TMA zero fill on
-// load and row masking on store, so no padding to 128 is ever materialised.
+// CG = 2 runs CTA pairs (cluster of 2, tcgen05 cta_group::2): a 256 x BN tile
+// per pair, each CTA staging its own 128 rows of A and BN/2 rows of B, so the
+// per-SM shared-memory traffic per MMA is half that of a 1-CTA 128 x BN tile.
+// The leader CTA issues the MMAs; smem-slot and accumulator barriers are
+// multicast-committed to both CTAs. CG = 1 (128 x BN) serves small M (LM head,
+// decode-only batches). Accumulators are double-buffered in TMEM so a tile's
+// epilogue overlaps the next tile's MMAs. The M tail (T = 481, 2017, ...) is
+// handled by TMA zero fill on load and row masking on store.
 //
 // Fused epilogues (K4 work folded into K3):
 //   EPI_BF16    store bf16 D (QKV projection, TP partials)
@@ -27,27 +32,106 @@ namespace ssk {
 
 namespace {
 
-constexpr int BM = 128;
 constexpr int BK = 64;  // 128 B of bf16: one SWIZZLE_128B row
 constexpr int kThreads = 192;
+constexpr int kSmemBudget = 200 * 1024;
 
-template <int BN>
+template <int CG, int BN>
 struct GemmCfg {
-    static constexpr int STAGES = BN == 256 ? 4 : 6;
-    static constexpr int A_BYTES = BM * BK * 2;
-    static constexpr int B_BYTES = BN * BK * 2;
+    static constexpr int A_BYTES = 128 * BK * 2;       // this CTA's 128 rows of A
+    static constexpr int B_ROWS = BN / CG;             // this CTA's rows of B
+    static constexpr int B_BYTES = B_ROWS * BK * 2;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int TMEM_COLS = 2 * BN;  // double-buffered fp32 accumulators
+    static constexpr int STAGES_FIT = kSmemBudget / STAGE_BYTES;
+    static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
+    static constexpr int TMEM_COLS = 2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512);
     static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + 256;
+    static constexpr int TILE_M = 128 * CG;
 };
 
 __device__ __forceinline__ float silu(float g) { return g / (1.0f + __expf(-g)); }
 
-template <int BN, int EPI>
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of the same smem offset in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t peer_addr(const void* p, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// 2-SM TMA: data lands in this CTA, completion is signalled on the leader's mbarrier.
+__device__ __forceinline__ void tma_load_2d_cg2(void* smem_dst, const CUtensorMap* m, int32_t c0, int32_t c1,
+                                                uint32_t bar_cluster) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+        "%3}], [%4];" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(bar_cluster)
+        : "memory");
+}
+
+template <int CG>
+__device__ __forceinline__ void tmem_alloc_cg(uint32_t* slot, uint32_t cols_pow2);
+template <>
+__device__ __forceinline__ void tmem_alloc_cg<1>(uint32_t* slot, uint32_t cols) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot)), "r"(cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+template <>
+__device__ __forceinline__ void tmem_alloc_cg<2>(uint32_t* slot, uint32_t cols) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot)), "r"(cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+template <int CG>
+__device__ __forceinline__ void tmem_dealloc_cg(uint32_t taddr, uint32_t cols) {
+    if constexpr (CG == 1)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(cols) : "memory");
+    else
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(cols) : "memory");
+}
+template <int CG>
+__device__ __forceinline__ void mma_cg(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    if constexpr (CG == 1) {
+        umma_bf16(d, a, b, idesc, acc);
+    } else {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+            "l"(a), "l"(b), "r"(idesc), "r"(acc)
+            : "memory");
+    }
+}
+// Commit: arrive on `bar` (same smem offset) in every CTA of the group once the
+// issued MMAs retire.
+template <int CG>
+__device__ __forceinline__ void commit_cg(uint64_t* bar) {
+    if constexpr (CG == 1) {
+        umma_commit(bar);
+    } else {
+        asm volatile(
+            "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                smem_u32(bar)),
+            "h"(uint16_t(3))
+            : "memory");
+    }
+}
+
+template <int CG, int BN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
-                        int N, int K, void* __restrict__ out, int ldo, int num_m, int num_tiles) {
-    using Cfg = GemmCfg<BN>;
+                        int N, int K, void* __restrict__ out, int ldo, int num_mt, int num_tiles) {
+    using Cfg = GemmCfg<CG, BN>;
     constexpr int STAGES = Cfg::STAGES;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
@@ -63,6 +147,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
     const int num_kb = (K + BK - 1) / BK;
+    const uint32_t rank = CG == 2 ? cluster_rank() : 0;
+    const bool leader = rank == 0;
+    const int cid = blockIdx.x / CG, ncl = gridDim.x / CG;
 
     if (threadIdx.x == 0) {
         tma_prefetch(&tmA);
@@ -73,27 +160,37 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 4);  // one arrive per epilogue warp
+            mbar_init(&tempty[a], 4 * CG);  // every epilogue warp of the group
         }
         mbar_fence_init();
     }
-    if (warp == 1) tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
+    if (warp == 1) tmem_alloc_cg<CG>(tmem_slot, Cfg::TMEM_COLS);
     tc_fence_before();
-    __syncthreads();
+    if constexpr (CG == 2) cluster_sync();
+    else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
     if (warp == 0) {
-        if (lane == 0) {  // ---------------- TMA producer
+        if (lane == 0) {  // ---------------- TMA producer (both CTAs)
+            const uint32_t full_leader = CG == 2 ? peer_addr(full, 0) : 0;
             int s = 0;
             uint32_t ph = 0;
-            for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-                const int m0 = (t % num_m) * BM, n0 = (t / num_m) * BN;
+            for (int t = cid; t < num_tiles; t += ncl) {
+                const int m0 = (t % num_mt) * Cfg::TILE_M + 128 * int(rank);
+                const int n0 = (t / num_mt) * BN + Cfg::B_ROWS * int(rank);
                 for (int kb = 0; kb < num_kb; ++kb) {
                     mbar_wait(&empty[s], ph ^ 1);
-                    mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
-                    tma_load_2d(sA + s * Cfg::A_BYTES, &tmA, kb * BK, m0, &full[s]);
-                    tma_load_2d(sB + s * Cfg::B_BYTES, &tmB, kb * BK, n0, &full[s]);
+                    if constexpr (CG == 1) {
+                        mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
+                        tma_load_2d(sA + s * Cfg::A_BYTES, &tmA, kb * BK, m0, &full[s]);
+                        tma_load_2d(sB + s * Cfg::B_BYTES, &tmB, kb * BK, n0, &full[s]);
+                    } else {
+                        if (leader) mbar_arrive_expect_tx(&full[s], 2 * Cfg::STAGE_BYTES);
+                        const uint32_t fb = full_leader + uint32_t(s * 8);
+                        tma_load_2d_cg2(sA + s * Cfg::A_BYTES, &tmA, kb * BK, m0, fb);
+                        tma_load_2d_cg2(sB + s * Cfg::B_BYTES, &tmB, kb * BK, n0, fb);
+                    }
                     if (++s == STAGES) {
                         s = 0;
                         ph ^= 1;
@@ -102,13 +199,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {  // ---------------- MMA issuer
-            constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
+        if (lane == 0 && leader) {  // ---------------- MMA issuer (leader CTA only)
+            constexpr uint32_t idesc = umma_idesc_bf16(Cfg::TILE_M, BN);
             int s = 0;
             uint32_t ph = 0;
             int acc = 0;
             uint32_t acc_ph = 0;
-            for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+            for (int t = cid; t < num_tiles; t += ncl) {
                 mbar_wait(&tempty[acc], acc_ph ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + uint32_t(acc * BN);
@@ -119,15 +216,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint32_t b_addr = smem_u32(sB + s * Cfg::B_BYTES);
 #pragma unroll
                     for (int k = 0; k < BK / 16; ++k)
-                        umma_bf16(d_tmem, umma_desc_sw128(a_addr + 32 * k), umma_desc_sw128(b_addr + 32 * k), idesc,
-                                  (kb | k) != 0);
-                    umma_commit(&empty[s]);  // smem slot free once these MMAs retire
+                        mma_cg<CG>(d_tmem, umma_desc_sw128(a_addr + 32 * k), umma_desc_sw128(b_addr + 32 * k), idesc,
+                                   (kb | k) != 0);
+                    commit_cg<CG>(&empty[s]);  // smem slot free (in both CTAs) once these MMAs retire
                     if (++s == STAGES) {
                         s = 0;
                         ph ^= 1;
                     }
                 }
-                umma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+                commit_cg<CG>(&tfull[acc]);  // accumulator ready for both CTAs' epilogues
                 if (++acc == 2) {
                     acc = 0;
                     acc_ph ^= 1;
@@ -136,10 +233,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else {  // ---------------------------- epilogue warps 2..5
         const int q = warp & 3;  // TMEM lane quarter this warp may access
+        const uint32_t tempty_leader = CG == 2 ? peer_addr(tempty, 0) : 0;
         int acc = 0;
         uint32_t acc_ph = 0;
-        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-            const int m0 = (t % num_m) * BM, n0 = (t / num_m) * BN;
+        for (int t = cid; t < num_tiles; t += ncl) {
+            const int m0 = (t % num_mt) * Cfg::TILE_M + 128 * int(rank), n0 = (t / num_mt) * BN;
             const int row = m0 + q * 32 + lane;
             mbar_wait(&tfull[acc], acc_ph);
             tc_fence_after();
@@ -161,7 +259,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                                               silu(__uint_as_float(g[2 * j + 1])) * __uint_as_float(u[2 * j + 1]));
 #pragma unroll
                         for (int j = 0; j < 4; ++j)
-                            reinterpret_cast<uint4*>(o)[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+                            reinterpret_cast<uint4*>(o)[j] =
+                                make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
                     }
                 }
             } else {
@@ -204,7 +303,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (lane == 0) {
+                if constexpr (CG == 1) mbar_arrive(&tempty[acc]);
+                else mbar_arrive_cluster(tempty_leader + uint32_t(acc * 8));
+            }
             if (++acc == 2) {
                 acc = 0;
                 acc_ph ^= 1;
@@ -212,10 +314,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     }
     tc_fence_before();
-    __syncthreads();
+    if constexpr (CG == 2) cluster_sync();
+    else __syncthreads();
     if (warp == 1) {
         tc_fence_after();
-        tmem_dealloc<GemmCfg<BN>::TMEM_COLS>(tmem_base);
+        tmem_dealloc_cg<CG>(tmem_base, Cfg::TMEM_COLS);
     }
 }
 
@@ -235,23 +338,38 @@ EncodeFn encode_fn() {
     return fn;
 }
 
-template <int BN, int EPI>
+template <int CG, int BN, int EPI>
 cudaError_t launch_t(const GemmPlan& p, cudaStream_t st) {
-    using Cfg = GemmCfg<BN>;
+    using Cfg = GemmCfg<CG, BN>;
     static bool attr_set = false;
-    auto kern = gemm_tcgen05_kernel<BN, EPI>;
+    auto kern = gemm_tcgen05_kernel<CG, BN, EPI>;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
-    const int num_m = (p.M + BM - 1) / BM;
+    const int num_mt = (p.M + Cfg::TILE_M - 1) / Cfg::TILE_M;
     const int num_n = (p.N + BN - 1) / BN;
-    const int tiles = num_m * num_n;
-    const int grid = tiles < p.num_sms ? tiles : p.num_sms;
-    kern<<<grid, kThreads, Cfg::SMEM, st>>>(p.tmA, p.tmB, p.M, p.N, p.K, p.out, p.ldo, num_m, tiles);
-    return cudaGetLastError();
+    const int tiles = num_mt * num_n;
+    const int slots = p.num_sms / CG;
+    const int grid = CG * (tiles < slots ? tiles : slots);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = Cfg::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, p.tmA, p.tmB, p.M, p.N, p.K, p.out, p.ldo, num_mt, tiles);
 }
+
+// Tile shapes compiled: CG=2 pairs with BN in steps of 32, CG=1 with 128 / 256.
+constexpr int kBn2[] = {64, 96, 128, 160, 192, 224, 256};
 
 }  // namespace
 
@@ -268,17 +386,36 @@ bool make_tmap_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-int gemm_pick_bn(int M, int N, int num_sms) {
-    if (const char* f = getenv("SS_GEMM_BN")) {  // tuning override (dev only)
-        const int bn = atoi(f);
-        if (bn == 128 || bn == 256) return bn;
-    }
-    auto cost = [&](int bn) {
-        const long tiles = long((M + BM - 1) / BM) * ((N + bn - 1) / bn);
-        const long waves = (tiles + num_sms - 1) / num_sms;
-        return double(waves) * bn * (bn == 128 ? 1.08 : 1.0);  // small per-tile overhead penalty
+GemmShape gemm_pick(int M, int N, int epi, int num_sms) {
+    int force_bn = 0, force_cg = 0;
+    if (const char* f = getenv("SS_GEMM_BN")) force_bn = atoi(f);  // tuning overrides (dev only)
+    if (const char* f = getenv("SS_GEMM_CG")) force_cg = atoi(f);
+    const bool swiglu = epi == EPI_SWIGLU;
+    GemmShape best{1, 256};
+    double best_cost = 1e30;
+    auto consider = [&](int cg, int bn, double per_tile_overhead) {
+        if (swiglu && bn % 64) return;
+        if (force_bn && bn != force_bn) return;
+        if (force_cg && cg != force_cg) return;
+        const long tiles = long((M + 128 * cg - 1) / (128 * cg)) * ((N + bn - 1) / bn);
+        const long slots = num_sms / cg;
+        const long waves = (tiles + slots - 1) / slots;
+        // per-wave time ~ BN (MMA-bound) + a fixed tile cost; 1-CTA 128-wide tiles
+        // are shared-memory-bandwidth bound (measured ~1.35x slower per column)
+        const double cost = double(waves) * (bn + per_tile_overhead) * (cg == 1 && bn == 128 ? 1.35 : 1.0);
+        if (cost < best_cost) {
+            best_cost = cost;
+            best = GemmShape{cg, bn};
+        }
     };
-    return cost(128) < cost(256) ? 128 : 256;
+    if (M <= 128 || force_cg == 1) {
+        consider(1, 256, 32);
+        consider(1, 128, 32);
+    }
+    if (M > 128)
+        for (int bn : kBn2) consider(2, bn, 32);
+    if (best_cost == 1e30) best = GemmShape{M > 128 ? 2 : 1, swiglu ? 256 : 128};
+    return best;
 }
 
 bool gemm_prepare(GemmPlan& p, const void* A, uint64_t a_rows, const void* B, int M, int N, int K, void* out,
@@ -291,23 +428,31 @@ bool gemm_prepare(GemmPlan& p, const void* A, uint64_t a_rows, const void* B, in
     p.ldo = ldo;
     p.epi = epi;
     p.num_sms = num_sms;
-    p.bn = bn ? bn : gemm_pick_bn(M, N, num_sms);
-    if (!make_tmap_2d(&p.tmA, A, a_rows, uint64_t(K), BM, BK)) return false;
-    if (!make_tmap_2d(&p.tmB, B, uint64_t(N), uint64_t(K), uint32_t(p.bn), BK)) return false;
+    const GemmShape s = gemm_pick(M, N, epi, num_sms);
+    p.cg = s.cg;
+    p.bn = bn ? bn : s.bn;
+    if (!make_tmap_2d(&p.tmA, A, a_rows, uint64_t(K), 128, BK)) return false;
+    if (!make_tmap_2d(&p.tmB, B, uint64_t(N), uint64_t(K), uint32_t(p.bn / p.cg), BK)) return false;
     return true;
 }
 
 cudaError_t gemm_launch(const GemmPlan& p, cudaStream_t st) {
-#define SS_GEMM_CASE(BNv, E) \
-    if (p.bn == BNv && p.epi == E) return launch_t<BNv, E>(p, st);
-    SS_GEMM_CASE(128, EPI_BF16)
-    SS_GEMM_CASE(128, EPI_RESADD)
-    SS_GEMM_CASE(128, EPI_SWIGLU)
-    SS_GEMM_CASE(128, EPI_F32)
-    SS_GEMM_CASE(256, EPI_BF16)
-    SS_GEMM_CASE(256, EPI_RESADD)
-    SS_GEMM_CASE(256, EPI_SWIGLU)
-    SS_GEMM_CASE(256, EPI_F32)
+#define SS_GEMM_CASE(CGv, BNv)                                                      \
+    if (p.cg == CGv && p.bn == BNv) {                                               \
+        if (p.epi == EPI_BF16) return launch_t<CGv, BNv, EPI_BF16>(p, st);          \
+        if (p.epi == EPI_RESADD) return launch_t<CGv, BNv, EPI_RESADD>(p, st);      \
+        if (p.epi == EPI_F32) return launch_t<CGv, BNv, EPI_F32>(p, st);            \
+        if (p.epi == EPI_SWIGLU && BNv % 64 == 0) return launch_t<CGv, (BNv % 64 == 0 ? BNv : 64), EPI_SWIGLU>(p, st); \
+    }
+    SS_GEMM_CASE(1, 128)
+    SS_GEMM_CASE(1, 256)
+    SS_GEMM_CASE(2, 64)
+    SS_GEMM_CASE(2, 96)
+    SS_GEMM_CASE(2, 128)
+    SS_GEMM_CASE(2, 160)
+    SS_GEMM_CASE(2, 192)
+    SS_GEMM_CASE(2, 224)
+    SS_GEMM_CASE(2, 256)
 #undef SS_GEMM_CASE
     return cudaErrorInvalidValue;
 }

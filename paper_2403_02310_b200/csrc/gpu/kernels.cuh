@@ -17,13 +17,19 @@ struct GemmPlan {
     void* out = nullptr;
     int ldo = 0;
     int epi = 0;
-    int bn = 256;
+    int cg = 1;    // CTAs per MMA group (2: cta_group::2 pairs, 256-row tiles)
+    int bn = 256;  // tile N; each CTA stages bn / cg rows of B (the B map's box rows)
     int num_sms = 148;
 } __attribute__((aligned(64)));
 
+struct GemmShape {
+    int cg, bn;
+};
+
 bool make_tmap_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
                   uint32_t box_cols);
-int gemm_pick_bn(int M, int N, int num_sms);
+// Tile shape for an M x N GEMM: minimises wave-quantised time over the compiled shapes.
+GemmShape gemm_pick(int M, int N, int epi, int num_sms);
 // A is [a_rows >= M][K] bf16; B is [N][K] bf16; out row stride ldo elements.
 bool gemm_prepare(GemmPlan& p, const void* A, uint64_t a_rows, const void* B, int M, int N, int K, void* out,
                   int ldo, int epi, int num_sms, int bn = 0);
