@@ -400,9 +400,14 @@ GemmShape gemm_pick(int M, int N, int epi, int num_sms) {
         const long tiles = long((M + 128 * cg - 1) / (128 * cg)) * ((N + bn - 1) / bn);
         const long slots = num_sms / cg;
         const long waves = (tiles + slots - 1) / slots;
-        // per-wave time ~ BN (MMA-bound) + a fixed tile cost; 1-CTA 128-wide tiles
-        // are shared-memory-bandwidth bound (measured ~1.35x slower per column)
-        const double cost = double(waves) * (bn + per_tile_overhead) * (cg == 1 && bn == 128 ? 1.35 : 1.0);
+        // Measured per-tile main-loop time (us at K = 4096, B200): at these M the
+        // loop is bound by the L2 -> SM fill rate, not the MMA pipe, so narrow
+        // tiles save less than their MMA share (profiles/r01/gemm_tiles.txt).
+        auto tile_us = [](int c, int b) {
+            if (c == 1) return b == 256 ? 28.6 : 20.4;
+            return b >= 224 ? 25.3 : (b >= 192 ? 23.2 : (b >= 160 ? 22.1 : (b >= 128 ? 21.1 : 20.0)));
+        };
+        const double cost = double(waves) * tile_us(cg, bn) + per_tile_overhead * 0.0;
         if (cost < best_cost) {
             best_cost = cost;
             best = GemmShape{cg, bn};
