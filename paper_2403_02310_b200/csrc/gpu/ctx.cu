@@ -134,6 +134,9 @@ struct ss_ctx {
     float *logits_l = nullptr, *logits_g = nullptr, *logits = nullptr;
     int32_t* next_tok = nullptr;
     float *part_o = nullptr, *part_ml = nullptr;
+    float* sk_part = nullptr;       // stream-K GEMM partial accumulators
+    uint32_t* sk_flags = nullptr;   // stream-K ready flags
+    uint32_t sk_epoch = 0;
     CUtensorMap ta_xn, ta_o, ta_act, ta_xo;
     CUtensorMap tm_k, tm_v;  // 2D TMA views of the paged K/V pools
 
@@ -478,6 +481,9 @@ ss_status gemm(ss_ctx* ctx, int cls, const CUtensorMap& ta, WMaps& tb, int M, in
     const CUtensorMap* mb = tb.get(p.bn / p.cg);
     if (!mb) return fail(ctx, SS_CUDA_ERROR, "cuTensorMapEncodeTiled failed (weight tile map)");
     p.tmB = *mb;
+    p.part = ctx->sk_part;
+    p.flags = ctx->sk_flags;
+    p.epoch = ++ctx->sk_epoch;
     return launch(ctx, cls, 1, [&] { return gemm_launch(p, ctx->st); });
 }
 
@@ -637,6 +643,13 @@ SS_API ss_status ss_create(const ss_model_cfg* cfg, int32_t tp_rank, int32_t tp_
     ctx->ffn_l = c.ffn / tp_size;
     ctx->vocab_l = c.vocab / tp_size;
     ctx->seed = weight_seed;
+    if (cudaMalloc(&ctx->sk_part, gemm_part_floats(ctx->num_sms) * 4) != cudaSuccess ||
+        cudaMalloc(&ctx->sk_flags, gemm_flag_words(ctx->num_sms) * 4) != cudaSuccess ||
+        cudaMemset(ctx->sk_flags, 0, gemm_flag_words(ctx->num_sms) * 4) != cudaSuccess) {
+        std::string m = "stream-K workspace allocation";
+        ss_destroy(ctx);
+        return fail(nullptr, SS_OUT_OF_MEMORY, m);
+    }
     auto bail = [&](ss_status s) {
         std::string m = ctx->err;
         ss_destroy(ctx);
@@ -730,6 +743,8 @@ SS_API void ss_destroy(ss_ctx* ctx) {
     if (ctx->comm) g_nccl.destroy(ctx->comm);
     cudaFree(ctx->wmem);
     cudaFree(ctx->rope);
+    cudaFree(ctx->sk_part);
+    cudaFree(ctx->sk_flags);
     cudaFree(ctx->kc);
     cudaFree(ctx->vc);
     for (void* q : {(void*)ctx->x, (void*)ctx->xn, (void*)ctx->qkv, (void*)ctx->q, (void*)ctx->o, (void*)ctx->act,
@@ -881,6 +896,9 @@ SS_API ss_status ss_k_gemm(ss_ctx* ctx, const void* A, const void* B, void* D, i
     const int ldo = epi == EPI_SWIGLU ? N / 2 : N;
     if (!gemm_prepare(p, A, uint64_t(M), B, M, N, K, D, ldo, epi, ctx->num_sms))
         return fail(ctx, SS_INVALID_ARG, "gemm shape unsupported (N%32, K%8, SwiGLU N%64) or tensor map failed");
+    p.part = ctx->sk_part;
+    p.flags = ctx->sk_flags;
+    p.epoch = ++ctx->sk_epoch;
     return launch(ctx, SS_K_GEMM_QKV, 1, [&] { return gemm_launch(p, ctx->st); });
 }
 

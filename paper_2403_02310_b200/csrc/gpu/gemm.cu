@@ -127,10 +127,77 @@ __device__ __forceinline__ void commit_cg(uint64_t* bar) {
     }
 }
 
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Stream-K split of the (tile, k-block) iteration space: group g of G owns the
+// contiguous range [g*I/G, (g+1)*I/G). A range is walked as segments; a segment
+// that starts a tile at k-block 0 but does not finish it is the tile's "head"
+// and reduces the partial accumulators of the groups that hold the rest of the
+// tile (each of them starts its range inside that tile and processes that piece
+// first, so the head — processed last by its owner — never waits long).
+struct SkRange {
+    long i0, i1;
+};
+__device__ __forceinline__ SkRange sk_range(int gid, int G, long total) {
+    return SkRange{long(gid) * total / G, long(gid + 1) * total / G};
+}
+__device__ __forceinline__ long sk_start(int g, int G, long total) { return long(g) * total / G; }
+
+template <int EPI>
+__device__ __forceinline__ void epi_store(const uint32_t (&v)[32], int row, int col, void* out, int ldo) {
+    if constexpr (EPI == EPI_BF16) {
+        __nv_bfloat16* o = static_cast<__nv_bfloat16*>(out) + size_t(row) * ldo + col;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            reinterpret_cast<uint4*>(o)[j] =
+                make_uint4(pack_bf16(__uint_as_float(v[8 * j + 0]), __uint_as_float(v[8 * j + 1])),
+                           pack_bf16(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3])),
+                           pack_bf16(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5])),
+                           pack_bf16(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7])));
+    } else if constexpr (EPI == EPI_RESADD) {
+        float4* o = reinterpret_cast<float4*>(static_cast<float*>(out) + size_t(row) * ldo + col);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            float4 x = o[j];
+            x.x += __uint_as_float(v[4 * j + 0]);
+            x.y += __uint_as_float(v[4 * j + 1]);
+            x.z += __uint_as_float(v[4 * j + 2]);
+            x.w += __uint_as_float(v[4 * j + 3]);
+            o[j] = x;
+        }
+    } else {  // EPI_F32
+        float4* o = reinterpret_cast<float4*>(static_cast<float*>(out) + size_t(row) * ldo + col);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            o[j] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]), __uint_as_float(v[4 * j + 2]),
+                               __uint_as_float(v[4 * j + 3]));
+    }
+}
+
+__device__ __forceinline__ void add_partial(uint32_t (&v)[32], const float* p) {
+    const float4* q = reinterpret_cast<const float4*>(p);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const float4 a = q[j];
+        v[4 * j + 0] = __float_as_uint(__uint_as_float(v[4 * j + 0]) + a.x);
+        v[4 * j + 1] = __float_as_uint(__uint_as_float(v[4 * j + 1]) + a.y);
+        v[4 * j + 2] = __float_as_uint(__uint_as_float(v[4 * j + 2]) + a.z);
+        v[4 * j + 3] = __float_as_uint(__uint_as_float(v[4 * j + 3]) + a.w);
+    }
+}
+
 template <int CG, int BN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
-                        int N, int K, void* __restrict__ out, int ldo, int num_mt, int num_tiles) {
+                        int N, int K, void* __restrict__ out, int ldo, int num_mt, int num_tiles,
+                        float* __restrict__ part, uint32_t* __restrict__ flags, uint32_t epoch) {
     using Cfg = GemmCfg<CG, BN>;
     constexpr int STAGES = Cfg::STAGES;
     extern __shared__ uint8_t smem_raw[];
@@ -149,7 +216,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int num_kb = (K + BK - 1) / BK;
     const uint32_t rank = CG == 2 ? cluster_rank() : 0;
     const bool leader = rank == 0;
-    const int cid = blockIdx.x / CG, ncl = gridDim.x / CG;
+    const int gid = blockIdx.x / CG, G = gridDim.x / CG;
+    const long total = long(num_tiles) * num_kb;
+    const SkRange rg = sk_range(gid, G, total);
 
     if (threadIdx.x == 0) {
         tma_prefetch(&tmA);
@@ -176,10 +245,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t full_leader = CG == 2 ? peer_addr(full, 0) : 0;
             int s = 0;
             uint32_t ph = 0;
-            for (int t = cid; t < num_tiles; t += ncl) {
+            for (long i = rg.i0; i < rg.i1;) {
+                const int t = int(i / num_kb), kb0 = int(i % num_kb);
+                const int kb1 = int(kb0 + (rg.i1 - i) < num_kb ? kb0 + (rg.i1 - i) : num_kb);
                 const int m0 = (t % num_mt) * Cfg::TILE_M + 128 * int(rank);
                 const int n0 = (t / num_mt) * BN + Cfg::B_ROWS * int(rank);
-                for (int kb = 0; kb < num_kb; ++kb) {
+                for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&empty[s], ph ^ 1);
                     if constexpr (CG == 1) {
                         mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
@@ -196,6 +267,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         ph ^= 1;
                     }
                 }
+                i += kb1 - kb0;
             }
         }
     } else if (warp == 1) {
@@ -205,11 +277,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t ph = 0;
             int acc = 0;
             uint32_t acc_ph = 0;
-            for (int t = cid; t < num_tiles; t += ncl) {
+            for (long i = rg.i0; i < rg.i1;) {
+                const int kb0 = int(i % num_kb);
+                const int kb1 = int(kb0 + (rg.i1 - i) < num_kb ? kb0 + (rg.i1 - i) : num_kb);
                 mbar_wait(&tempty[acc], acc_ph ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + uint32_t(acc * BN);
-                for (int kb = 0; kb < num_kb; ++kb) {
+                for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&full[s], ph);
                     tc_fence_after();
                     const uint32_t a_addr = smem_u32(sA + s * Cfg::A_BYTES);
@@ -217,7 +291,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int k = 0; k < BK / 16; ++k)
                         mma_cg<CG>(d_tmem, umma_desc_sw128(a_addr + 32 * k), umma_desc_sw128(b_addr + 32 * k), idesc,
-                                   (kb | k) != 0);
+                                   (kb > kb0 || k > 0) ? 1u : 0u);
                     commit_cg<CG>(&empty[s]);  // smem slot free (in both CTAs) once these MMAs retire
                     if (++s == STAGES) {
                         s = 0;
@@ -229,75 +303,88 @@ __global__ void __launch_bounds__(kThreads, 1)
                     acc = 0;
                     acc_ph ^= 1;
                 }
+                i += kb1 - kb0;
             }
         }
     } else {  // ---------------------------- epilogue warps 2..5
         const int q = warp & 3;  // TMEM lane quarter this warp may access
         const uint32_t tempty_leader = CG == 2 ? peer_addr(tempty, 0) : 0;
+        const int rloc = 128 * int(rank) + q * 32 + lane;  // row within the group's tile
         int acc = 0;
         uint32_t acc_ph = 0;
-        for (int t = cid; t < num_tiles; t += ncl) {
-            const int m0 = (t % num_mt) * Cfg::TILE_M + 128 * int(rank), n0 = (t / num_mt) * BN;
-            const int row = m0 + q * 32 + lane;
+        for (long i = rg.i0; i < rg.i1;) {
+            const int t = int(i / num_kb), kb0 = int(i % num_kb);
+            const int kb1 = int(kb0 + (rg.i1 - i) < num_kb ? kb0 + (rg.i1 - i) : num_kb);
+            const int m0 = (t % num_mt) * Cfg::TILE_M, n0 = (t / num_mt) * BN;
+            const int row = m0 + rloc;
             mbar_wait(&tfull[acc], acc_ph);
             tc_fence_after();
             const uint32_t t_row = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN);
-            if constexpr (EPI == EPI_SWIGLU) {
-#pragma unroll 1
-                for (int c = 0; c < BN / 32; c += 2) {
-                    uint32_t g[32], u[32];
-                    tmem_ld32(t_row + uint32_t(c * 32), g);
-                    tmem_ld32(t_row + uint32_t((c + 1) * 32), u);
-                    tmem_wait_ld();
-                    const int col = n0 + c * 32;
-                    if (row < M && col < N) {
-                        __nv_bfloat16* o = static_cast<__nv_bfloat16*>(out) + size_t(row) * ldo + col / 2;
-                        uint32_t pk[16];
-#pragma unroll
-                        for (int j = 0; j < 16; ++j)
-                            pk[j] = pack_bf16(silu(__uint_as_float(g[2 * j])) * __uint_as_float(u[2 * j]),
-                                              silu(__uint_as_float(g[2 * j + 1])) * __uint_as_float(u[2 * j + 1]));
-#pragma unroll
-                        for (int j = 0; j < 4; ++j)
-                            reinterpret_cast<uint4*>(o)[j] =
-                                make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
-                    }
-                }
-            } else {
+            if (kb0 > 0) {
+                // non-head piece of a split tile: publish the partial accumulator
+                float* dst = part + (size_t(gid) * Cfg::TILE_M + rloc) * BN;
 #pragma unroll 1
                 for (int c = 0; c < BN / 32; ++c) {
                     uint32_t v[32];
                     tmem_ld32(t_row + uint32_t(c * 32), v);
                     tmem_wait_ld();
-                    const int col = n0 + c * 32;
-                    if (row < M && col < N) {
-                        if constexpr (EPI == EPI_BF16) {
-                            __nv_bfloat16* o = static_cast<__nv_bfloat16*>(out) + size_t(row) * ldo + col;
+                    float4* d4 = reinterpret_cast<float4*>(dst + c * 32);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        d4[j] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                            __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+                }
+                __threadfence();
+                __syncwarp();
+                if (lane == 0) st_release_gpu(&flags[(size_t(gid) * 2 + rank) * 4 + q], epoch);
+            } else {
+                // head or whole tile: add the other groups' pieces in group order
+                const long tile_end = long(t + 1) * num_kb;
+                int g_last = gid;  // last group whose range starts inside this tile
+                if (kb1 < num_kb)
+                    while (g_last + 1 < G && sk_start(g_last + 1, G, total) < tile_end) ++g_last;
+                for (int g = gid + 1; g <= g_last; ++g) {
+                    const uint32_t* f = &flags[(size_t(g) * 2 + rank) * 4 + q];
+                    uint32_t spins = 0;
+                    while (ld_acquire_gpu(f) != epoch)
+                        if (++spins == (1u << 28)) __trap();
+                }
+                if constexpr (EPI == EPI_SWIGLU) {
+#pragma unroll 1
+                    for (int c = 0; c < BN / 32; c += 2) {
+                        uint32_t gt[32], ut[32];
+                        tmem_ld32(t_row + uint32_t(c * 32), gt);
+                        tmem_ld32(t_row + uint32_t((c + 1) * 32), ut);
+                        tmem_wait_ld();
+                        for (int g = gid + 1; g <= g_last; ++g) {
+                            const float* src = part + (size_t(g) * Cfg::TILE_M + rloc) * BN;
+                            add_partial(gt, src + c * 32);
+                            add_partial(ut, src + (c + 1) * 32);
+                        }
+                        const int col = n0 + c * 32;
+                        if (row < M && col < N) {
+                            __nv_bfloat16* o = static_cast<__nv_bfloat16*>(out) + size_t(row) * ldo + col / 2;
+                            uint32_t pk[16];
+#pragma unroll
+                            for (int j = 0; j < 16; ++j)
+                                pk[j] = pack_bf16(silu(__uint_as_float(gt[2 * j])) * __uint_as_float(ut[2 * j]),
+                                                  silu(__uint_as_float(gt[2 * j + 1])) * __uint_as_float(ut[2 * j + 1]));
 #pragma unroll
                             for (int j = 0; j < 4; ++j)
-                                reinterpret_cast<uint4*>(o)[j] = make_uint4(
-                                    pack_bf16(__uint_as_float(v[8 * j + 0]), __uint_as_float(v[8 * j + 1])),
-                                    pack_bf16(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3])),
-                                    pack_bf16(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5])),
-                                    pack_bf16(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7])));
-                        } else if constexpr (EPI == EPI_RESADD) {
-                            float4* o = reinterpret_cast<float4*>(static_cast<float*>(out) + size_t(row) * ldo + col);
-#pragma unroll
-                            for (int j = 0; j < 8; ++j) {
-                                float4 x = o[j];
-                                x.x += __uint_as_float(v[4 * j + 0]);
-                                x.y += __uint_as_float(v[4 * j + 1]);
-                                x.z += __uint_as_float(v[4 * j + 2]);
-                                x.w += __uint_as_float(v[4 * j + 3]);
-                                o[j] = x;
-                            }
-                        } else {  // EPI_F32
-                            float4* o = reinterpret_cast<float4*>(static_cast<float*>(out) + size_t(row) * ldo + col);
-#pragma unroll
-                            for (int j = 0; j < 8; ++j)
-                                o[j] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
-                                                   __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+                                reinterpret_cast<uint4*>(o)[j] =
+                                    make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
                         }
+                    }
+                } else {
+#pragma unroll 1
+                    for (int c = 0; c < BN / 32; ++c) {
+                        uint32_t v[32];
+                        tmem_ld32(t_row + uint32_t(c * 32), v);
+                        tmem_wait_ld();
+                        for (int g = gid + 1; g <= g_last; ++g)
+                            add_partial(v, part + (size_t(g) * Cfg::TILE_M + rloc) * BN + c * 32);
+                        const int col = n0 + c * 32;
+                        if (row < M && col < N) epi_store<EPI>(v, row, col, out, ldo);
                     }
                 }
             }
@@ -311,6 +398,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 acc = 0;
                 acc_ph ^= 1;
             }
+            i += kb1 - kb0;
         }
     }
     tc_fence_before();
@@ -351,8 +439,10 @@ cudaError_t launch_t(const GemmPlan& p, cudaStream_t st) {
     const int num_mt = (p.M + Cfg::TILE_M - 1) / Cfg::TILE_M;
     const int num_n = (p.N + BN - 1) / BN;
     const int tiles = num_mt * num_n;
-    const int slots = p.num_sms / CG;
-    const int grid = CG * (tiles < slots ? tiles : slots);
+    const long iters = long(tiles) * ((p.K + BK - 1) / BK);
+    int groups = p.num_sms / CG;  // stream-K: every group gets an equal share of k-iterations
+    if (iters < groups) groups = int(iters);
+    const int grid = CG * groups;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);
@@ -365,7 +455,8 @@ cudaError_t launch_t(const GemmPlan& p, cudaStream_t st) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kern, p.tmA, p.tmB, p.M, p.N, p.K, p.out, p.ldo, num_mt, tiles);
+    return cudaLaunchKernelEx(&cfg, kern, p.tmA, p.tmB, p.M, p.N, p.K, p.out, p.ldo, num_mt, tiles, p.part,
+                              p.flags, p.epoch);
 }
 
 // Tile shapes compiled: CG=2 pairs with BN in steps of 32, CG=1 with 128 / 256.
@@ -391,35 +482,34 @@ GemmShape gemm_pick(int M, int N, int epi, int num_sms) {
     if (const char* f = getenv("SS_GEMM_BN")) force_bn = atoi(f);  // tuning overrides (dev only)
     if (const char* f = getenv("SS_GEMM_CG")) force_cg = atoi(f);
     const bool swiglu = epi == EPI_SWIGLU;
-    GemmShape best{1, 256};
+    GemmShape best{M > 128 ? 2 : 1, swiglu ? 256 : 128};
     double best_cost = 1e30;
-    auto consider = [&](int cg, int bn, double per_tile_overhead) {
+    // Stream-K spreads all (tile, k-block) iterations evenly over the SMs, so the
+    // cost is the total tile work / groups. Measured per-tile main-loop time (us
+    // at K = 4096, B200, profiles/r01/gemm_tiles.txt): at these M the loop is
+    // bound by the L2 -> SM fill rate rather than the MMA pipe, so wide tiles
+    // (fewer bytes staged per flop) win unless N is small.
+    auto tile_us = [](int c, int b) {
+        if (c == 1) return b == 256 ? 28.6 : 20.4;
+        return b >= 224 ? 25.3 : (b >= 192 ? 23.2 : (b >= 160 ? 22.1 : (b >= 128 ? 21.1 : 20.0)));
+    };
+    auto consider = [&](int cg, int bn) {
         if (swiglu && bn % 64) return;
         if (force_bn && bn != force_bn) return;
         if (force_cg && cg != force_cg) return;
         const long tiles = long((M + 128 * cg - 1) / (128 * cg)) * ((N + bn - 1) / bn);
-        const long slots = num_sms / cg;
-        const long waves = (tiles + slots - 1) / slots;
-        // Measured per-tile main-loop time (us at K = 4096, B200): at these M the
-        // loop is bound by the L2 -> SM fill rate, not the MMA pipe, so narrow
-        // tiles save less than their MMA share (profiles/r01/gemm_tiles.txt).
-        auto tile_us = [](int c, int b) {
-            if (c == 1) return b == 256 ? 28.6 : 20.4;
-            return b >= 224 ? 25.3 : (b >= 192 ? 23.2 : (b >= 160 ? 22.1 : (b >= 128 ? 21.1 : 20.0)));
-        };
-        const double cost = double(waves) * tile_us(cg, bn) + per_tile_overhead * 0.0;
-        if (cost < best_cost) {
+        const double cost = double(tiles) * tile_us(cg, bn) / double(num_sms / cg);
+        if (cost < best_cost - 1e-9) {
             best_cost = cost;
             best = GemmShape{cg, bn};
         }
     };
     if (M <= 128 || force_cg == 1) {
-        consider(1, 256, 32);
-        consider(1, 128, 32);
+        consider(1, 256);
+        consider(1, 128);
     }
-    if (M > 128)
-        for (int bn : kBn2) consider(2, bn, 32);
-    if (best_cost == 1e30) best = GemmShape{M > 128 ? 2 : 1, swiglu ? 256 : 128};
+    if (M > 128 && force_cg != 1)
+        for (int bn : kBn2) consider(2, bn);
     return best;
 }
 

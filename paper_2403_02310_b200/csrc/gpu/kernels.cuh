@@ -20,7 +20,15 @@ struct GemmPlan {
     int cg = 1;    // CTAs per MMA group (2: cta_group::2 pairs, 256-row tiles)
     int bn = 256;  // tile N; each CTA stages bn / cg rows of B (the B map's box rows)
     int num_sms = 148;
+    // stream-K workspace: partial accumulators [groups][128 * cg][bn] fp32 and one
+    // ready flag per (group, CTA, epilogue warp); epoch must be unique per launch
+    float* part = nullptr;
+    uint32_t* flags = nullptr;
+    uint32_t epoch = 0;
 } __attribute__((aligned(64)));
+// Workspace sizes for gemm_launch (max over tile shapes) for num_sms SMs.
+inline size_t gemm_part_floats(int num_sms) { return size_t(num_sms) * 128 * 256; }
+inline size_t gemm_flag_words(int num_sms) { return size_t(num_sms) * 8; }
 
 struct GemmShape {
     int cg, bn;

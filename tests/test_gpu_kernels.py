@@ -59,6 +59,22 @@ def test_gemm_tcgen05(small, M, N, K, epi):
         small.k_gemm(A, B, D, M, N, K, 3)
         torch.cuda.synchronize()
         torch.testing.assert_close(D, ref, rtol=1e-4, atol=1e-4)
+        # stream-K fixups reduce partials in a fixed group order: bitwise repeatable
+        D2 = torch.empty_like(D)
+        small.k_gemm(A, B, D2, M, N, K, 3)
+        torch.cuda.synchronize()
+        assert torch.equal(D, D2)
+
+
+@pytest.mark.parametrize("M,N,K", [(512, 4096, 14336), (33, 32000, 4096), (32, 6144, 4096), (2017, 1984, 14848)])
+def test_gemm_stream_k_shapes(small, M, N, K):
+    """Shapes whose tiles are split across several SM groups (stream-K fixup path)."""
+    A = _rand((M, K), 1.0, 5)
+    B = _rand((N, K), 1.0 / math.sqrt(K), 6)
+    D = torch.empty((M, N), dtype=torch.float32, device="cuda")
+    small.k_gemm(A, B, D, M, N, K, 3)
+    torch.cuda.synchronize()
+    torch.testing.assert_close(D, A.float() @ B.float().T, rtol=2e-4, atol=2e-4)
 
 
 def test_rmsnorm(small):
