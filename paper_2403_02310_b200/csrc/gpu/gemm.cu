@@ -150,6 +150,33 @@ __device__ __forceinline__ SkRange sk_range(int gid, int G, long total) {
 }
 __device__ __forceinline__ long sk_start(int g, int G, long total) { return long(g) * total / G; }
 
+// Work segments of one group. mode 0: whole tiles round-robin (tile g, g+G, ...:
+// concurrently active tiles are neighbours, so B/A tiles are shared in L2);
+// mode 1: the group's stream-K range cut at tile boundaries.
+struct Seg {
+    int t, kb0, kb1;
+};
+struct SegIter {
+    int mode, G, num_kb, num_tiles, t_rr;
+    long i, i1;
+    __device__ SegIter(int m, int gid, int G_, int nkb, int nt, SkRange r)
+        : mode(m), G(G_), num_kb(nkb), num_tiles(nt), t_rr(gid), i(r.i0), i1(r.i1) {}
+    __device__ __forceinline__ bool next(Seg& s) {
+        if (mode == 0) {
+            if (t_rr >= num_tiles) return false;
+            s = Seg{t_rr, 0, num_kb};
+            t_rr += G;
+            return true;
+        }
+        if (i >= i1) return false;
+        s.t = int(i / num_kb);
+        s.kb0 = int(i % num_kb);
+        s.kb1 = int(s.kb0 + (i1 - i) < num_kb ? s.kb0 + (i1 - i) : num_kb);
+        i += s.kb1 - s.kb0;
+        return true;
+    }
+};
+
 template <int EPI>
 __device__ __forceinline__ void epi_store(const uint32_t (&v)[32], int row, int col, void* out, int ldo) {
     if constexpr (EPI == EPI_BF16) {
@@ -197,7 +224,7 @@ template <int CG, int BN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
                         int N, int K, void* __restrict__ out, int ldo, int num_mt, int num_tiles,
-                        float* __restrict__ part, uint32_t* __restrict__ flags, uint32_t epoch) {
+                        float* __restrict__ part, uint32_t* __restrict__ flags, uint32_t epoch, int sk_mode) {
     using Cfg = GemmCfg<CG, BN>;
     constexpr int STAGES = Cfg::STAGES;
     extern __shared__ uint8_t smem_raw[];
@@ -245,9 +272,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t full_leader = CG == 2 ? peer_addr(full, 0) : 0;
             int s = 0;
             uint32_t ph = 0;
-            for (long i = rg.i0; i < rg.i1;) {
-                const int t = int(i / num_kb), kb0 = int(i % num_kb);
-                const int kb1 = int(kb0 + (rg.i1 - i) < num_kb ? kb0 + (rg.i1 - i) : num_kb);
+            SegIter sit(sk_mode, gid, G, num_kb, num_tiles, rg);
+            for (Seg sg; sit.next(sg);) {
+                const int t = sg.t, kb0 = sg.kb0, kb1 = sg.kb1;
                 const int m0 = (t % num_mt) * Cfg::TILE_M + 128 * int(rank);
                 const int n0 = (t / num_mt) * BN + Cfg::B_ROWS * int(rank);
                 for (int kb = kb0; kb < kb1; ++kb) {
@@ -267,7 +294,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                         ph ^= 1;
                     }
                 }
-                i += kb1 - kb0;
             }
         }
     } else if (warp == 1) {
@@ -277,9 +303,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t ph = 0;
             int acc = 0;
             uint32_t acc_ph = 0;
-            for (long i = rg.i0; i < rg.i1;) {
-                const int kb0 = int(i % num_kb);
-                const int kb1 = int(kb0 + (rg.i1 - i) < num_kb ? kb0 + (rg.i1 - i) : num_kb);
+            SegIter sit(sk_mode, gid, G, num_kb, num_tiles, rg);
+            for (Seg sg; sit.next(sg);) {
+                const int kb0 = sg.kb0, kb1 = sg.kb1;
                 mbar_wait(&tempty[acc], acc_ph ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + uint32_t(acc * BN);
@@ -303,7 +329,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                     acc = 0;
                     acc_ph ^= 1;
                 }
-                i += kb1 - kb0;
             }
         }
     } else {  // ---------------------------- epilogue warps 2..5
@@ -312,9 +337,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int rloc = 128 * int(rank) + q * 32 + lane;  // row within the group's tile
         int acc = 0;
         uint32_t acc_ph = 0;
-        for (long i = rg.i0; i < rg.i1;) {
-            const int t = int(i / num_kb), kb0 = int(i % num_kb);
-            const int kb1 = int(kb0 + (rg.i1 - i) < num_kb ? kb0 + (rg.i1 - i) : num_kb);
+        SegIter sit(sk_mode, gid, G, num_kb, num_tiles, rg);
+        for (Seg sg; sit.next(sg);) {
+            const int t = sg.t, kb0 = sg.kb0, kb1 = sg.kb1;
             const int m0 = (t % num_mt) * Cfg::TILE_M, n0 = (t / num_mt) * BN;
             const int row = m0 + rloc;
             mbar_wait(&tfull[acc], acc_ph);
@@ -398,7 +423,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                 acc = 0;
                 acc_ph ^= 1;
             }
-            i += kb1 - kb0;
         }
     }
     tc_fence_before();
@@ -440,9 +464,6 @@ cudaError_t launch_t(const GemmPlan& p, cudaStream_t st) {
     const int num_n = (p.N + BN - 1) / BN;
     const int tiles = num_mt * num_n;
     const long iters = long(tiles) * ((p.K + BK - 1) / BK);
-    int groups = p.num_sms / CG;  // stream-K: every group gets an equal share of k-iterations
-    if (iters < groups) groups = int(iters);
-    const int grid = CG * groups;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);
@@ -455,8 +476,28 @@ cudaError_t launch_t(const GemmPlan& p, cudaStream_t st) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    // Groups that can be co-resident: stream-K heads spin on other groups, so the
+    // grid must never exceed one resident wave.
+    static int resident = 0;
+    if (resident == 0) {
+        cfg.gridDim = dim3(CG * (p.num_sms / CG));
+        int n = 0;
+        if (CG > 1 && cudaOccupancyMaxActiveClusters(&n, kern, &cfg) == cudaSuccess && n > 0) resident = n;
+        else resident = p.num_sms / CG;
+        if (resident > p.num_sms / CG) resident = p.num_sms / CG;
+    }
+    int mode = p.sk_mode;
+    if (mode < 0) mode = tiles % resident == 0 || tiles > 6 * resident ? 0 : 1;  // stream-K only for ragged waves
+    if (const char* f = getenv("SS_GEMM_SK")) mode = atoi(f) ? 1 : 0;
+    int groups = resident;
+    if (mode == 0 && tiles < groups) groups = tiles;
+    if (mode == 1 && iters < groups) groups = int(iters);
+    cfg.gridDim = dim3(CG * groups);
+    if (getenv("SS_GEMM_DEBUG"))
+        fprintf(stderr, "gemm cg=%d bn=%d epi=%d M=%d N=%d K=%d tiles=%d resident=%d mode=%d groups=%d\n", CG, BN,
+                EPI, p.M, p.N, p.K, tiles, resident, mode, groups);
     return cudaLaunchKernelEx(&cfg, kern, p.tmA, p.tmB, p.M, p.N, p.K, p.out, p.ldo, num_mt, tiles, p.part,
-                              p.flags, p.epoch);
+                              p.flags, p.epoch, mode);
 }
 
 // Tile shapes compiled: CG=2 pairs with BN in steps of 32, CG=1 with 128 / 256.

@@ -25,6 +25,7 @@ struct GemmPlan {
     float* part = nullptr;
     uint32_t* flags = nullptr;
     uint32_t epoch = 0;
+    int sk_mode = -1;  // -1 auto, 0 whole tiles round-robin, 1 stream-K
 } __attribute__((aligned(64)));
 // Workspace sizes for gemm_launch (max over tile shapes) for num_sms SMs.
 inline size_t gemm_part_floats(int num_sms) { return size_t(num_sms) * 128 * 256; }
