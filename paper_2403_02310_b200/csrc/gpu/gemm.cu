@@ -465,7 +465,6 @@ cudaError_t launch_t(const GemmPlan& p, cudaStream_t st) {
     const int tiles = num_mt * num_n;
     const long iters = long(tiles) * ((p.K + BK - 1) / BK);
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = Cfg::SMEM;
     cfg.stream = st;
