@@ -474,9 +474,10 @@ ss_status gemm(ss_ctx* ctx, int cls, const CUtensorMap& ta, WMaps& tb, int M, in
     p.ldo = ldo;
     p.epi = epi;
     p.num_sms = ctx->num_sms;
-    const GemmShape s = gemm_pick(M, N, epi, ctx->num_sms);
+    const GemmShape s = gemm_pick(M, N, K, epi, ctx->num_sms);
     p.cg = s.cg;
     p.bn = s.bn;
+    p.splits = s.splits;
     p.tmA = ta;
     const CUtensorMap* mb = tb.get(p.bn / p.cg);
     if (!mb) return fail(ctx, SS_CUDA_ERROR, "cuTensorMapEncodeTiled failed (weight tile map)");

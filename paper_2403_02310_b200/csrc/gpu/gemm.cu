@@ -156,16 +156,27 @@ __device__ __forceinline__ long sk_start(int g, int G, long total) { return long
 struct Seg {
     int t, kb0, kb1;
 };
+// mode 2: split-K in lockstep — S aligned K slices per tile, one (tile, slice)
+// unit per group (units <= groups): group g runs slice g % S of tile g / S, so
+// every group walks the same K offsets at the same time (A k-blocks shared in
+// L2) and a tile's pieces sit on consecutive groups.
 struct SegIter {
-    int mode, G, num_kb, num_tiles, t_rr;
+    int mode, G, num_kb, num_tiles, t_rr, S;
     long i, i1;
-    __device__ SegIter(int m, int gid, int G_, int nkb, int nt, SkRange r)
-        : mode(m), G(G_), num_kb(nkb), num_tiles(nt), t_rr(gid), i(r.i0), i1(r.i1) {}
+    __device__ SegIter(int m, int gid, int G_, int nkb, int nt, SkRange r, int S_)
+        : mode(m), G(G_), num_kb(nkb), num_tiles(nt), t_rr(gid), S(S_), i(r.i0), i1(r.i1) {}
     __device__ __forceinline__ bool next(Seg& s) {
         if (mode == 0) {
             if (t_rr >= num_tiles) return false;
             s = Seg{t_rr, 0, num_kb};
             t_rr += G;
+            return true;
+        }
+        if (mode == 2) {
+            if (t_rr >= num_tiles * S) return false;
+            const int sl = t_rr % S;
+            s = Seg{t_rr / S, sl * num_kb / S, (sl + 1) * num_kb / S};
+            t_rr += 1 << 30;  // one unit per group
             return true;
         }
         if (i >= i1) return false;
@@ -224,7 +235,8 @@ template <int CG, int BN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
                         int N, int K, void* __restrict__ out, int ldo, int num_mt, int num_tiles,
-                        float* __restrict__ part, uint32_t* __restrict__ flags, uint32_t epoch, int sk_mode) {
+                        float* __restrict__ part, uint32_t* __restrict__ flags, uint32_t epoch, int sk_mode,
+                        int sk_slices) {
     using Cfg = GemmCfg<CG, BN>;
     constexpr int STAGES = Cfg::STAGES;
     extern __shared__ uint8_t smem_raw[];
@@ -272,7 +284,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t full_leader = CG == 2 ? peer_addr(full, 0) : 0;
             int s = 0;
             uint32_t ph = 0;
-            SegIter sit(sk_mode, gid, G, num_kb, num_tiles, rg);
+            SegIter sit(sk_mode, gid, G, num_kb, num_tiles, rg, sk_slices);
             for (Seg sg; sit.next(sg);) {
                 const int t = sg.t, kb0 = sg.kb0, kb1 = sg.kb1;
                 const int m0 = (t % num_mt) * Cfg::TILE_M + 128 * int(rank);
@@ -303,7 +315,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t ph = 0;
             int acc = 0;
             uint32_t acc_ph = 0;
-            SegIter sit(sk_mode, gid, G, num_kb, num_tiles, rg);
+            SegIter sit(sk_mode, gid, G, num_kb, num_tiles, rg, sk_slices);
             for (Seg sg; sit.next(sg);) {
                 const int kb0 = sg.kb0, kb1 = sg.kb1;
                 mbar_wait(&tempty[acc], acc_ph ^ 1);
@@ -337,7 +349,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int rloc = 128 * int(rank) + q * 32 + lane;  // row within the group's tile
         int acc = 0;
         uint32_t acc_ph = 0;
-        SegIter sit(sk_mode, gid, G, num_kb, num_tiles, rg);
+        SegIter sit(sk_mode, gid, G, num_kb, num_tiles, rg, sk_slices);
         for (Seg sg; sit.next(sg);) {
             const int t = sg.t, kb0 = sg.kb0, kb1 = sg.kb1;
             const int m0 = (t % num_mt) * Cfg::TILE_M, n0 = (t / num_mt) * BN;
@@ -365,9 +377,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             } else {
                 // head or whole tile: add the other groups' pieces in group order
                 const long tile_end = long(t + 1) * num_kb;
-                int g_last = gid;  // last group whose range starts inside this tile
-                if (kb1 < num_kb)
-                    while (g_last + 1 < G && sk_start(g_last + 1, G, total) < tile_end) ++g_last;
+                int g_last = gid;  // last group holding a piece of this tile
+                if (kb1 < num_kb) {
+                    if (sk_mode == 2) g_last = gid + sk_slices - 1;
+                    else
+                        while (g_last + 1 < G && sk_start(g_last + 1, G, total) < tile_end) ++g_last;
+                }
                 for (int g = gid + 1; g <= g_last; ++g) {
                     const uint32_t* f = &flags[(size_t(g) * 2 + rank) * 4 + q];
                     uint32_t spins = 0;
@@ -485,18 +500,21 @@ cudaError_t launch_t(const GemmPlan& p, cudaStream_t st) {
         else resident = p.num_sms / CG;
         if (resident > p.num_sms / CG) resident = p.num_sms / CG;
     }
-    int mode = p.sk_mode;
-    if (mode < 0) mode = tiles % resident == 0 || tiles > 6 * resident ? 0 : 1;  // stream-K only for ragged waves
-    if (const char* f = getenv("SS_GEMM_SK")) mode = atoi(f) ? 1 : 0;
+    int mode = p.sk_mode, S = p.splits < 1 ? 1 : p.splits;
+    if (mode < 0) mode = S > 1 ? 2 : 0;
+    if (const char* f = getenv("SS_GEMM_SK")) mode = atoi(f);
+    if (const char* f = getenv("SS_GEMM_SPLITS")) S = atoi(f);
+    if (mode == 2 && (S < 2 || long(tiles) * S > resident)) mode = 0;  // lockstep split needs one wave
     int groups = resident;
     if (mode == 0 && tiles < groups) groups = tiles;
     if (mode == 1 && iters < groups) groups = int(iters);
+    if (mode == 2) groups = tiles * S;
     cfg.gridDim = dim3(CG * groups);
     if (getenv("SS_GEMM_DEBUG"))
         fprintf(stderr, "gemm cg=%d bn=%d epi=%d M=%d N=%d K=%d tiles=%d resident=%d mode=%d groups=%d\n", CG, BN,
                 EPI, p.M, p.N, p.K, tiles, resident, mode, groups);
     return cudaLaunchKernelEx(&cfg, kern, p.tmA, p.tmB, p.M, p.N, p.K, p.out, p.ldo, num_mt, tiles, p.part,
-                              p.flags, p.epoch, mode);
+                              p.flags, p.epoch, mode, S);
 }
 
 // Tile shapes compiled: CG=2 pairs with BN in steps of 32, CG=1 with 128 / 256.
@@ -517,31 +535,40 @@ bool make_tmap_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-GemmShape gemm_pick(int M, int N, int epi, int num_sms) {
-    int force_bn = 0, force_cg = 0;
+GemmShape gemm_pick(int M, int N, int K, int epi, int num_sms) {
+    int force_bn = 0, force_cg = 0, force_s = 0;
     if (const char* f = getenv("SS_GEMM_BN")) force_bn = atoi(f);  // tuning overrides (dev only)
     if (const char* f = getenv("SS_GEMM_CG")) force_cg = atoi(f);
+    if (const char* f = getenv("SS_GEMM_SPLITS")) force_s = atoi(f);
     const bool swiglu = epi == EPI_SWIGLU;
-    GemmShape best{M > 128 ? 2 : 1, swiglu ? 256 : 128};
+    GemmShape best{M > 128 ? 2 : 1, swiglu ? 256 : 128, 1};
     double best_cost = 1e30;
-    // Stream-K spreads all (tile, k-block) iterations evenly over the SMs, so the
-    // cost is the total tile work / groups. Measured per-tile main-loop time (us
-    // at K = 4096, B200, profiles/r01/gemm_tiles.txt): at these M the loop is
-    // bound by the L2 -> SM fill rate rather than the MMA pipe, so wide tiles
-    // (fewer bytes staged per flop) win unless N is small.
+    // Measured per-tile main-loop time (us per 64 k-blocks, B200,
+    // profiles/r01/gemm_tiles.txt): at these M the loop is bound by the L2 -> SM
+    // fill rate rather than the MMA pipe, so narrow tiles save less than their
+    // MMA share. Whole tiles go round-robin (groups stay in K-lockstep, sharing
+    // A k-blocks in L2); when one wave leaves groups idle, K is split into S
+    // aligned slices that still run in lockstep (mode 2), at a fixup cost.
     auto tile_us = [](int c, int b) {
         if (c == 1) return b == 256 ? 28.6 : 20.4;
         return b >= 224 ? 25.3 : (b >= 192 ? 23.2 : (b >= 160 ? 22.1 : (b >= 128 ? 21.1 : 20.0)));
     };
+    const double kscale = double((K + BK - 1) / BK) / 64.0;
     auto consider = [&](int cg, int bn) {
         if (swiglu && bn % 64) return;
         if (force_bn && bn != force_bn) return;
         if (force_cg && cg != force_cg) return;
         const long tiles = long((M + 128 * cg - 1) / (128 * cg)) * ((N + bn - 1) / bn);
-        const double cost = double(tiles) * tile_us(cg, bn) / double(num_sms / cg);
-        if (cost < best_cost - 1e-9) {
-            best_cost = cost;
-            best = GemmShape{cg, bn};
+        const long slots = num_sms / cg;
+        for (int S = 1; S <= 4; ++S) {
+            if (force_s && S != force_s) continue;
+            if (S > 1 && tiles * S > slots) break;
+            const long waves = S == 1 ? (tiles + slots - 1) / slots : 1;
+            const double cost = double(waves) * tile_us(cg, bn) * kscale / S + (S > 1 ? 2.0 + 1.5 * (S - 1) : 0.0);
+            if (cost < best_cost - 1e-9) {
+                best_cost = cost;
+                best = GemmShape{cg, bn, S};
+            }
         }
     };
     if (M <= 128 || force_cg == 1) {
@@ -563,9 +590,10 @@ bool gemm_prepare(GemmPlan& p, const void* A, uint64_t a_rows, const void* B, in
     p.ldo = ldo;
     p.epi = epi;
     p.num_sms = num_sms;
-    const GemmShape s = gemm_pick(M, N, epi, num_sms);
+    const GemmShape s = gemm_pick(M, N, K, epi, num_sms);
     p.cg = s.cg;
     p.bn = bn ? bn : s.bn;
+    p.splits = s.splits;
     if (!make_tmap_2d(&p.tmA, A, a_rows, uint64_t(K), 128, BK)) return false;
     if (!make_tmap_2d(&p.tmB, B, uint64_t(N), uint64_t(K), uint32_t(p.bn / p.cg), BK)) return false;
     return true;

@@ -25,20 +25,22 @@ struct GemmPlan {
     float* part = nullptr;
     uint32_t* flags = nullptr;
     uint32_t epoch = 0;
-    int sk_mode = -1;  // -1 auto, 0 whole tiles round-robin, 1 stream-K
+    int sk_mode = -1;  // -1 auto, 0 whole tiles round-robin, 1 stream-K, 2 lockstep split-K
+    int splits = 1;    // K slices per tile for mode 2 (tiles * splits must fit one resident wave)
 } __attribute__((aligned(64)));
+
 // Workspace sizes for gemm_launch (max over tile shapes) for num_sms SMs.
 inline size_t gemm_part_floats(int num_sms) { return size_t(num_sms) * 128 * 256; }
 inline size_t gemm_flag_words(int num_sms) { return size_t(num_sms) * 8; }
 
 struct GemmShape {
-    int cg, bn;
+    int cg, bn, splits;
 };
 
 bool make_tmap_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
                   uint32_t box_cols);
 // Tile shape for an M x N GEMM: minimises wave-quantised time over the compiled shapes.
-GemmShape gemm_pick(int M, int N, int epi, int num_sms);
+GemmShape gemm_pick(int M, int N, int K, int epi, int num_sms);
 // A is [a_rows >= M][K] bf16; B is [N][K] bf16; out row stride ldo elements.
 bool gemm_prepare(GemmPlan& p, const void* A, uint64_t a_rows, const void* B, int M, int N, int K, void* out,
                   int ldo, int epi, int num_sms, int bn = 0);
