@@ -7,7 +7,8 @@
 //   warp 0       TMA producer: A/B tiles (SWIZZLE_128B) into a STAGES-deep ring
 //   warp 1       TMEM allocator + single-thread tcgen05.mma issuer (fp32
 //                accumulators in TMEM, K = 16 per instruction)
-//   warps 2..5   epilogue: tcgen05.ld -> registers -> fused epilogue -> HBM
+//   warps 2..9   epilogue: tcgen05.ld -> registers -> fused epilogue -> HBM
+//                (two warps per TMEM lane quarter, alternating 32-column chunks)
 // CG = 2 runs CTA pairs (cluster of 2, tcgen05 cta_group::2): a 256 x BN tile
 // per pair, each CTA staging its own 128 rows of A and BN/2 rows of B, so the
 // per-SM shared-memory traffic per MMA is half that of a 1-CTA 128 x BN tile.
@@ -33,7 +34,7 @@ namespace ssk {
 namespace {
 
 constexpr int BK = 64;  // 128 B of bf16: one SWIZZLE_128B row
-constexpr int kThreads = 192;
+constexpr int kThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue
 constexpr int kSmemBudget = 200 * 1024;
 
 template <int CG, int BN>
@@ -268,7 +269,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 4 * CG);  // every epilogue warp of the group
+            mbar_init(&tempty[a], 8 * CG);  // every epilogue warp of the group
         }
         mbar_fence_init();
     }
@@ -343,8 +344,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
         }
-    } else {  // ---------------------------- epilogue warps 2..5
-        const int q = warp & 3;  // TMEM lane quarter this warp may access
+    } else {  // ---------------------------- epilogue warps 2..9
+        // two warps per TMEM lane quarter (warp % 4 selects the quarter), splitting
+        // the tile's 32-column chunks (pairs for SwiGLU) between them
+        const int q = warp & 3;
+        const int ew = warp - 2, half = ew >> 2;
         const uint32_t tempty_leader = CG == 2 ? peer_addr(tempty, 0) : 0;
         const int rloc = 128 * int(rank) + q * 32 + lane;  // row within the group's tile
         int acc = 0;
@@ -361,7 +365,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // non-head piece of a split tile: publish the partial accumulator
                 float* dst = part + (size_t(gid) * Cfg::TILE_M + rloc) * BN;
 #pragma unroll 1
-                for (int c = 0; c < BN / 32; ++c) {
+                for (int c = half; c < BN / 32; c += 2) {
                     uint32_t v[32];
                     tmem_ld32(t_row + uint32_t(c * 32), v);
                     tmem_wait_ld();
@@ -373,7 +377,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 __threadfence();
                 __syncwarp();
-                if (lane == 0) st_release_gpu(&flags[(size_t(gid) * 2 + rank) * 4 + q], epoch);
+                if (lane == 0) st_release_gpu(&flags[(size_t(gid) * 2 + rank) * 8 + ew], epoch);
             } else {
                 // head or whole tile: add the other groups' pieces in group order
                 const long tile_end = long(t + 1) * num_kb;
@@ -384,14 +388,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                         while (g_last + 1 < G && sk_start(g_last + 1, G, total) < tile_end) ++g_last;
                 }
                 for (int g = gid + 1; g <= g_last; ++g) {
-                    const uint32_t* f = &flags[(size_t(g) * 2 + rank) * 4 + q];
+                    const uint32_t* f = &flags[(size_t(g) * 2 + rank) * 8 + ew];
                     uint32_t spins = 0;
                     while (ld_acquire_gpu(f) != epoch)
                         if (++spins == (1u << 28)) __trap();
                 }
                 if constexpr (EPI == EPI_SWIGLU) {
 #pragma unroll 1
-                    for (int c = 0; c < BN / 32; c += 2) {
+                    for (int c = 2 * half; c < BN / 32; c += 4) {
                         uint32_t gt[32], ut[32];
                         tmem_ld32(t_row + uint32_t(c * 32), gt);
                         tmem_ld32(t_row + uint32_t((c + 1) * 32), ut);
@@ -417,7 +421,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 } else {
 #pragma unroll 1
-                    for (int c = 0; c < BN / 32; ++c) {
+                    for (int c = half; c < BN / 32; c += 2) {
                         uint32_t v[32];
                         tmem_ld32(t_row + uint32_t(c * 32), v);
                         tmem_wait_ld();
@@ -564,7 +568,10 @@ GemmShape gemm_pick(int M, int N, int K, int epi, int num_sms) {
             if (force_s && S != force_s) continue;
             if (S > 1 && tiles * S > slots) break;
             const long waves = S == 1 ? (tiles + slots - 1) / slots : 1;
-            const double cost = double(waves) * tile_us(cg, bn) * kscale / S + (S > 1 ? 2.0 + 1.5 * (S - 1) : 0.0);
+            // + exposed epilogue (~6 us when a group owns one tile); split-K adds the
+            // partial write / fixup read of a 256-wide fp32 tile (measured ~2.5x that)
+            const double epi = waves == 1 ? 6.0 : 0.0;
+            const double cost = double(waves) * tile_us(cg, bn) * kscale / S + (S > 1 ? 3.5 * 6.0 : epi);
             if (cost < best_cost - 1e-9) {
                 best_cost = cost;
                 best = GemmShape{cg, bn, S};

@@ -31,7 +31,7 @@ struct GemmPlan {
 
 // Workspace sizes for gemm_launch (max over tile shapes) for num_sms SMs.
 inline size_t gemm_part_floats(int num_sms) { return size_t(num_sms) * 128 * 256; }
-inline size_t gemm_flag_words(int num_sms) { return size_t(num_sms) * 8; }
+inline size_t gemm_flag_words(int num_sms) { return size_t(num_sms) * 16; }
 
 struct GemmShape {
     int cg, bn, splits;
