@@ -22,8 +22,9 @@
 // workspace and attention_combine merges them in a fixed order (deterministic).
 //
 // K/V pages ([block][kv_head][16][hd], 4 KB contiguous at hd=128) are moved by
-// TMA (cp.async.bulk.tensor, SWIZZLE_128B) into a kStages-deep ring, issued by
-// one thread: no per-thread address math or block-table loads in the stream.
+// TMA (cp.async.bulk.tensor, SWIZZLE_128B) into a kStages-deep full/empty
+// mbarrier ring by a dedicated producer warp: no per-thread address math or
+// block-table loads in the compute warps, and no CTA-wide barrier per tile.
 // S = QK^T and O += PV use mma.sync m16n8k16 (bf16 in, fp32 accumulate); the
 // decode path is HBM-bound, so the MMA flavour does not limit it.
 #include <cfloat>
@@ -119,27 +120,13 @@ __device__ __forceinline__ void attend(const AttnParams& p, const CUtensorMap* t
 #pragma unroll
     for (int dt = 0; dt < HD / 8; ++dt) O[dt][0] = O[dt][1] = O[dt][2] = O[dt][3] = 0.f;
 
+    uint64_t* empty = full + kStages;
     const int ntiles = (it.key1 - it.key0 + kKeysPerTile - 1) / kKeysPerTile;
-    if (threadIdx.x == 0) {
-#pragma unroll
-        for (int s = 0; s < kStages - 1; ++s)
-            if (s < ntiles) {
-                uint8_t* sk = smem + S::Q_BYTES + s * S::STAGE;
-                issue_kv_tile<HD>(p, tmK, tmV, sk, sk + S::KV_TILE, &full[s], e, it.kv_head,
-                                  it.key0 + s * kKeysPerTile);
-            }
-    }
     for (int t = 0; t < ntiles; ++t) {
         const int kbase = it.key0 + t * kKeysPerTile;
         const int st = t % kStages;
         uint8_t* sK = smem + S::Q_BYTES + st * S::STAGE;
         uint8_t* sV = sK + S::KV_TILE;
-        if (threadIdx.x == 0 && t + kStages - 1 < ntiles) {
-            const int ns = (t + kStages - 1) % kStages;
-            uint8_t* nk = smem + S::Q_BYTES + ns * S::STAGE;
-            issue_kv_tile<HD>(p, tmK, tmV, nk, nk + S::KV_TILE, &full[ns], e, it.kv_head,
-                              kbase + (kStages - 1) * kKeysPerTile);
-        }
         mbar_wait(&full[st], uint32_t((t / kStages) & 1));
 
         // S = Q K^T for this warp's key slice
@@ -219,7 +206,8 @@ __device__ __forceinline__ void attend(const AttnParams& p, const CUtensorMap* t
                 mma_bf16_16816(O[dt + 1], a, b2, b3);
             }
         }
-        __syncthreads();  // stage st is refilled by a later iteration's TMA
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);  // this warp is done with stage st
     }
 #pragma unroll
     for (int hr = 0; hr < 2; ++hr) {
@@ -246,8 +234,9 @@ __device__ __forceinline__ void emit_pair(const AttnParams& p, const AttnItem& i
 }
 
 template <int HD>
-__global__ void __launch_bounds__(kWarps * 32) attention_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmK,
-                                                                const __grid_constant__ CUtensorMap tmV) {
+__global__ void __launch_bounds__((kWarps + 1) * 32) attention_kernel(const AttnParams p,
+                                                                      const __grid_constant__ CUtensorMap tmK,
+                                                                      const __grid_constant__ CUtensorMap tmV) {
     using S = AttnSmem<HD>;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
@@ -257,12 +246,16 @@ __global__ void __launch_bounds__(kWarps * 32) attention_kernel(const AttnParams
     const AttnItem it = p.items[blockIdx.x];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool key_mode = it.nrows <= 16;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
+    uint64_t* empty = full + kStages;
 
     if (threadIdx.x == 0) {
         tma_prefetch(&tmK);
         tma_prefetch(&tmV);
-        uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
-        for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kWarps);
+        }
         mbar_fence_init();
     }
     // stage the Q tile (rows beyond nrows are zero)
@@ -270,7 +263,7 @@ __global__ void __launch_bounds__(kWarps * 32) attention_kernel(const AttnParams
         constexpr int CH = HD / 8;
         const int e = it.entry, tok0 = p.cu_q[e];
         const int nr = key_mode ? 16 : kRowsPerTile;
-        for (int idx = threadIdx.x; idx < nr * CH; idx += kWarps * 32) {
+        for (int idx = threadIdx.x; idx < nr * CH; idx += (kWarps + 1) * 32) {
             const int r = idx / CH, c = idx % CH;
             const uint32_t so = smem_u32(smem) + swz_q<HD>(r, c);
             if (r < it.nrows) {
@@ -287,6 +280,20 @@ __global__ void __launch_bounds__(kWarps * 32) attention_kernel(const AttnParams
         __syncthreads();
     }
 
+    if (warp == kWarps) {  // ---- producer warp: K/V pages by TMA into the ring
+        if (lane == 0) {
+            const int ntiles = (it.key1 - it.key0 + kKeysPerTile - 1) / kKeysPerTile;
+            for (int t = 0; t < ntiles; ++t) {
+                const int st = t % kStages;
+                if (t >= kStages) mbar_wait(&empty[st], uint32_t(((t / kStages) - 1) & 1));
+                uint8_t* sk = smem + S::Q_BYTES + st * S::STAGE;
+                issue_kv_tile<HD>(p, &tmK, &tmV, sk, sk + S::KV_TILE, &full[st], it.entry, it.kv_head,
+                                  it.key0 + t * kKeysPerTile);
+            }
+        }
+        return;
+    }
+
     float O[HD / 8][4], m[2], l[2];
     if (!key_mode) {
         attend<HD, 64>(p, &tmK, &tmV, it, smem, warp * 16, 0, O, m, l);
@@ -301,7 +308,9 @@ __global__ void __launch_bounds__(kWarps * 32) attention_kernel(const AttnParams
     }
 
     attend<HD, 16>(p, &tmK, &tmV, it, smem, 0, warp * 16, O, m, l);
-    // merge the four warps' partial softmax states (K/V stages reused as scratch)
+    // merge the four warps' partial softmax states (K/V stages reused as scratch,
+    // once every compute warp is past its last tile)
+    asm volatile("bar.sync 1, %0;" ::"n"(kWarps * 32) : "memory");
     float* sO = reinterpret_cast<float*>(smem + S::Q_BYTES);  // [4][16][HD]
     float* sML = sO + kWarps * 16 * HD;                        // [4][16][2]
     {
@@ -319,7 +328,7 @@ __global__ void __launch_bounds__(kWarps * 32) attention_kernel(const AttnParams
             sML[(warp * 16 + r0 + 8) * 2 + 1] = l[1];
         }
     }
-    __syncthreads();
+    asm volatile("bar.sync 1, %0;" ::"n"(kWarps * 32) : "memory");
     for (int idx = threadIdx.x; idx < it.nrows * (HD / 2); idx += kWarps * 32) {
         const int r = idx / (HD / 2), d = (idx % (HD / 2)) * 2;
         float M = -INFINITY;
@@ -370,7 +379,7 @@ cudaError_t launch_hd(const AttnParams& p, const CUtensorMap& tk, const CUtensor
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    if (p.n_items > 0) attention_kernel<HD><<<p.n_items, kWarps * 32, AttnSmem<HD>::TOTAL, st>>>(p, tk, tv);
+    if (p.n_items > 0) attention_kernel<HD><<<p.n_items, (kWarps + 1) * 32, AttnSmem<HD>::TOTAL, st>>>(p, tk, tv);
     return cudaGetLastError();
 }
 
