@@ -216,6 +216,48 @@ __device__ __forceinline__ void attend(const AttnParams& p, const CUtensorMap* t
     }
 }
 
+// Merges the partial (m, l, O) of every split of a group into the final bf16
+// output, in split order (deterministic). Run by the CTA that finishes a
+// group's last split; 128 compute threads.
+template <int HD>
+__device__ __forceinline__ void combine_group(const AttnParams& p, const AttnCombine& c, int tid) {
+    for (int idx = tid; idx < c.nrows * HD; idx += kWarps * 32) {
+        const int r = idx / HD, d = idx % HD;
+        float M = -INFINITY;
+        for (int s = 0; s < c.nsplit; ++s) M = fmaxf(M, __ldcg(p.part_ml + size_t(c.part + s * c.stride + r) * 2));
+        const float Ms = M == -INFINITY ? 0.f : M;
+        float L = 0.f, o = 0.f;
+        for (int s = 0; s < c.nsplit; ++s) {
+            const size_t slot = size_t(c.part + s * c.stride + r);
+            const float f = exp2f(__ldcg(p.part_ml + slot * 2) - Ms);
+            L += __ldcg(p.part_ml + slot * 2 + 1) * f;
+            o += __ldcg(p.part_o + slot * HD + d) * f;
+        }
+        const int gr = c.row0 + r;
+        const int tok = p.cu_q[c.entry] + gr / p.group;
+        const int hq = c.kv_head * p.group + gr % p.group;
+        p.o[(size_t(tok) * p.nq_l + hq) * HD + d] = __float2bfloat16(L > 0.f ? o / L : 0.f);
+    }
+}
+
+// After a split's partials are written: the last split of the group to finish
+// (threadFenceReduction pattern) merges all splits and resets the counter.
+template <int HD>
+__device__ __forceinline__ void finish_split(const AttnParams& p, const AttnItem& it, int* s_flag) {
+    if (it.comb < 0) return;
+    __threadfence();
+    asm volatile("bar.sync 1, %0;" ::"n"(kWarps * 32) : "memory");
+    if (threadIdx.x == 0) {
+        const AttnCombine c = p.combines[it.comb];
+        *s_flag = atomicAdd(&p.comb_count[it.comb], 1) == c.nsplit - 1;
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(kWarps * 32) : "memory");
+    if (!*s_flag) return;
+    __threadfence();
+    combine_group<HD>(p, p.combines[it.comb], threadIdx.x);
+    if (threadIdx.x == 0) p.comb_count[it.comb] = 0;
+}
+
 // Writes one row's final (normalised bf16) or partial (fp32 O, m, l) result.
 template <int HD>
 __device__ __forceinline__ void emit_pair(const AttnParams& p, const AttnItem& it, int r, int d, float o0, float o1,
@@ -304,6 +346,7 @@ __global__ void __launch_bounds__((kWarps + 1) * 32) attention_kernel(const Attn
             emit_pair<HD>(p, it, r0, d, O[dt][0], O[dt][1], m[0], l[0]);
             emit_pair<HD>(p, it, r0 + 8, d, O[dt][2], O[dt][3], m[1], l[1]);
         }
+        finish_split<HD>(p, it, reinterpret_cast<int*>(smem + S::BAR_OFF + 2 * kStages * 8));
         return;
     }
 
@@ -346,6 +389,7 @@ __global__ void __launch_bounds__((kWarps + 1) * 32) attention_kernel(const Attn
         }
         emit_pair<HD>(p, it, r, d, o0, o1, M, L);
     }
+    finish_split<HD>(p, it, reinterpret_cast<int*>(smem + S::BAR_OFF + 2 * kStages * 8));
 }
 
 template <int HD>

@@ -134,6 +134,7 @@ struct ss_ctx {
     float *logits_l = nullptr, *logits_g = nullptr, *logits = nullptr;
     int32_t* next_tok = nullptr;
     float *part_o = nullptr, *part_ml = nullptr;
+    int32_t* comb_count = nullptr;  // split-KV group counters (self-resetting)
     float* sk_part = nullptr;       // stream-K GEMM partial accumulators
     uint32_t* sk_flags = nullptr;   // stream-K ready flags
     uint32_t sk_epoch = 0;
@@ -292,8 +293,11 @@ ss_status ensure_workspace(ss_ctx* ctx, int T, int n_out, int part_rows) {
         const int cap = std::max(part_rows, 2 * ctx->P_cap);
         cudaFree(ctx->part_o);
         cudaFree(ctx->part_ml);
+        cudaFree(ctx->comb_count);
         CK(cudaMalloc(&ctx->part_o, size_t(cap) * ctx->hd * 4));
         CK(cudaMalloc(&ctx->part_ml, size_t(cap) * 2 * 4));
+        CK(cudaMalloc(&ctx->comb_count, size_t(cap) * 4));
+        CK(cudaMemsetAsync(ctx->comb_count, 0, size_t(cap) * 4, ctx->st));
         ctx->P_cap = cap;
     }
     return SS_OK;
@@ -322,16 +326,18 @@ void build_items(const ss_ctx* ctx, const ss_batch_desc* d, std::vector<AttnItem
     part_rows = 0;
     for (const Tile& t : tiles) {
         const int split = t.nr <= 16 ? 512 : long_split;
-        const int ns = (t.extent + split - 1) / split;
+        // floor: the last split absorbs the remainder (no 1-key tail splits)
+        const int ns = std::max(1, t.extent / split);
         for (int h = 0; h < ctx->nkv_l; ++h) {
             if (ns <= 1) {
-                items.push_back(AttnItem{t.e, h, t.row0, t.nr, 0, t.extent, -1, 0});
+                items.push_back(AttnItem{t.e, h, t.row0, t.nr, 0, t.extent, -1, -1});
                 continue;
             }
             const int base = part_rows;
+            const int ci = int(combs.size());
             for (int s = 0; s < ns; ++s)
-                items.push_back(AttnItem{t.e, h, t.row0, t.nr, s * split, std::min(t.extent, (s + 1) * split),
-                                         base + s * t.nr, 0});
+                items.push_back(AttnItem{t.e, h, t.row0, t.nr, s * split, s + 1 == ns ? t.extent : (s + 1) * split,
+                                         base + s * t.nr, ci});
             combs.push_back(AttnCombine{t.e, h, t.row0, t.nr, ns, base, t.nr, 0});
             part_rows += ns * t.nr;
         }
@@ -452,6 +458,7 @@ AttnParams attn_params(const ss_ctx* ctx, const ss_batch* b, const bf16* q, bf16
     p.n_items = b->n_items;
     p.part_o = ctx->part_o;
     p.part_ml = ctx->part_ml;
+    p.comb_count = ctx->comb_count;
     p.combines = b->combs;
     p.n_combines = b->n_combs;
     p.nq_l = ctx->nq_l;
@@ -517,7 +524,6 @@ ss_status enqueue_forward(ss_ctx* ctx, const ss_batch* b) {
         }));
         const AttnParams ap = attn_params(ctx, b, ctx->q, ctx->o, l);
         RUN(launch(ctx, SS_K_ATTN, 1, [&] { return attention_launch(ap, ctx->tm_k, ctx->tm_v, ctx->st); }));
-        if (b->n_combs) RUN(launch(ctx, SS_K_ATTN_COMBINE, 1, [&] { return attention_combine_launch(ap, ctx->st); }));
         if (ctx->tp == 1) {
             RUN(gemm(ctx, SS_K_GEMM_O, ctx->ta_o, W.tb_o, T, h, qd, ctx->x, h, EPI_RESADD));
         } else {
@@ -750,7 +756,7 @@ SS_API void ss_destroy(ss_ctx* ctx) {
     cudaFree(ctx->vc);
     for (void* q : {(void*)ctx->x, (void*)ctx->xn, (void*)ctx->qkv, (void*)ctx->q, (void*)ctx->o, (void*)ctx->act,
                     (void*)ctx->part, (void*)ctx->xo, (void*)ctx->logits_l, (void*)ctx->logits_g, (void*)ctx->logits,
-                    (void*)ctx->next_tok, (void*)ctx->part_o, (void*)ctx->part_ml, (void*)ctx->scratch.dev})
+                    (void*)ctx->next_tok, (void*)ctx->part_o, (void*)ctx->part_ml, (void*)ctx->comb_count, (void*)ctx->scratch.dev})
         cudaFree(q);
     cudaFreeHost(ctx->pinned);
     for (const Prof& p : ctx->pend) {
@@ -926,7 +932,6 @@ SS_API ss_status ss_k_attention(ss_ctx* ctx, const ss_batch* b, const void* q, v
     if (ss_status s = ensure_workspace(ctx, b->T, std::max(b->n_out, 1), b->part_rows)) return s;
     const AttnParams ap = attn_params(ctx, b, static_cast<const bf16*>(q), static_cast<bf16*>(o), layer);
     if (ss_status s = launch(ctx, SS_K_ATTN, 1, [&] { return attention_launch(ap, ctx->tm_k, ctx->tm_v, ctx->st); })) return s;
-    if (b->n_combs) return launch(ctx, SS_K_ATTN_COMBINE, 1, [&] { return attention_combine_launch(ap, ctx->st); });
     return SS_OK;
 }
 

@@ -57,7 +57,7 @@ struct AttnItem {
     int32_t key0;      // key range [key0, key1)
     int32_t key1;
     int32_t part;      // -1: final output; else partial slot base (rows)
-    int32_t pad;
+    int32_t comb;      // split group (index into combines) or -1
 };
 struct AttnCombine {  // one split group: partial slots base + s * nrows_pad
     int32_t entry;
@@ -87,6 +87,7 @@ struct AttnParams {
     int32_t nq_l, nkv_l, group, head_dim, block_size;
     float scale_log2;            // softmax scale * log2(e)
     int64_t layer_row0;          // first row of this layer in the 2D [rows][hd] TMA view of the cache
+    int32_t* comb_count;         // per split group: finished splits (zeroed, self-resetting)
 };
 // 2D TMA views [L * nblocks * nkv * 16][hd] of the K and V pools (box 16 x 64, SWIZZLE_128B).
 bool attention_tmaps(CUtensorMap* tk, CUtensorMap* tv, const void* kc, const void* vc, int64_t total_rows, int hd);
