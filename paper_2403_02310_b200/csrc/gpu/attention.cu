@@ -346,7 +346,7 @@ __global__ void __launch_bounds__((kWarps + 1) * 32) attention_kernel(const Attn
             emit_pair<HD>(p, it, r0, d, O[dt][0], O[dt][1], m[0], l[0]);
             emit_pair<HD>(p, it, r0 + 8, d, O[dt][2], O[dt][3], m[1], l[1]);
         }
-        finish_split<HD>(p, it, reinterpret_cast<int*>(smem + S::BAR_OFF + 2 * kStages * 8));
+        if (p.fused_combine) finish_split<HD>(p, it, reinterpret_cast<int*>(smem + S::BAR_OFF + 2 * kStages * 8));
         return;
     }
 
@@ -389,7 +389,7 @@ __global__ void __launch_bounds__((kWarps + 1) * 32) attention_kernel(const Attn
         }
         emit_pair<HD>(p, it, r, d, o0, o1, M, L);
     }
-    finish_split<HD>(p, it, reinterpret_cast<int*>(smem + S::BAR_OFF + 2 * kStages * 8));
+    if (p.fused_combine) finish_split<HD>(p, it, reinterpret_cast<int*>(smem + S::BAR_OFF + 2 * kStages * 8));
 }
 
 template <int HD>

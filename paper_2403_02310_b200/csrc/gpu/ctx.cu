@@ -135,6 +135,8 @@ struct ss_ctx {
     int32_t* next_tok = nullptr;
     float *part_o = nullptr, *part_ml = nullptr;
     int32_t* comb_count = nullptr;  // split-KV group counters (self-resetting)
+    int fused_combine = 0;          // in-kernel split merge (measured slower at 8 splits; off)
+    int decode_split = 1024;        // keys per split-KV piece for decode-like items
     float* sk_part = nullptr;       // stream-K GEMM partial accumulators
     uint32_t* sk_flags = nullptr;   // stream-K ready flags
     uint32_t sk_epoch = 0;
@@ -325,7 +327,7 @@ void build_items(const ss_ctx* ctx, const ss_batch_desc* d, std::vector<AttnItem
     const int long_split = prefill_items < ctx->num_sms ? 2048 : (1 << 30);
     part_rows = 0;
     for (const Tile& t : tiles) {
-        const int split = t.nr <= 16 ? 512 : long_split;
+        const int split = t.nr <= 16 ? ctx->decode_split : long_split;
         // floor: the last split absorbs the remainder (no 1-key tail splits)
         const int ns = std::max(1, t.extent / split);
         for (int h = 0; h < ctx->nkv_l; ++h) {
@@ -459,6 +461,7 @@ AttnParams attn_params(const ss_ctx* ctx, const ss_batch* b, const bf16* q, bf16
     p.part_o = ctx->part_o;
     p.part_ml = ctx->part_ml;
     p.comb_count = ctx->comb_count;
+    p.fused_combine = ctx->fused_combine;
     p.combines = b->combs;
     p.n_combines = b->n_combs;
     p.nq_l = ctx->nq_l;
@@ -524,6 +527,8 @@ ss_status enqueue_forward(ss_ctx* ctx, const ss_batch* b) {
         }));
         const AttnParams ap = attn_params(ctx, b, ctx->q, ctx->o, l);
         RUN(launch(ctx, SS_K_ATTN, 1, [&] { return attention_launch(ap, ctx->tm_k, ctx->tm_v, ctx->st); }));
+        if (b->n_combs && !ctx->fused_combine)
+            RUN(launch(ctx, SS_K_ATTN_COMBINE, 1, [&] { return attention_combine_launch(ap, ctx->st); }));
         if (ctx->tp == 1) {
             RUN(gemm(ctx, SS_K_GEMM_O, ctx->ta_o, W.tb_o, T, h, qd, ctx->x, h, EPI_RESADD));
         } else {
@@ -650,6 +655,8 @@ SS_API ss_status ss_create(const ss_model_cfg* cfg, int32_t tp_rank, int32_t tp_
     ctx->ffn_l = c.ffn / tp_size;
     ctx->vocab_l = c.vocab / tp_size;
     ctx->seed = weight_seed;
+    if (const char* f = getenv("SS_ATTN_SPLIT")) ctx->decode_split = std::max(64, atoi(f) / 64 * 64);  // dev tuning
+    if (const char* f = getenv("SS_ATTN_FUSED_COMBINE")) ctx->fused_combine = atoi(f);
     if (cudaMalloc(&ctx->sk_part, gemm_part_floats(ctx->num_sms) * 4) != cudaSuccess ||
         cudaMalloc(&ctx->sk_flags, gemm_flag_words(ctx->num_sms) * 4) != cudaSuccess ||
         cudaMemset(ctx->sk_flags, 0, gemm_flag_words(ctx->num_sms) * 4) != cudaSuccess) {
@@ -932,6 +939,8 @@ SS_API ss_status ss_k_attention(ss_ctx* ctx, const ss_batch* b, const void* q, v
     if (ss_status s = ensure_workspace(ctx, b->T, std::max(b->n_out, 1), b->part_rows)) return s;
     const AttnParams ap = attn_params(ctx, b, static_cast<const bf16*>(q), static_cast<bf16*>(o), layer);
     if (ss_status s = launch(ctx, SS_K_ATTN, 1, [&] { return attention_launch(ap, ctx->tm_k, ctx->tm_v, ctx->st); })) return s;
+    if (b->n_combs && !ctx->fused_combine)
+        return launch(ctx, SS_K_ATTN_COMBINE, 1, [&] { return attention_combine_launch(ap, ctx->st); });
     return SS_OK;
 }
 

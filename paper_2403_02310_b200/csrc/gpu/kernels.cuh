@@ -88,6 +88,7 @@ struct AttnParams {
     float scale_log2;            // softmax scale * log2(e)
     int64_t layer_row0;          // first row of this layer in the 2D [rows][hd] TMA view of the cache
     int32_t* comb_count;         // per split group: finished splits (zeroed, self-resetting)
+    int32_t fused_combine;       // 1: last split merges in-kernel; 0: attention_combine launch
 };
 // 2D TMA views [L * nblocks * nkv * 16][hd] of the K and V pools (box 16 x 64, SWIZZLE_128B).
 bool attention_tmaps(CUtensorMap* tk, CUtensorMap* tv, const void* kc, const void* vc, int64_t total_rows, int hd);
