@@ -136,7 +136,7 @@ struct ss_ctx {
     float *part_o = nullptr, *part_ml = nullptr;
     int32_t* comb_count = nullptr;  // split-KV group counters (self-resetting)
     int fused_combine = 0;          // in-kernel split merge (measured slower at 8 splits; off)
-    int decode_split = 1024;        // keys per split-KV piece for decode-like items
+    int decode_split = 1536;        // target keys per split-KV piece for decode-like items (measured)
     float* sk_part = nullptr;       // stream-K GEMM partial accumulators
     uint32_t* sk_flags = nullptr;   // stream-K ready flags
     uint32_t sk_epoch = 0;
@@ -328,8 +328,9 @@ void build_items(const ss_ctx* ctx, const ss_batch_desc* d, std::vector<AttnItem
     part_rows = 0;
     for (const Tile& t : tiles) {
         const int split = t.nr <= 16 ? ctx->decode_split : long_split;
-        // floor: the last split absorbs the remainder (no 1-key tail splits)
-        const int ns = std::max(1, t.extent / split);
+        // balanced splits on 64-key boundaries (no 1-key tail splits)
+        const int ns = split >= (1 << 30) ? 1 : std::max(1, (t.extent + split / 2) / split);
+        auto bound = [&](int s) { return s >= ns ? t.extent : int((int64_t(s) * t.extent / ns) & ~int64_t(63)); };
         for (int h = 0; h < ctx->nkv_l; ++h) {
             if (ns <= 1) {
                 items.push_back(AttnItem{t.e, h, t.row0, t.nr, 0, t.extent, -1, -1});
@@ -338,8 +339,7 @@ void build_items(const ss_ctx* ctx, const ss_batch_desc* d, std::vector<AttnItem
             const int base = part_rows;
             const int ci = int(combs.size());
             for (int s = 0; s < ns; ++s)
-                items.push_back(AttnItem{t.e, h, t.row0, t.nr, s * split, s + 1 == ns ? t.extent : (s + 1) * split,
-                                         base + s * t.nr, ci});
+                items.push_back(AttnItem{t.e, h, t.row0, t.nr, bound(s), bound(s + 1), base + s * t.nr, ci});
             combs.push_back(AttnCombine{t.e, h, t.row0, t.nr, ns, base, t.nr, 0});
             part_rows += ns * t.nr;
         }
