@@ -300,6 +300,8 @@ __global__ void __launch_bounds__((kWarps + 1) * 32) attention_kernel(const Attn
         }
         mbar_fence_init();
     }
+    pdl_launch_dependents();
+    pdl_wait();  // q / KV of this layer come from the preceding kernels
     // stage the Q tile (rows beyond nrows are zero)
     {
         constexpr int CH = HD / 8;
@@ -394,6 +396,8 @@ __global__ void __launch_bounds__((kWarps + 1) * 32) attention_kernel(const Attn
 
 template <int HD>
 __global__ void attention_combine_kernel(const AttnParams p) {
+    pdl_launch_dependents();
+    pdl_wait();
     const AttnCombine c = p.combines[blockIdx.x];
     for (int idx = threadIdx.x; idx < c.nrows * HD; idx += blockDim.x) {
         const int r = idx / HD, d = idx % HD;
@@ -423,8 +427,9 @@ cudaError_t launch_hd(const AttnParams& p, const CUtensorMap& tk, const CUtensor
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    if (p.n_items > 0) attention_kernel<HD><<<p.n_items, (kWarps + 1) * 32, AttnSmem<HD>::TOTAL, st>>>(p, tk, tv);
-    return cudaGetLastError();
+    return p.n_items > 0 ? launch_pdl(attention_kernel<HD>, dim3(p.n_items), dim3((kWarps + 1) * 32), AttnSmem<HD>::TOTAL,
+                                      st, 1, p, tk, tv)
+                         : cudaSuccess;
 }
 
 }  // namespace
@@ -444,10 +449,9 @@ cudaError_t attention_launch(const AttnParams& p, const CUtensorMap& tk, const C
 
 cudaError_t attention_combine_launch(const AttnParams& p, cudaStream_t st) {
     if (p.n_combines == 0) return cudaSuccess;
-    if (p.head_dim == 128) attention_combine_kernel<128><<<p.n_combines, 256, 0, st>>>(p);
-    else if (p.head_dim == 64) attention_combine_kernel<64><<<p.n_combines, 256, 0, st>>>(p);
-    else return cudaErrorInvalidValue;
-    return cudaGetLastError();
+    if (p.head_dim == 128) return launch_pdl(attention_combine_kernel<128>, dim3(p.n_combines), dim3(256), 0, st, 1, p);
+    if (p.head_dim == 64) return launch_pdl(attention_combine_kernel<64>, dim3(p.n_combines), dim3(256), 0, st, 1, p);
+    return cudaErrorInvalidValue;
 }
 
 }  // namespace ssk

@@ -17,6 +17,8 @@ __device__ __forceinline__ float warp_sum(float v) {
 
 __global__ void embed_kernel(const int32_t* __restrict__ tokens, const __nv_bfloat16* __restrict__ table,
                              float* __restrict__ x, int h) {
+    pdl_launch_dependents();
+    pdl_wait();
     const int t = blockIdx.x;
     const uint4* src = reinterpret_cast<const uint4*>(table + size_t(tokens[t]) * h);
     float4* dst = reinterpret_cast<float4*>(x + size_t(t) * h);
@@ -30,6 +32,8 @@ __global__ void embed_kernel(const int32_t* __restrict__ tokens, const __nv_bflo
 // One CTA per row: out = bf16(x * rsqrt(mean(x^2) + eps) * w).
 __global__ void rmsnorm_kernel(const float* __restrict__ x, const __nv_bfloat16* __restrict__ w,
                                __nv_bfloat16* __restrict__ out, const int32_t* __restrict__ rows, int h, float eps) {
+    pdl_launch_dependents();
+    pdl_wait();
     __shared__ float red[32];
     const int r = blockIdx.x;
     const int src_row = rows ? rows[r] : r;
@@ -65,6 +69,8 @@ __global__ void rope_append_kernel(const __nv_bfloat16* __restrict__ qkv, __nv_b
                                    const int32_t* __restrict__ pos, const int64_t* __restrict__ slot,
                                    const float2* __restrict__ cs, int nq, int nkv, int hd, int bs,
                                    __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc) {
+    pdl_launch_dependents();
+    pdl_wait();
     const int t = blockIdx.x;
     const int half = hd / 2;
     const int p = pos[t];
@@ -104,6 +110,8 @@ __global__ void rope_append_kernel(const __nv_bfloat16* __restrict__ qkv, __nv_b
 }
 
 __global__ void residual_add_kernel(float* __restrict__ x, const __nv_bfloat16* __restrict__ part, int64_t n8) {
+    pdl_launch_dependents();
+    pdl_wait();
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n8; i += int64_t(gridDim.x) * blockDim.x) {
         const uint4 v = reinterpret_cast<const uint4*>(part)[i];
         float4* d = reinterpret_cast<float4*>(x) + 2 * i;
@@ -117,6 +125,8 @@ __global__ void residual_add_kernel(float* __restrict__ x, const __nv_bfloat16* 
 
 // Greedy argmax per row; ties resolve to the lowest index.
 __global__ void argmax_kernel(const float* __restrict__ logits, int V, int ld, int32_t* __restrict__ out) {
+    pdl_launch_dependents();
+    pdl_wait();
     __shared__ float sv[32];
     __shared__ int si[32];
     const float* r = logits + size_t(blockIdx.x) * ld;
@@ -154,6 +164,8 @@ __global__ void argmax_kernel(const float* __restrict__ logits, int V, int ld, i
 }
 
 __global__ void gather_vocab_kernel(const float* __restrict__ in, float* __restrict__ out, int tp, int rows, int vl) {
+    pdl_launch_dependents();
+    pdl_wait();
     const int64_t n = int64_t(tp) * rows * vl;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
         const int64_t r = (i / vl) % rows, k = i / (int64_t(vl) * rows), c = i % vl;
@@ -250,37 +262,36 @@ int grid_for(int64_t n, int threads) {
 }  // namespace
 
 cudaError_t embed_launch(const int32_t* tokens, const __nv_bfloat16* table, float* x, int T, int h, cudaStream_t st) {
-    if (T > 0) embed_kernel<<<T, 256, 0, st>>>(tokens, table, x, h);
-    return cudaGetLastError();
+    return T > 0 ? launch_pdl(embed_kernel, dim3(T), dim3(256), 0, st, 1, tokens, table, x, h) : cudaSuccess;
 }
 
 cudaError_t rmsnorm_launch(const float* x, const __nv_bfloat16* w, __nv_bfloat16* out, const int32_t* rows, int M,
                            int h, float eps, cudaStream_t st) {
-    if (M > 0) rmsnorm_kernel<<<M, h >= 4096 ? 512 : 256, 0, st>>>(x, w, out, rows, h, eps);
-    return cudaGetLastError();
+    return M > 0 ? launch_pdl(rmsnorm_kernel, dim3(M), dim3(h >= 4096 ? 512 : 256), 0, st, 1, x, w, out, rows, h, eps)
+                 : cudaSuccess;
 }
 
 cudaError_t rope_append_launch(const __nv_bfloat16* qkv, __nv_bfloat16* q_out, const int32_t* pos, const int64_t* slot,
                                const float2* cs, int T, int nq, int nkv, int hd, int bs, __nv_bfloat16* kc,
                                __nv_bfloat16* vc, cudaStream_t st) {
-    if (T > 0) rope_append_kernel<<<T, 256, 0, st>>>(qkv, q_out, pos, slot, cs, nq, nkv, hd, bs, kc, vc);
-    return cudaGetLastError();
+    return T > 0 ? launch_pdl(rope_append_kernel, dim3(T), dim3(256), 0, st, 1, qkv, q_out, pos, slot, cs, nq, nkv, hd,
+                              bs, kc, vc)
+                 : cudaSuccess;
 }
 
 cudaError_t residual_add_launch(float* x, const __nv_bfloat16* part, int64_t n, cudaStream_t st) {
-    if (n > 0) residual_add_kernel<<<grid_for(n / 8, 256), 256, 0, st>>>(x, part, n / 8);
-    return cudaGetLastError();
+    return n > 0 ? launch_pdl(residual_add_kernel, dim3(grid_for(n / 8, 256)), dim3(256), 0, st, 1, x, part, n / 8)
+                 : cudaSuccess;
 }
 
 cudaError_t argmax_launch(const float* logits, int rows, int V, int ld, int32_t* out, cudaStream_t st) {
-    if (rows > 0) argmax_kernel<<<rows, 512, 0, st>>>(logits, V, ld, out);
-    return cudaGetLastError();
+    return rows > 0 ? launch_pdl(argmax_kernel, dim3(rows), dim3(512), 0, st, 1, logits, V, ld, out) : cudaSuccess;
 }
 
 cudaError_t gather_vocab_launch(const float* in, float* out, int tp, int rows, int vl, cudaStream_t st) {
     const int64_t n = int64_t(tp) * rows * vl;
-    if (n > 0) gather_vocab_kernel<<<grid_for(n, 256), 256, 0, st>>>(in, out, tp, rows, vl);
-    return cudaGetLastError();
+    return n > 0 ? launch_pdl(gather_vocab_kernel, dim3(grid_for(n, 256)), dim3(256), 0, st, 1, in, out, tp, rows, vl)
+                 : cudaSuccess;
 }
 
 cudaError_t init_weight_launch(__nv_bfloat16* w, const WeightInit& wi, cudaStream_t st) {

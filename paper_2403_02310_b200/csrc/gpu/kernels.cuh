@@ -6,6 +6,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 namespace ssk {
 
 // ------------------------------------------------------------------ K3 GEMM
@@ -123,4 +125,34 @@ cudaError_t kv_fill_launch(__nv_bfloat16* kbase, __nv_bfloat16* vbase, int64_t l
                            const int32_t* bt_dev, int n_tokens, int rid, int nkv_l, int kv_off, int nkv_g, int hd,
                            int bs, uint64_t seed, cudaStream_t st);
 
+}  // namespace ssk
+
+namespace ssk {
+// Launch with the programmatic-stream-serialization attribute (PDL) and an
+// optional cluster shape. Every kernel in this library calls pdl_wait() before
+// its first global access, so PDL launches are always safe.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              int cluster_x, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    int n = 0;
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+    if (cluster_x > 1) {
+        attr[n].id = cudaLaunchAttributeClusterDimension;
+        attr[n].val.clusterDim.x = cluster_x;
+        attr[n].val.clusterDim.y = 1;
+        attr[n].val.clusterDim.z = 1;
+        ++n;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = n;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 }  // namespace ssk
