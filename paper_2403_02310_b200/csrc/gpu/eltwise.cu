@@ -16,16 +16,25 @@ __device__ __forceinline__ float warp_sum(float v) {
 }
 
 __global__ void embed_kernel(const int32_t* __restrict__ tokens, const __nv_bfloat16* __restrict__ table,
-                             float* __restrict__ x, int h) {
+                             float* __restrict__ x, __nv_bfloat16* __restrict__ xb, float* __restrict__ ssq, int h) {
     pdl_launch_dependents();
     pdl_wait();
     const int t = blockIdx.x;
     const uint4* src = reinterpret_cast<const uint4*>(table + size_t(tokens[t]) * h);
     float4* dst = reinterpret_cast<float4*>(x + size_t(t) * h);
+    uint4* dxb = reinterpret_cast<uint4*>(xb + size_t(t) * h);
+    // 8 elements per thread; 4 consecutive threads cover one 32-column chunk
     for (int i = threadIdx.x; i < h / 8; i += blockDim.x) {
         const uint4 v = src[i];
-        dst[2 * i] = make_float4(bf16_lo(v.x), bf16_hi(v.x), bf16_lo(v.y), bf16_hi(v.y));
-        dst[2 * i + 1] = make_float4(bf16_lo(v.z), bf16_hi(v.z), bf16_lo(v.w), bf16_hi(v.w));
+        const float4 a = make_float4(bf16_lo(v.x), bf16_hi(v.x), bf16_lo(v.y), bf16_hi(v.y));
+        const float4 b = make_float4(bf16_lo(v.z), bf16_hi(v.z), bf16_lo(v.w), bf16_hi(v.w));
+        dst[2 * i] = a;
+        dst[2 * i + 1] = b;
+        dxb[i] = v;
+        float ss = a.x * a.x + a.y * a.y + a.z * a.z + a.w * a.w + b.x * b.x + b.y * b.y + b.z * b.z + b.w * b.w;
+        ss += __shfl_xor_sync(0xffffffffu, ss, 1);
+        ss += __shfl_xor_sync(0xffffffffu, ss, 2);
+        if ((i & 3) == 0) ssq[size_t(t) * (h / 32) + i / 4] = ss;
     }
 }
 
@@ -109,17 +118,33 @@ __global__ void rope_append_kernel(const __nv_bfloat16* __restrict__ qkv, __nv_b
     }
 }
 
-__global__ void residual_add_kernel(float* __restrict__ x, const __nv_bfloat16* __restrict__ part, int64_t n8) {
+__global__ void residual_add_kernel(float* __restrict__ x, const __nv_bfloat16* __restrict__ part,
+                                    __nv_bfloat16* __restrict__ xb, float* __restrict__ ssq, int64_t n8, int h) {
     pdl_launch_dependents();
     pdl_wait();
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n8; i += int64_t(gridDim.x) * blockDim.x) {
-        const uint4 v = reinterpret_cast<const uint4*>(part)[i];
-        float4* d = reinterpret_cast<float4*>(x) + 2 * i;
-        float4 a = d[0], b = d[1];
-        a.x += bf16_lo(v.x); a.y += bf16_hi(v.x); a.z += bf16_lo(v.y); a.w += bf16_hi(v.y);
-        b.x += bf16_lo(v.z); b.y += bf16_hi(v.z); b.z += bf16_lo(v.w); b.w += bf16_hi(v.w);
-        d[0] = a;
-        d[1] = b;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;  // multiple of 32
+    for (int64_t base = blockIdx.x * int64_t(blockDim.x); base < n8; base += stride) {
+        const int64_t i = base + threadIdx.x;
+        const bool act = i < n8;
+        float ss = 0.f;
+        if (act) {
+            const uint4 v = reinterpret_cast<const uint4*>(part)[i];
+            float4* d = reinterpret_cast<float4*>(x) + 2 * i;
+            float4 a = d[0], b = d[1];
+            a.x += bf16_lo(v.x); a.y += bf16_hi(v.x); a.z += bf16_lo(v.y); a.w += bf16_hi(v.y);
+            b.x += bf16_lo(v.z); b.y += bf16_hi(v.z); b.z += bf16_lo(v.w); b.w += bf16_hi(v.w);
+            d[0] = a;
+            d[1] = b;
+            reinterpret_cast<uint4*>(xb)[i] =
+                make_uint4(pack_bf16(a.x, a.y), pack_bf16(a.z, a.w), pack_bf16(b.x, b.y), pack_bf16(b.z, b.w));
+            ss = a.x * a.x + a.y * a.y + a.z * a.z + a.w * a.w + b.x * b.x + b.y * b.y + b.z * b.z + b.w * b.w;
+        }
+        ss += __shfl_xor_sync(0xffffffffu, ss, 1);
+        ss += __shfl_xor_sync(0xffffffffu, ss, 2);
+        if (act && (i & 3) == 0) {  // 4 threads = one 32-column chunk of one row
+            const int64_t row = i / (h / 8), g = i % (h / 8);
+            ssq[row * (h / 32) + g / 4] = ss;
+        }
     }
 }
 
@@ -261,8 +286,9 @@ int grid_for(int64_t n, int threads) {
 
 }  // namespace
 
-cudaError_t embed_launch(const int32_t* tokens, const __nv_bfloat16* table, float* x, int T, int h, cudaStream_t st) {
-    return T > 0 ? launch_pdl(embed_kernel, dim3(T), dim3(256), 0, st, 1, tokens, table, x, h) : cudaSuccess;
+cudaError_t embed_launch(const int32_t* tokens, const __nv_bfloat16* table, float* x, __nv_bfloat16* xb, float* ssq,
+                         int T, int h, cudaStream_t st) {
+    return T > 0 ? launch_pdl(embed_kernel, dim3(T), dim3(256), 0, st, 1, tokens, table, x, xb, ssq, h) : cudaSuccess;
 }
 
 cudaError_t rmsnorm_launch(const float* x, const __nv_bfloat16* w, __nv_bfloat16* out, const int32_t* rows, int M,
@@ -279,9 +305,12 @@ cudaError_t rope_append_launch(const __nv_bfloat16* qkv, __nv_bfloat16* q_out, c
                  : cudaSuccess;
 }
 
-cudaError_t residual_add_launch(float* x, const __nv_bfloat16* part, int64_t n, cudaStream_t st) {
-    return n > 0 ? launch_pdl(residual_add_kernel, dim3(grid_for(n / 8, 256)), dim3(256), 0, st, 1, x, part, n / 8)
-                 : cudaSuccess;
+cudaError_t residual_add_launch(float* x, const __nv_bfloat16* part, __nv_bfloat16* xb, float* ssq, int T, int h,
+                                cudaStream_t st) {
+    const int64_t n8 = int64_t(T) * h / 8;
+    return n8 > 0 ? launch_pdl(residual_add_kernel, dim3(grid_for(n8, 256)), dim3(256), 0, st, 1, x, part, xb, ssq, n8,
+                               h)
+                  : cudaSuccess;
 }
 
 cudaError_t argmax_launch(const float* logits, int rows, int V, int ld, int32_t* out, cudaStream_t st) {

@@ -190,7 +190,8 @@ struct SegIter {
 };
 
 template <int EPI>
-__device__ __forceinline__ void epi_store(const uint32_t (&v)[32], int row, int col, void* out, int ldo) {
+__device__ __forceinline__ void epi_store(const uint32_t (&v)[32], int row, int col, void* out, int ldo,
+                                          const EpiArgs& ea) {
     if constexpr (EPI == EPI_BF16) {
         __nv_bfloat16* o = static_cast<__nv_bfloat16*>(out) + size_t(row) * ldo + col;
 #pragma unroll
@@ -202,6 +203,8 @@ __device__ __forceinline__ void epi_store(const uint32_t (&v)[32], int row, int 
                            pack_bf16(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7])));
     } else if constexpr (EPI == EPI_RESADD) {
         float4* o = reinterpret_cast<float4*>(static_cast<float*>(out) + size_t(row) * ldo + col);
+        float ss = 0.f;
+        uint32_t pk[16];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
             float4 x = o[j];
@@ -210,6 +213,15 @@ __device__ __forceinline__ void epi_store(const uint32_t (&v)[32], int row, int 
             x.z += __uint_as_float(v[4 * j + 2]);
             x.w += __uint_as_float(v[4 * j + 3]);
             o[j] = x;
+            ss += x.x * x.x + x.y * x.y + x.z * x.z + x.w * x.w;
+            pk[2 * j] = pack_bf16(x.x, x.y);
+            pk[2 * j + 1] = pack_bf16(x.z, x.w);
+        }
+        if (ea.xb_out) {  // feed the next norm-folded GEMM: bf16 row copy + chunk sum of squares
+            uint4* xb = reinterpret_cast<uint4*>(ea.xb_out + size_t(row) * ldo + col);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) xb[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+            ea.ssq_out[size_t(row) * (ldo / 32) + col / 32] = ss;
         }
     } else {  // EPI_F32
         float4* o = reinterpret_cast<float4*>(static_cast<float*>(out) + size_t(row) * ldo + col);
@@ -237,7 +249,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
                         int N, int K, void* __restrict__ out, int ldo, int num_mt, int num_tiles,
                         float* __restrict__ part, uint32_t* __restrict__ flags, uint32_t epoch, int sk_mode,
-                        int sk_slices) {
+                        int sk_slices, const EpiArgs ea) {
     using Cfg = GemmCfg<CG, BN>;
     constexpr int STAGES = Cfg::STAGES;
     extern __shared__ uint8_t smem_raw[];
@@ -395,7 +407,73 @@ __global__ void __launch_bounds__(kThreads, 1)
                     while (ld_acquire_gpu(f) != epoch)
                         if (++spins == (1u << 28)) __trap();
                 }
-                if constexpr (EPI == EPI_SWIGLU) {
+                // RMSNorm of the A row, folded in: scale = rsqrt(mean(x^2) + eps)
+                float rs = 1.f;
+                if (ea.ssq_in && row < M) {
+                    const float4* q4 = reinterpret_cast<const float4*>(ea.ssq_in + size_t(row) * ea.ssq_in_n);
+                    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+                    for (int i = 0; i < ea.ssq_in_n / 4; ++i) {
+                        const float4 w = q4[i];
+                        a0 += w.x;
+                        a1 += w.y;
+                        a2 += w.z;
+                        a3 += w.w;
+                    }
+                    rs = rsqrtf(((a0 + a1) + (a2 + a3)) * ea.inv_dim + ea.eps);
+                }
+                if constexpr (EPI == EPI_QKV) {
+                    // chunk pairs (c, c + ps) hold the rotate-half partners i, i + hd/2 of one head
+                    const int ps = ea.hd / 64;
+                    const int row_ok = row < M;
+                    const int p_row = row_ok ? ea.pos[row] : 0;
+                    const int64_t s_row = row_ok ? ea.slot[row] : 0;
+                    const int64_t blk = s_row / ea.bs, off = s_row % ea.bs;
+#pragma unroll 1
+                    for (int pi = half; pi < (BN / ea.hd) * ps; pi += 2) {
+                        const int c = (pi / ps) * (2 * ps) + (pi % ps);
+                        uint32_t x1[32], x2[32];
+                        tmem_ld32(t_row + uint32_t(c * 32), x1);
+                        tmem_ld32(t_row + uint32_t((c + ps) * 32), x2);
+                        tmem_wait_ld();
+                        for (int g = gid + 1; g <= g_last; ++g) {
+                            const float* src = part + (size_t(g) * Cfg::TILE_M + rloc) * BN;
+                            add_partial(x1, src + c * 32);
+                            add_partial(x2, src + (c + ps) * 32);
+                        }
+                        const int col = n0 + c * 32;
+                        if (!row_ok || col >= N) continue;
+                        const int hh = col / ea.hd, i0 = col % ea.hd;  // i0 < hd/2
+                        uint32_t lo[16], hi[16];
+                        if (hh < ea.nq + ea.nkv) {  // q or k head: rotate
+                            const float2* cs = ea.rope + size_t(p_row) * (ea.hd / 2) + i0;
+#pragma unroll
+                            for (int j = 0; j < 16; ++j) {
+                                const float2 c0 = cs[2 * j], c1 = cs[2 * j + 1];
+                                const float a0 = __uint_as_float(x1[2 * j]) * rs, a1 = __uint_as_float(x1[2 * j + 1]) * rs;
+                                const float b0 = __uint_as_float(x2[2 * j]) * rs, b1 = __uint_as_float(x2[2 * j + 1]) * rs;
+                                lo[j] = pack_bf16(a0 * c0.x - b0 * c0.y, a1 * c1.x - b1 * c1.y);
+                                hi[j] = pack_bf16(b0 * c0.x + a0 * c0.y, b1 * c1.x + a1 * c1.y);
+                            }
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 16; ++j) {
+                                lo[j] = pack_bf16(__uint_as_float(x1[2 * j]) * rs, __uint_as_float(x1[2 * j + 1]) * rs);
+                                hi[j] = pack_bf16(__uint_as_float(x2[2 * j]) * rs, __uint_as_float(x2[2 * j + 1]) * rs);
+                            }
+                        }
+                        __nv_bfloat16* dst;
+                        if (hh < ea.nq) dst = ea.q_out + (size_t(row) * ea.nq + hh) * ea.hd;
+                        else if (hh < ea.nq + ea.nkv) dst = ea.kc + ((size_t(blk) * ea.nkv + (hh - ea.nq)) * ea.bs + off) * ea.hd;
+                        else dst = ea.vc + ((size_t(blk) * ea.nkv + (hh - ea.nq - ea.nkv)) * ea.bs + off) * ea.hd;
+                        uint4* d1 = reinterpret_cast<uint4*>(dst + i0);
+                        uint4* d2 = reinterpret_cast<uint4*>(dst + i0 + ea.hd / 2);
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            d1[j] = make_uint4(lo[4 * j], lo[4 * j + 1], lo[4 * j + 2], lo[4 * j + 3]);
+                            d2[j] = make_uint4(hi[4 * j], hi[4 * j + 1], hi[4 * j + 2], hi[4 * j + 3]);
+                        }
+                    }
+                } else if constexpr (EPI == EPI_SWIGLU) {
 #pragma unroll 1
                     for (int c = 2 * half; c < BN / 32; c += 4) {
                         uint32_t gt[32], ut[32];
@@ -413,8 +491,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                             uint32_t pk[16];
 #pragma unroll
                             for (int j = 0; j < 16; ++j)
-                                pk[j] = pack_bf16(silu(__uint_as_float(gt[2 * j])) * __uint_as_float(ut[2 * j]),
-                                                  silu(__uint_as_float(gt[2 * j + 1])) * __uint_as_float(ut[2 * j + 1]));
+                                pk[j] = pack_bf16(
+                                    silu(__uint_as_float(gt[2 * j]) * rs) * (__uint_as_float(ut[2 * j]) * rs),
+                                    silu(__uint_as_float(gt[2 * j + 1]) * rs) * (__uint_as_float(ut[2 * j + 1]) * rs));
 #pragma unroll
                             for (int j = 0; j < 4; ++j)
                                 reinterpret_cast<uint4*>(o)[j] =
@@ -429,8 +508,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                         tmem_wait_ld();
                         for (int g = gid + 1; g <= g_last; ++g)
                             add_partial(v, part + (size_t(g) * Cfg::TILE_M + rloc) * BN + c * 32);
+                        if (ea.ssq_in) {
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) * rs);
+                        }
                         const int col = n0 + c * 32;
-                        if (row < M && col < N) epi_store<EPI>(v, row, col, out, ldo);
+                        if (row < M && col < N) epi_store<EPI>(v, row, col, out, ldo, ea);
                     }
                 }
             }
@@ -522,7 +605,7 @@ cudaError_t launch_t(const GemmPlan& p, cudaStream_t st) {
         fprintf(stderr, "gemm cg=%d bn=%d epi=%d M=%d N=%d K=%d tiles=%d resident=%d mode=%d groups=%d\n", CG, BN,
                 EPI, p.M, p.N, p.K, tiles, resident, mode, groups);
     return cudaLaunchKernelEx(&cfg, kern, p.tmA, p.tmB, p.M, p.N, p.K, p.out, p.ldo, num_mt, tiles, p.part,
-                              p.flags, p.epoch, mode, S);
+                              p.flags, p.epoch, mode, S, p.ea);
 }
 
 // Tile shapes compiled: CG=2 pairs with BN in steps of 32, CG=1 with 128 / 256.
@@ -564,6 +647,7 @@ GemmShape gemm_pick(int M, int N, int K, int epi, int num_sms) {
     const double kscale = double((K + BK - 1) / BK) / 64.0;
     auto consider = [&](int cg, int bn) {
         if (swiglu && bn % 64) return;
+        if (epi == EPI_QKV && bn % 128) return;  // whole heads per tile (hd 64 or 128)
         if (force_bn && bn != force_bn) return;
         if (force_cg && cg != force_cg) return;
         const long tiles = long((M + 128 * cg - 1) / (128 * cg)) * ((N + bn - 1) / bn);
@@ -593,7 +677,7 @@ GemmShape gemm_pick(int M, int N, int K, int epi, int num_sms) {
 
 bool gemm_prepare(GemmPlan& p, const void* A, uint64_t a_rows, const void* B, int M, int N, int K, void* out,
                   int ldo, int epi, int num_sms, int bn) {
-    if (M < 1 || N < 32 || K < 16 || N % 32 || K % 8 || (epi == EPI_SWIGLU && N % 64)) return false;
+    if (M < 1 || N < 32 || K < 16 || N % 32 || K % 8 || (epi == EPI_SWIGLU && N % 64) || epi == EPI_QKV) return false;
     p.M = M;
     p.N = N;
     p.K = K;
@@ -617,6 +701,7 @@ cudaError_t gemm_launch(const GemmPlan& p, cudaStream_t st) {
         if (p.epi == EPI_RESADD) return launch_t<CGv, BNv, EPI_RESADD>(p, st);      \
         if (p.epi == EPI_F32) return launch_t<CGv, BNv, EPI_F32>(p, st);            \
         if (p.epi == EPI_SWIGLU && BNv % 64 == 0) return launch_t<CGv, (BNv % 64 == 0 ? BNv : 64), EPI_SWIGLU>(p, st); \
+        if (p.epi == EPI_QKV && BNv % 128 == 0) return launch_t<CGv, (BNv % 128 == 0 ? BNv : 128), EPI_QKV>(p, st); \
     }
     SS_GEMM_CASE(1, 128)
     SS_GEMM_CASE(1, 256)

@@ -11,7 +11,29 @@
 namespace ssk {
 
 // ------------------------------------------------------------------ K3 GEMM
-enum { EPI_BF16 = 0, EPI_RESADD = 1, EPI_SWIGLU = 2, EPI_F32 = 3 };
+enum { EPI_BF16 = 0, EPI_RESADD = 1, EPI_SWIGLU = 2, EPI_F32 = 3, EPI_QKV = 4 };
+
+// Extra epilogue operands (all optional / mode specific).
+struct EpiArgs {
+    // RMSNorm folded into the consumer GEMM: A holds the un-normalised bf16 rows;
+    // each output row is scaled by rsqrt(sum(ssq_in[row][0..ssq_in_n)) * inv_dim + eps)
+    // (norm gains are folded into the weights). Fixed summation order: deterministic.
+    const float* ssq_in = nullptr;
+    int ssq_in_n = 0;
+    float inv_dim = 0.f, eps = 0.f;
+    // EPI_RESADD producer side: bf16 copy of the updated residual row and the
+    // per-(row, 32-column chunk) sums of squares the next consumer needs
+    __nv_bfloat16* xb_out = nullptr;
+    float* ssq_out = nullptr;
+    // EPI_QKV: RoPE (rotate-half) of q/k heads + paged KV append; q -> q_out
+    const int32_t* pos = nullptr;
+    const int64_t* slot = nullptr;
+    const float2* rope = nullptr;
+    __nv_bfloat16* q_out = nullptr;
+    __nv_bfloat16* kc = nullptr;
+    __nv_bfloat16* vc = nullptr;
+    int nq = 0, nkv = 0, hd = 0, bs = 16;
+};
 
 struct GemmPlan {
     CUtensorMap tmA, tmB;  // 64-byte aligned members of a 64-aligned struct
@@ -29,6 +51,7 @@ struct GemmPlan {
     uint32_t epoch = 0;
     int sk_mode = -1;  // -1 auto, 0 whole tiles round-robin, 1 stream-K, 2 lockstep split-K
     int splits = 1;    // K slices per tile for mode 2 (tiles * splits must fit one resident wave)
+    EpiArgs ea;
 } __attribute__((aligned(64)));
 
 // Workspace sizes for gemm_launch (max over tile shapes) for num_sms SMs.
@@ -98,15 +121,19 @@ cudaError_t attention_launch(const AttnParams& p, const CUtensorMap& tk, const C
 cudaError_t attention_combine_launch(const AttnParams& p, cudaStream_t st);
 
 // ------------------------------------------------------------------ K2/K4 elementwise
-cudaError_t embed_launch(const int32_t* tokens, const __nv_bfloat16* table, float* x, int T, int h,
-                         cudaStream_t st);
+// x = embed[tokens] (fp32) plus the bf16 copy and per-chunk sums of squares the
+// first (norm-folded) QKV GEMM consumes.
+cudaError_t embed_launch(const int32_t* tokens, const __nv_bfloat16* table, float* x, __nv_bfloat16* xb, float* ssq,
+                         int T, int h, cudaStream_t st);
 cudaError_t rmsnorm_launch(const float* x, const __nv_bfloat16* w, __nv_bfloat16* out, const int32_t* rows, int M,
                            int h, float eps, cudaStream_t st);
 // RoPE (rotate-half) of q and k heads + paged KV append of k and v.
 cudaError_t rope_append_launch(const __nv_bfloat16* qkv, __nv_bfloat16* q_out, const int32_t* pos,
                                const int64_t* slot, const float2* rope_cs, int T, int nq_l, int nkv_l, int hd,
                                int bs, __nv_bfloat16* kc, __nv_bfloat16* vc, cudaStream_t st);
-cudaError_t residual_add_launch(float* x, const __nv_bfloat16* part, int64_t n, cudaStream_t st);
+// x += part (TP all-reduce result), also refreshing xb / ssq for the next norm-folded GEMM.
+cudaError_t residual_add_launch(float* x, const __nv_bfloat16* part, __nv_bfloat16* xb, float* ssq, int T, int h,
+                                cudaStream_t st);
 cudaError_t argmax_launch(const float* logits, int rows, int V, int ld, int32_t* out, cudaStream_t st);
 // logits gathered [tp][rows][V_l] -> [rows][tp * V_l]
 cudaError_t gather_vocab_launch(const float* in, float* out, int tp, int rows, int vl, cudaStream_t st);
