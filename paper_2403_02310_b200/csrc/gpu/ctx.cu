@@ -137,6 +137,7 @@ struct ss_ctx {
     int32_t* comb_count = nullptr;  // split-KV group counters (self-resetting)
     int fused_combine = 0;          // in-kernel split merge (measured slower at 8 splits; off)
     int decode_split = 1536;        // target keys per split-KV piece for decode-like items (measured)
+    int fuse_rope = 1;              // RoPE + KV append in the QKV GEMM epilogue (else the K2 kernel)
     float* sk_part = nullptr;       // stream-K GEMM partial accumulators
     uint32_t* sk_flags = nullptr;   // stream-K ready flags
     uint32_t sk_epoch = 0;
@@ -549,7 +550,15 @@ ss_status enqueue_forward(ss_ctx* ctx, const ss_batch* b) {
         qkv_ea.nkv = ctx->nkv_l;
         qkv_ea.hd = ctx->hd;
         qkv_ea.bs = ctx->bs;
-        RUN(gemm(ctx, SS_K_GEMM_QKV, ctx->ta_xb, W.tb_qkv, T, qkvN, h, nullptr, qkvN, EPI_QKV, qkv_ea));
+        if (ctx->fuse_rope) {
+            RUN(gemm(ctx, SS_K_GEMM_QKV, ctx->ta_xb, W.tb_qkv, T, qkvN, h, nullptr, qkvN, EPI_QKV, qkv_ea));
+        } else {
+            RUN(gemm(ctx, SS_K_GEMM_QKV, ctx->ta_xb, W.tb_qkv, T, qkvN, h, ctx->qkv, qkvN, EPI_BF16, norm_in));
+            RUN(launch(ctx, SS_K_ROPE_APPEND, 1, [&] {
+                return rope_append_launch(ctx->qkv, ctx->q, b->pos, b->slot, ctx->rope, T, ctx->nq_l, ctx->nkv_l,
+                                          ctx->hd, ctx->bs, qkv_ea.kc, qkv_ea.vc, ctx->st);
+            }));
+        }
         const AttnParams ap = attn_params(ctx, b, ctx->q, ctx->o, l);
         RUN(launch(ctx, SS_K_ATTN, 1, [&] { return attention_launch(ap, ctx->tm_k, ctx->tm_v, ctx->st); }));
         if (b->n_combs && !ctx->fused_combine)
@@ -683,6 +692,7 @@ SS_API ss_status ss_create(const ss_model_cfg* cfg, int32_t tp_rank, int32_t tp_
     ctx->seed = weight_seed;
     if (const char* f = getenv("SS_ATTN_SPLIT")) ctx->decode_split = std::max(64, atoi(f) / 64 * 64);  // dev tuning
     if (const char* f = getenv("SS_ATTN_FUSED_COMBINE")) ctx->fused_combine = atoi(f);
+    if (const char* f = getenv("SS_FUSE_ROPE")) ctx->fuse_rope = atoi(f);
     if (cudaMalloc(&ctx->sk_part, gemm_part_floats(ctx->num_sms) * 4) != cudaSuccess ||
         cudaMalloc(&ctx->sk_flags, gemm_flag_words(ctx->num_sms) * 4) != cudaSuccess ||
         cudaMemset(ctx->sk_flags, 0, gemm_flag_words(ctx->num_sms) * 4) != cudaSuccess) {

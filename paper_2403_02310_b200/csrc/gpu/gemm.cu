@@ -372,6 +372,23 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int t = sg.t, kb0 = sg.kb0, kb1 = sg.kb1;
             const int m0 = (t % num_mt) * Cfg::TILE_M, n0 = (t / num_mt) * BN;
             const int row = m0 + rloc;
+            // RMSNorm of the A row, folded in: scale = rsqrt(mean(x^2) + eps). The
+            // sums of squares come from the previous kernel, so this overlaps the
+            // tile's main loop (computed before waiting for the accumulator).
+            float rs = 1.f;
+            if (ea.ssq_in && row < M) {
+                const float4* q4 = reinterpret_cast<const float4*>(ea.ssq_in + size_t(row) * ea.ssq_in_n);
+                float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll 8
+                for (int i = 0; i < ea.ssq_in_n / 4; ++i) {
+                    const float4 w = __ldg(q4 + i);
+                    a0 += w.x;
+                    a1 += w.y;
+                    a2 += w.z;
+                    a3 += w.w;
+                }
+                rs = rsqrtf(((a0 + a1) + (a2 + a3)) * ea.inv_dim + ea.eps);
+            }
             mbar_wait(&tfull[acc], acc_ph);
             tc_fence_after();
             const uint32_t t_row = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN);
@@ -406,20 +423,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                     uint32_t spins = 0;
                     while (ld_acquire_gpu(f) != epoch)
                         if (++spins == (1u << 28)) __trap();
-                }
-                // RMSNorm of the A row, folded in: scale = rsqrt(mean(x^2) + eps)
-                float rs = 1.f;
-                if (ea.ssq_in && row < M) {
-                    const float4* q4 = reinterpret_cast<const float4*>(ea.ssq_in + size_t(row) * ea.ssq_in_n);
-                    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-                    for (int i = 0; i < ea.ssq_in_n / 4; ++i) {
-                        const float4 w = q4[i];
-                        a0 += w.x;
-                        a1 += w.y;
-                        a2 += w.z;
-                        a3 += w.w;
-                    }
-                    rs = rsqrtf(((a0 + a1) + (a2 + a3)) * ea.inv_dim + ea.eps);
                 }
                 if constexpr (EPI == EPI_QKV) {
                     // chunk pairs (c, c + ps) hold the rotate-half partners i, i + hd/2 of one head
