@@ -174,10 +174,20 @@ struct SegIter {
             return true;
         }
         if (mode == 2) {
-            if (t_rr >= num_tiles * S) return false;
-            const int sl = t_rr % S;
-            s = Seg{t_rr / S, sl * num_kb / S, (sl + 1) * num_kb / S};
-            t_rr += 1 << 30;  // one unit per group
+            // whole tiles for the full waves, then the ragged last wave split in
+            // S aligned K slices (one unit per group, consecutive groups per tile)
+            const int full = (num_tiles / G) * G;
+            if (t_rr < full) {
+                s = Seg{t_rr, 0, num_kb};
+                t_rr += G;
+                return true;
+            }
+            if (t_rr >= (1 << 29)) return false;
+            const int u = t_rr - full - (t_rr - full) / G * G;  // == gid
+            t_rr = 1 << 29;
+            if (u >= (num_tiles - full) * S) return false;
+            const int sl = u % S;
+            s = Seg{full + u / S, sl * num_kb / S, (sl + 1) * num_kb / S};
             return true;
         }
         if (i >= i1) return false;
@@ -598,11 +608,13 @@ cudaError_t launch_t(const GemmPlan& p, cudaStream_t st) {
     if (mode < 0) mode = S > 1 ? 2 : 0;
     if (const char* f = getenv("SS_GEMM_SK")) mode = atoi(f);
     if (const char* f = getenv("SS_GEMM_SPLITS")) S = atoi(f);
-    if (mode == 2 && (S < 2 || long(tiles) * S > resident)) mode = 0;  // lockstep split needs one wave
+    const int rem = tiles % resident;  // tiles of the ragged last wave
+    if (mode == 2 && rem > 0 && long(rem) * S > resident) S = resident / rem;
+    if (mode == 2 && (S < 2 || rem == 0)) mode = 0;  // nothing to split
     int groups = resident;
     if (mode == 0 && tiles < groups) groups = tiles;
     if (mode == 1 && iters < groups) groups = int(iters);
-    if (mode == 2) groups = tiles * S;
+    if (mode == 2 && tiles < resident) groups = tiles * S;
     cfg.gridDim = dim3(CG * groups);
     if (getenv("SS_GEMM_DEBUG"))
         fprintf(stderr, "gemm cg=%d bn=%d epi=%d M=%d N=%d K=%d tiles=%d resident=%d mode=%d groups=%d\n", CG, BN,
@@ -655,14 +667,16 @@ GemmShape gemm_pick(int M, int N, int K, int epi, int num_sms) {
         if (force_cg && cg != force_cg) return;
         const long tiles = long((M + 128 * cg - 1) / (128 * cg)) * ((N + bn - 1) / bn);
         const long slots = num_sms / cg;
+        const long full = tiles / slots, rem = tiles % slots;
         for (int S = 1; S <= 4; ++S) {
             if (force_s && S != force_s) continue;
-            if (S > 1 && tiles * S > slots) break;
-            const long waves = S == 1 ? (tiles + slots - 1) / slots : 1;
-            // + exposed epilogue (~6 us when a group owns one tile); split-K adds the
-            // partial write / fixup read of a 256-wide fp32 tile (measured ~2.5x that)
-            const double epi = waves == 1 ? 6.0 : 0.0;
-            const double cost = double(waves) * tile_us(cg, bn) * kscale / S + (S > 1 ? 3.5 * 6.0 : epi);
+            if (S > 1 && (rem == 0 || rem * S > slots)) break;
+            // whole-tile waves + the ragged last wave, its tiles split S ways in K;
+            // + exposed epilogue (~6 us at the end); split-K adds the partial write
+            // and fixup read of a 256-wide fp32 tile (measured ~2.5x that)
+            const double t1 = tile_us(cg, bn) * kscale;
+            const double last = rem == 0 ? 0.0 : t1 / S + (S > 1 ? 3.5 * 6.0 : 0.0);
+            const double cost = double(full) * t1 + last + 6.0;
             if (cost < best_cost - 1e-9) {
                 best_cost = cost;
                 best = GemmShape{cg, bn, S};
