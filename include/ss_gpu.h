@@ -91,6 +91,18 @@ ss_status ss_kv_alloc(ss_ctx* ctx, int64_t num_blocks, int32_t block_size);
 ss_status ss_forward_hybrid(ss_ctx* ctx, const ss_batch_desc* desc, float* logits_out,
                             int32_t* next_tokens_out, float* elapsed_ms);
 
+/* Tensor parallelism on ONE device (validation transport where only one GPU is
+ * visible): creates tp_size rank contexts (out[0..tp_size-1]) that share one
+ * stream; ss_forward_local_group drives one host thread per rank through the
+ * same sharded forward as a tp-GPU job, with every NCCL collective replaced by
+ * host barriers + a peer-sum kernel (all-reduce) / peer copies (all-gather).
+ * Each rank still needs ss_kv_alloc (+ fills) on its own context; outputs are
+ * rank 0's. ss_destroy each context; the shared stream goes with the last. */
+ss_status ss_create_local_group(const ss_model_cfg* cfg, int32_t tp_size, uint64_t weight_seed,
+                                int32_t device, ss_ctx** out);
+ss_status ss_forward_local_group(ss_ctx* const* ranks, int32_t n, const ss_batch_desc* desc,
+                                 float* logits_out, int32_t* next_tokens_out, float* elapsed_ms);
+
 /* Device-resident batches for steady-state timing: upload once, then enqueue
  * forwards on the context stream without host synchronisation. */
 typedef struct ss_batch ss_batch;

@@ -18,8 +18,11 @@
 
 #include <algorithm>
 #include <cmath>
+#include <condition_variable>
 #include <cstring>
+#include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../../include/ss_gpu.h"
@@ -109,6 +112,46 @@ struct ss_batch {
     int n_items = 0, n_combs = 0, part_rows = 0;
 };
 
+// Tensor parallelism on ONE device, for validating the sharded forward where only
+// one GPU is visible: tp contexts share a stream, the caller drives one host
+// thread per rank, and each collective is a host barrier (every rank's producer
+// kernel enqueued) + a peer-sum kernel / peer copies + a second barrier (every
+// reader enqueued before any rank overwrites its buffer). The kernels, shard
+// math and call sequence are the tp-GPU ones; only the NCCL call differs.
+struct LocalGroup {
+    int n = 0, live = 0;
+    cudaStream_t st = nullptr;
+    std::vector<ss_ctx*> ranks;
+    std::mutex mu;
+    std::condition_variable cv;
+    int arrived = 0;
+    uint64_t gen = 0;
+    bool aborted = false;
+    bool barrier() {
+        std::unique_lock<std::mutex> lk(mu);
+        if (aborted) return false;
+        const uint64_t g = gen;
+        if (++arrived == n) {
+            arrived = 0;
+            ++gen;
+            cv.notify_all();
+            return true;
+        }
+        cv.wait(lk, [&] { return gen != g || aborted; });
+        return gen != g;
+    }
+    void abort() {
+        std::lock_guard<std::mutex> lk(mu);
+        aborted = true;
+        cv.notify_all();
+    }
+    void reset() {
+        std::lock_guard<std::mutex> lk(mu);
+        aborted = false;
+        arrived = 0;
+    }
+};
+
 struct ss_ctx {
     ss_model_cfg cfg{};
     int rank = 0, tp = 1, device = 0, num_sms = 148;
@@ -152,6 +195,8 @@ struct ss_ctx {
     const ss_batch* last = nullptr;
 
     ncclComm_t comm = nullptr;
+    LocalGroup* grp = nullptr;  // set instead of comm for a one-device TP group
+    bf16* part_red = nullptr;   // local-group all-reduce result
 
     bool prof = false;
     std::vector<Prof> pend;
@@ -263,6 +308,8 @@ ss_status ensure_workspace(ss_ctx* ctx, int T, int n_out, int part_rows) {
         cudaFree(ctx->part);
         cudaFree(ctx->xb);
         cudaFree(ctx->ssq);
+        cudaFree(ctx->part_red);
+        ctx->part_red = nullptr;
         const size_t h = size_t(ctx->h), qd = size_t(ctx->nq_l) * ctx->hd;
         const size_t qkvd = size_t(ctx->nq_l + 2 * ctx->nkv_l) * ctx->hd;
         CK(cudaMalloc(&ctx->x, size_t(cap) * h * 4));
@@ -274,6 +321,7 @@ ss_status ensure_workspace(ss_ctx* ctx, int T, int n_out, int part_rows) {
         CK(cudaMalloc(&ctx->part, size_t(cap) * h * 2));
         CK(cudaMalloc(&ctx->xb, size_t(cap) * h * 2));
         CK(cudaMalloc(&ctx->ssq, size_t(cap) * (h / 32) * 4));
+        if (ctx->grp) CK(cudaMalloc(&ctx->part_red, size_t(cap) * h * 2));
         ctx->T_cap = cap;
         if (!make_tmap_2d(&ctx->ta_xn, ctx->xn, cap, h, 128, 64) ||
             !make_tmap_2d(&ctx->ta_o, ctx->o, cap, qd, 128, 64) ||
@@ -507,9 +555,40 @@ ss_status gemm(ss_ctx* ctx, int cls, const CUtensorMap& ta, WMaps& tb, int M, in
     return launch(ctx, cls, 1, [&] { return gemm_launch(p, ctx->st); });
 }
 
-ss_status allreduce_bf16(ss_ctx* ctx, bf16* buf, size_t n) {
+// Sums this rank's partial (n bf16) over the TP group; *sum = where the result lives.
+ss_status allreduce_bf16(ss_ctx* ctx, bf16* buf, size_t n, const bf16** sum) {
+    if (LocalGroup* g = ctx->grp) {
+        if (!g->barrier()) return fail(ctx, SS_NCCL_ERROR, "local TP group aborted by another rank");
+        PeerBufs pb{};
+        for (int r = 0; r < g->n; ++r) pb.p[r] = g->ranks[size_t(r)]->part;
+        if (ss_status s = launch(ctx, SS_K_ALLREDUCE, 1,
+                                 [&] { return peer_sum_launch(ctx->part_red, pb, g->n, int64_t(n), ctx->st); }))
+            return s;
+        if (!g->barrier()) return fail(ctx, SS_NCCL_ERROR, "local TP group aborted by another rank");
+        *sum = ctx->part_red;
+        return SS_OK;
+    }
+    *sum = buf;
     return launch(ctx, SS_K_ALLREDUCE, 1, [&]() -> cudaError_t {
         return g_nccl.all_reduce(buf, buf, n, ncclBfloat16, ncclSum, ctx->comm, ctx->st) == ncclSuccess
+                   ? cudaSuccess
+                   : cudaErrorUnknown;
+    });
+}
+
+// logits_l (n_out x vocab_l, this rank's vocab shard) of every rank -> logits_g (rank-major).
+ss_status allgather_logits(ss_ctx* ctx, int n_out) {
+    const size_t cnt = size_t(n_out) * ctx->vocab_l;
+    if (LocalGroup* g = ctx->grp) {
+        if (!g->barrier()) return fail(ctx, SS_NCCL_ERROR, "local TP group aborted by another rank");
+        for (int r = 0; r < g->n; ++r)
+            CK(cudaMemcpyAsync(ctx->logits_g + size_t(r) * cnt, g->ranks[size_t(r)]->logits_l, cnt * 4,
+                               cudaMemcpyDeviceToDevice, ctx->st));
+        if (!g->barrier()) return fail(ctx, SS_NCCL_ERROR, "local TP group aborted by another rank");
+        return SS_OK;
+    }
+    return launch(ctx, SS_K_ALLREDUCE, 1, [&]() -> cudaError_t {
+        return g_nccl.all_gather(ctx->logits_l, ctx->logits_g, cnt, ncclFloat32, ctx->comm, ctx->st) == ncclSuccess
                    ? cudaSuccess
                    : cudaErrorUnknown;
     });
@@ -567,10 +646,10 @@ ss_status enqueue_forward(ss_ctx* ctx, const ss_batch* b) {
             RUN(gemm(ctx, SS_K_GEMM_O, ctx->ta_o, W.tb_o, T, h, qd, ctx->x, h, EPI_RESADD, res_out));
         } else {
             RUN(gemm(ctx, SS_K_GEMM_O, ctx->ta_o, W.tb_o, T, h, qd, ctx->part, h, EPI_BF16));
-            RUN(allreduce_bf16(ctx, ctx->part, size_t(T) * h));
-            RUN(launch(ctx, SS_K_ALLREDUCE, 1, [&] {
-                return residual_add_launch(ctx->x, ctx->part, ctx->xb, ctx->ssq, T, h, ctx->st);
-            }));
+            const bf16* sum = nullptr;
+            RUN(allreduce_bf16(ctx, ctx->part, size_t(T) * h, &sum));
+            RUN(launch(ctx, SS_K_ALLREDUCE, 1,
+                       [&] { return residual_add_launch(ctx->x, sum, ctx->xb, ctx->ssq, T, h, ctx->st); }));
         }
         RUN(gemm(ctx, SS_K_GEMM_GATEUP, ctx->ta_xb, W.tb_gu, T, 2 * ctx->ffn_l, h, ctx->act, ctx->ffn_l, EPI_SWIGLU,
                  norm_in));
@@ -578,10 +657,10 @@ ss_status enqueue_forward(ss_ctx* ctx, const ss_batch* b) {
             RUN(gemm(ctx, SS_K_GEMM_DOWN, ctx->ta_act, W.tb_down, T, h, ctx->ffn_l, ctx->x, h, EPI_RESADD, res_out));
         } else {
             RUN(gemm(ctx, SS_K_GEMM_DOWN, ctx->ta_act, W.tb_down, T, h, ctx->ffn_l, ctx->part, h, EPI_BF16));
-            RUN(allreduce_bf16(ctx, ctx->part, size_t(T) * h));
-            RUN(launch(ctx, SS_K_ALLREDUCE, 1, [&] {
-                return residual_add_launch(ctx->x, ctx->part, ctx->xb, ctx->ssq, T, h, ctx->st);
-            }));
+            const bf16* sum = nullptr;
+            RUN(allreduce_bf16(ctx, ctx->part, size_t(T) * h, &sum));
+            RUN(launch(ctx, SS_K_ALLREDUCE, 1,
+                       [&] { return residual_add_launch(ctx->x, sum, ctx->xb, ctx->ssq, T, h, ctx->st); }));
         }
     }
     if (b->n_out > 0) {
@@ -592,12 +671,7 @@ ss_status enqueue_forward(ss_ctx* ctx, const ss_batch* b) {
                  EPI_F32));
         const float* full = ctx->logits_l;
         if (ctx->tp > 1) {
-            RUN(launch(ctx, SS_K_ALLREDUCE, 1, [&]() -> cudaError_t {
-                return g_nccl.all_gather(ctx->logits_l, ctx->logits_g, size_t(b->n_out) * ctx->vocab_l, ncclFloat32,
-                                         ctx->comm, ctx->st) == ncclSuccess
-                           ? cudaSuccess
-                           : cudaErrorUnknown;
-            }));
+            RUN(allgather_logits(ctx, b->n_out));
             RUN(launch(ctx, SS_K_ARGMAX, 1, [&] {
                 return gather_vocab_launch(ctx->logits_g, ctx->logits, ctx->tp, b->n_out, ctx->vocab_l, ctx->st);
             }));
@@ -655,8 +729,15 @@ SS_API ss_status ss_nccl_unique_id(void* out) {
     return SS_OK;
 }
 
-SS_API ss_status ss_create(const ss_model_cfg* cfg, int32_t tp_rank, int32_t tp_size, const void* nccl_id,
-                           uint64_t weight_seed, int32_t device, ss_ctx** out) {
+static void group_release(LocalGroup* g) {
+    if (--g->live == 0) {
+        if (g->st) cudaStreamDestroy(g->st);
+        delete g;
+    }
+}
+
+static ss_status create_impl(const ss_model_cfg* cfg, int32_t tp_rank, int32_t tp_size, const void* nccl_id,
+                             uint64_t weight_seed, int32_t device, LocalGroup* grp, ss_ctx** out) {
     ss_ctx* ctx = nullptr;
     if (!cfg || !out) return fail(ctx, SS_INVALID_ARG, "null argument");
     const ss_model_cfg& c = *cfg;
@@ -690,6 +771,7 @@ SS_API ss_status ss_create(const ss_model_cfg* cfg, int32_t tp_rank, int32_t tp_
     ctx->ffn_l = c.ffn / tp_size;
     ctx->vocab_l = c.vocab / tp_size;
     ctx->seed = weight_seed;
+    ctx->grp = grp;
     if (const char* f = getenv("SS_ATTN_SPLIT")) ctx->decode_split = std::max(64, atoi(f) / 64 * 64);  // dev tuning
     if (const char* f = getenv("SS_ATTN_FUSED_COMBINE")) ctx->fused_combine = atoi(f);
     if (const char* f = getenv("SS_FUSE_ROPE")) ctx->fuse_rope = atoi(f);
@@ -707,7 +789,8 @@ SS_API ss_status ss_create(const ss_model_cfg* cfg, int32_t tp_rank, int32_t tp_
         return s;
     };
     if (cudaSetDevice(device) != cudaSuccess) return bail(fail(ctx, SS_CUDA_ERROR, "cudaSetDevice"));
-    if (cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking) != cudaSuccess)
+    if (grp) ctx->st = grp->st;
+    else if (cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking) != cudaSuccess)
         return bail(fail(ctx, SS_CUDA_ERROR, "stream create"));
     cudaEventCreate(&ctx->ev0);
     cudaEventCreate(&ctx->ev1);
@@ -772,7 +855,7 @@ SS_API ss_status ss_create(const ss_model_cfg* cfg, int32_t tp_rank, int32_t tp_
             return bail(fail(ctx, SS_OUT_OF_MEMORY, "rope table"));
         cudaMemcpy(ctx->rope, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice);
     }
-    if (tp_size > 1) {
+    if (tp_size > 1 && !grp) {
         std::string why;
         if (!nccl_id) return bail(fail(ctx, SS_INVALID_ARG, "tp_size > 1 needs an NCCL unique id"));
         if (!g_nccl.load(why)) return bail(fail(ctx, SS_NCCL_ERROR, why));
@@ -784,6 +867,75 @@ SS_API ss_status ss_create(const ss_model_cfg* cfg, int32_t tp_rank, int32_t tp_
     if (cudaStreamSynchronize(ctx->st) != cudaSuccess)
         return bail(fail(ctx, SS_CUDA_ERROR, std::string("init: ") + cudaGetErrorString(cudaGetLastError())));
     *out = ctx;
+    return SS_OK;
+}
+
+SS_API ss_status ss_create(const ss_model_cfg* cfg, int32_t tp_rank, int32_t tp_size, const void* nccl_id,
+                           uint64_t weight_seed, int32_t device, ss_ctx** out) {
+    return create_impl(cfg, tp_rank, tp_size, nccl_id, weight_seed, device, nullptr, out);
+}
+
+SS_API ss_status ss_create_local_group(const ss_model_cfg* cfg, int32_t tp_size, uint64_t weight_seed,
+                                       int32_t device, ss_ctx** out) {
+    ss_ctx* ctx = nullptr;
+    if (!cfg || !out || tp_size < 1 || tp_size > 8) return fail(ctx, SS_INVALID_ARG, "local group needs 1..8 ranks");
+    LocalGroup* g = new LocalGroup();
+    g->n = tp_size;
+    g->live = 1;  // the creator's hold
+    if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreateWithFlags(&g->st, cudaStreamNonBlocking) != cudaSuccess) {
+        group_release(g);
+        return fail(ctx, SS_CUDA_ERROR, "local group stream");
+    }
+    for (int r = 0; r < tp_size; ++r) {
+        ++g->live;
+        ss_ctx* c = nullptr;
+        if (ss_status s = create_impl(cfg, r, tp_size, nullptr, weight_seed, device, g, &c)) {
+            const std::string m = g_create_err;
+            for (ss_ctx* done : g->ranks) ss_destroy(done);
+            group_release(g);
+            g_create_err = m;
+            return s;
+        }
+        g->ranks.push_back(c);
+        out[r] = c;
+    }
+    group_release(g);
+    return SS_OK;
+}
+
+SS_API ss_status ss_forward_local_group(ss_ctx* const* ranks, int32_t n, const ss_batch_desc* desc, float* logits,
+                                        int32_t* next, float* elapsed_ms) {
+    ss_ctx* ctx = (ranks && n > 0) ? ranks[0] : nullptr;
+    if (!ctx || !ctx->grp || n != ctx->grp->n) return fail(ctx, SS_INVALID_ARG, "not the full local TP group");
+    LocalGroup* g = ctx->grp;
+    for (int r = 0; r < n; ++r)
+        if (!ranks[r] || ranks[r] != g->ranks[size_t(r)]) return fail(ctx, SS_INVALID_ARG, "ranks out of order");
+    g->reset();
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaEventRecord(ctx->ev0, g->st));
+    std::vector<ss_status> st(size_t(n), SS_OK);
+    auto body = [&](int r) {
+        ss_ctx* c = ranks[r];
+        cudaSetDevice(c->device);
+        ss_status s = upload(c, desc, &c->scratch);
+        if (s == SS_OK) s = enqueue_forward(c, &c->scratch);
+        if (s != SS_OK) g->abort();
+        st[size_t(r)] = s;
+    };
+    std::vector<std::thread> th;
+    for (int r = 1; r < n; ++r) th.emplace_back(body, r);
+    body(0);
+    for (std::thread& t : th) t.join();
+    for (int r = 0; r < n; ++r)
+        if (st[size_t(r)] != SS_OK) {
+            if (r != 0) ctx->err = "rank " + std::to_string(r) + ": " + ranks[r]->err;
+            cudaStreamSynchronize(g->st);
+            return st[size_t(r)];
+        }
+    CK(cudaEventRecord(ctx->ev1, g->st));
+    if (ss_status s = read_outputs(ctx, &ctx->scratch, logits, next)) return s;
+    CK(cudaEventSynchronize(ctx->ev1));
+    if (elapsed_ms) CK(cudaEventElapsedTime(elapsed_ms, ctx->ev0, ctx->ev1));
     return SS_OK;
 }
 
@@ -809,7 +961,14 @@ SS_API void ss_destroy(ss_ctx* ctx) {
     for (cudaEvent_t e : ctx->free_ev) cudaEventDestroy(e);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
-    if (ctx->st) cudaStreamDestroy(ctx->st);
+    cudaFree(ctx->part_red);
+    if (ctx->grp) {
+        for (ss_ctx*& r : ctx->grp->ranks)
+            if (r == ctx) r = nullptr;
+        group_release(ctx->grp);
+    } else if (ctx->st) {
+        cudaStreamDestroy(ctx->st);
+    }
     delete ctx;
 }
 

@@ -198,6 +198,29 @@ __global__ void gather_vocab_kernel(const float* __restrict__ in, float* __restr
     }
 }
 
+// One-shot all-reduce over peer buffers: out = sum_r src[r], fp32 accumulation in
+// rank order, 8 bf16 per thread per step. The sources are device pointers the
+// caller can dereference (ranks of a local group on one device; the same kernel
+// reads NVLink peer memory when handed IPC-mapped pointers).
+__global__ void peer_sum_kernel(__nv_bfloat16* __restrict__ out, const PeerBufs src, int n_src, int64_t n8) {
+    pdl_launch_dependents();
+    pdl_wait();
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n8; i += int64_t(gridDim.x) * blockDim.x) {
+        float acc[8] = {};
+        for (int r = 0; r < n_src; ++r) {
+            const uint4 v = reinterpret_cast<const uint4*>(src.p[r])[i];
+            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                acc[2 * j] += bf16_lo(w[j]);
+                acc[2 * j + 1] += bf16_hi(w[j]);
+            }
+        }
+        reinterpret_cast<uint4*>(out)[i] = make_uint4(pack_bf16(acc[0], acc[1]), pack_bf16(acc[2], acc[3]),
+                                                      pack_bf16(acc[4], acc[5]), pack_bf16(acc[6], acc[7]));
+    }
+}
+
 // Element (i, j) of this rank's shard -> (tag, global row, global col, scale).
 __global__ void init_weight_kernel(__nv_bfloat16* __restrict__ w, const WeightInit wi) {
     const int64_t n = wi.rows * wi.cols;
@@ -321,6 +344,12 @@ cudaError_t gather_vocab_launch(const float* in, float* out, int tp, int rows, i
     const int64_t n = int64_t(tp) * rows * vl;
     return n > 0 ? launch_pdl(gather_vocab_kernel, dim3(grid_for(n, 256)), dim3(256), 0, st, 1, in, out, tp, rows, vl)
                  : cudaSuccess;
+}
+
+cudaError_t peer_sum_launch(__nv_bfloat16* out, const PeerBufs& src, int n_src, int64_t n, cudaStream_t st) {
+    const int64_t n8 = n / 8;
+    return n8 > 0 ? launch_pdl(peer_sum_kernel, dim3(grid_for(n8, 256)), dim3(256), 0, st, 1, out, src, n_src, n8)
+                  : cudaSuccess;
 }
 
 cudaError_t init_weight_launch(__nv_bfloat16* w, const WeightInit& wi, cudaStream_t st) {

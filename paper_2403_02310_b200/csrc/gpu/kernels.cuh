@@ -136,6 +136,11 @@ cudaError_t residual_add_launch(float* x, const __nv_bfloat16* part, __nv_bfloat
                                 cudaStream_t st);
 cudaError_t argmax_launch(const float* logits, int rows, int V, int ld, int32_t* out, cudaStream_t st);
 // logits gathered [tp][rows][V_l] -> [rows][tp * V_l]
+struct PeerBufs {
+    const __nv_bfloat16* p[8];
+};
+// out = sum of n_src (<= 8) bf16 buffers of n elements (n % 8 == 0).
+cudaError_t peer_sum_launch(__nv_bfloat16* out, const PeerBufs& src, int n_src, int64_t n, cudaStream_t st);
 cudaError_t gather_vocab_launch(const float* in, float* out, int tp, int rows, int vl, cudaStream_t st);
 
 // Synthetic initialisers (ss_synth.h).

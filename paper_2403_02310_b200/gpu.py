@@ -110,6 +110,14 @@ class HybridForward:
         self._h = h
         self.kv_blocks = 0
 
+    @classmethod
+    def _adopt(cls, shape: ModelShape, handle: int, tp_rank: int, tp_size: int) -> "HybridForward":
+        self = cls.__new__(cls)
+        self.shape, self.tp_rank, self.tp_size = shape, tp_rank, tp_size
+        self._h = C.c_void_p(handle)
+        self.kv_blocks = 0
+        return self
+
     @property
     def handle(self):
         return self._h
@@ -244,3 +252,40 @@ class HybridForward:
     def k_attention(self, batch: Batch, q, o, layer: int):
         self._fence()
         self._check(gpu_lib().ss_k_attention(self._h, batch.handle, q.data_ptr(), o.data_ptr(), layer))
+
+
+class LocalTPGroup:
+    """tp rank contexts on ONE device (ss_create_local_group): the sharded forward
+    of a tp-GPU job with NCCL replaced by barriers + peer-sum kernels, so tensor
+    parallelism can be checked against the oracle where one GPU is visible."""
+
+    def __init__(self, shape: ModelShape, tp_size: int, weight_seed: int = 1234, device: int = 0):
+        self.shape, self.tp_size = shape, tp_size
+        hs = (C.c_void_p * tp_size)()
+        st = gpu_lib().ss_create_local_group(C.byref(shape.c()), tp_size, weight_seed, device, hs)
+        if st:
+            _lib.raise_for(st, gpu_lib().ss_last_error(None).decode())
+        self._hs = hs
+        self.ranks = [HybridForward._adopt(shape, hs[r], r, tp_size) for r in range(tp_size)]
+
+    def kv_alloc(self, num_blocks: int, block_size: int = 16):
+        for r in self.ranks:
+            r.kv_alloc(num_blocks, block_size)
+
+    def fill_descriptor_prefixes(self, desc, seed: int):
+        for r in self.ranks:
+            r.fill_descriptor_prefixes(desc, seed)
+
+    def forward(self, desc, logits: bool = True) -> Tuple[Optional[np.ndarray], np.ndarray, float]:
+        v = desc.view if hasattr(desc, "view") else desc
+        lg = np.empty((v.n_out, self.shape.vocab), np.float32) if logits else None
+        nt = np.empty(v.n_out, np.int32)
+        ms = C.c_float()
+        st = gpu_lib().ss_forward_local_group(self._hs, self.tp_size, C.byref(v), lg.ctypes.data if logits else None,
+                                              nt.ctypes.data, C.byref(ms))
+        self.ranks[0]._check(st)
+        return lg, nt, ms.value
+
+    def close(self):
+        for r in self.ranks:
+            r.close()
