@@ -18,7 +18,7 @@ pytest.importorskip("torch")
 from paper_2403_02310_b200 import gpu, host  # noqa: E402
 
 orc_mod = pytest.importorskip("oracle.forward")
-from tests.test_gpu_forward import compare  # noqa: E402
+from test_gpu_forward import compare  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 
