@@ -239,6 +239,12 @@ def run_ours(args):
         roof = {"bound": "tensor", "achieved": kernels[dom]["tflops"], "peak": peaks["bf16_tflops_sustained"],
                 "unit": "TFLOP/s"}
     roof["frac"] = roof["achieved"] / roof["peak"]
+    if roof["unit"] == "TFLOP/s":
+        # The sustained figure is cuBLAS 8192^3 back to back for 4 s (power-capped);
+        # a GEMM interleaved with HBM-bound attention runs at higher clocks, so
+        # frac can exceed 1 — the burst figure bounds it.
+        roof["peak_burst"] = peaks["bf16_tflops"]
+        roof["frac_of_burst"] = roof["achieved"] / peaks["bf16_tflops"]
     roof["traffic"] = traffic
     roof["kernel"] = dom
     roof["peak_source"] = f"{peak_src} ({'sustained' if roof['unit'] == 'TFLOP/s' else 'copy'})"
