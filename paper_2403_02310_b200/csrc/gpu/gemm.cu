@@ -69,6 +69,11 @@ __device__ __forceinline__ uint32_t peer_addr(const void* p, uint32_t rank) {
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
+// Relaxed arrive: orders nothing but the (tcgen05-fenced) TMEM reads, so the
+// epilogue's global stores need not drain before the accumulator is handed back.
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
 // 2-SM TMA: data lands in this CTA, completion is signalled on the leader's mbarrier.
 __device__ __forceinline__ void tma_load_2d_cg2(void* smem_dst, const CUtensorMap* m, int32_t c0, int32_t c1,
                                                 uint32_t bar_cluster) {
@@ -199,6 +204,30 @@ struct SegIter {
     }
 };
 
+#ifdef SS_GEMM_TRACE
+// Dev-only timeline (build with -DSS_GEMM_TRACE): per CTA, globaltimer ns at
+// entry, after pdl_wait, first full stage, last MMA of the first segment,
+// accumulator seen by the epilogue, first segment stored, exit.
+__device__ unsigned long long g_gemm_trace[1024][8];
+__device__ __forceinline__ void trace(int i) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (blockIdx.x < 1024) g_gemm_trace[blockIdx.x][i] = t;
+}
+__device__ unsigned long long g_gemm_trace2[1024][4];
+__device__ __forceinline__ void trace2(int i) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (blockIdx.x < 1024) g_gemm_trace2[blockIdx.x][i] = t;
+}
+#define TRACE(i) trace(i)
+#define TRACE2(i) \
+    if (warp == 2 && lane == 0) trace2(i)
+#else
+#define TRACE(i)
+#define TRACE2(i)
+#endif
+
 template <int EPI>
 __device__ __forceinline__ void epi_store(const uint32_t (&v)[32], int row, int col, void* out, int ldo,
                                           const EpiArgs& ea) {
@@ -242,11 +271,68 @@ __device__ __forceinline__ void epi_store(const uint32_t (&v)[32], int row, int 
     }
 }
 
-__device__ __forceinline__ void add_partial(uint32_t (&v)[32], const float* p) {
+// ---- staged split-K fixup (last segment of a group: the smem ring is idle)
+// Partial layout per (group, CTA rank): [chunk c][row 0..127][32 fp32], a warp's
+// 32 rows of one chunk = 4 KB contiguous, float4 j of row r at slot j ^ (r & 7)
+// (conflict-free smem reads for the 8 lanes of a quarter-warp).
+__device__ __forceinline__ void bulk_store_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit_wait_all() {
+    asm volatile("cp.async.bulk.commit_group;\n\tcp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+__device__ __forceinline__ void named_bar(int id, int threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+        "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+        "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+        : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// p = this thread's 32-float row slice of one chunk in the partial layout above
+// EPI_RESADD with the residual already in registers (x_in = the row's 32 floats at col)
+__device__ __forceinline__ void epi_resadd(const uint32_t (&v)[32], int row, int col, void* out, int ldo,
+                                           const EpiArgs& ea, const float4 (&x_in)[8]) {
+    float4* o = reinterpret_cast<float4*>(static_cast<float*>(out) + size_t(row) * ldo + col);
+    float ss = 0.f;
+    uint32_t pk[16];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        float4 x = x_in[j];
+        x.x += __uint_as_float(v[4 * j + 0]);
+        x.y += __uint_as_float(v[4 * j + 1]);
+        x.z += __uint_as_float(v[4 * j + 2]);
+        x.w += __uint_as_float(v[4 * j + 3]);
+        o[j] = x;
+        ss += x.x * x.x + x.y * x.y + x.z * x.z + x.w * x.w;
+        pk[2 * j] = pack_bf16(x.x, x.y);
+        pk[2 * j + 1] = pack_bf16(x.z, x.w);
+    }
+    if (ea.xb_out) {
+        uint4* xb = reinterpret_cast<uint4*>(ea.xb_out + size_t(row) * ldo + col);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) xb[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+        ea.ssq_out[size_t(row) * (ldo / 32) + col / 32] = ss;
+    }
+}
+
+__device__ __forceinline__ void add_partial(uint32_t (&v)[32], const float* p, int lane) {
     const float4* q = reinterpret_cast<const float4*>(p);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-        const float4 a = q[j];
+        const float4 a = q[j ^ (lane & 7)];
         v[4 * j + 0] = __float_as_uint(__uint_as_float(v[4 * j + 0]) + a.x);
         v[4 * j + 1] = __float_as_uint(__uint_as_float(v[4 * j + 1]) + a.y);
         v[4 * j + 2] = __float_as_uint(__uint_as_float(v[4 * j + 2]) + a.z);
@@ -271,7 +357,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* ebar = tempty + 2;  // one per epilogue warp (staged fixup loads)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ebar + 8);
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
@@ -281,6 +368,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int gid = blockIdx.x / CG, G = gridDim.x / CG;
     const long total = long(num_tiles) * num_kb;
     const SkRange rg = sk_range(gid, G, total);
+    if (threadIdx.x == 0) TRACE(0);
 
     if (threadIdx.x == 0) {
         tma_prefetch(&tmA);
@@ -293,6 +381,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&tfull[a], 1);
             mbar_init(&tempty[a], 8 * CG);  // every epilogue warp of the group
         }
+        for (int a = 0; a < 8; ++a) mbar_init(&ebar[a], 1);
         mbar_fence_init();
     }
     if (warp == 1) tmem_alloc_cg<CG>(tmem_slot, Cfg::TMEM_COLS);
@@ -303,6 +392,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tmem_base = *tmem_slot;
     pdl_launch_dependents();
     pdl_wait();  // A (activations) and the residual come from the preceding kernels
+    if (threadIdx.x == 0) TRACE(1);
 
     if (warp == 0) {
         if (lane == 0) {  // ---------------- TMA producer (both CTAs)
@@ -316,6 +406,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int n0 = (t / num_mt) * BN + Cfg::B_ROWS * int(rank);
                 for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&empty[s], ph ^ 1);
+#if defined(SS_GEMM_EXP) && SS_GEMM_EXP == 1  // dev experiment: no loads (MMA on stale smem)
+                    if (leader) mbar_arrive(&full[s]);
+                    if (false)
+#endif
                     if constexpr (CG == 1) {
                         mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
                         tma_load_2d(sA + s * Cfg::A_BYTES, &tmA, kb * BK, m0, &full[s]);
@@ -341,20 +435,30 @@ __global__ void __launch_bounds__(kThreads, 1)
             int acc = 0;
             uint32_t acc_ph = 0;
             SegIter sit(sk_mode, gid, G, num_kb, num_tiles, rg, sk_slices);
+#ifdef SS_GEMM_TRACE
+            int seg_no = 0;
+#endif
             for (Seg sg; sit.next(sg);) {
                 const int kb0 = sg.kb0, kb1 = sg.kb1;
                 mbar_wait(&tempty[acc], acc_ph ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + uint32_t(acc * BN);
-                for (int kb = kb0; kb < kb1; ++kb) {
+                const int nk = kb1 - kb0;
+                for (int i = 0; i < nk; ++i) {
                     mbar_wait(&full[s], ph);
                     tc_fence_after();
+#ifdef SS_GEMM_TRACE
+                    if (i == 0 && seg_no == 0) TRACE(2);
+#endif
                     const uint32_t a_addr = smem_u32(sA + s * Cfg::A_BYTES);
                     const uint32_t b_addr = smem_u32(sB + s * Cfg::B_BYTES);
+#if defined(SS_GEMM_EXP) && SS_GEMM_EXP == 2  // dev experiment: loads only, no MMA
+                    if (false)
+#endif
 #pragma unroll
                     for (int k = 0; k < BK / 16; ++k)
                         mma_cg<CG>(d_tmem, umma_desc_sw128(a_addr + 32 * k), umma_desc_sw128(b_addr + 32 * k), idesc,
-                                   (kb > kb0 || k > 0) ? 1u : 0u);
+                                   (i > 0 || k > 0) ? 1u : 0u);
                     commit_cg<CG>(&empty[s]);  // smem slot free (in both CTAs) once these MMAs retire
                     if (++s == STAGES) {
                         s = 0;
@@ -362,6 +466,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
                 commit_cg<CG>(&tfull[acc]);  // accumulator ready for both CTAs' epilogues
+#ifdef SS_GEMM_TRACE
+                if (seg_no < 4) TRACE(3 + seg_no);
+                ++seg_no;
+#endif
                 if (++acc == 2) {
                     acc = 0;
                     acc_ph ^= 1;
@@ -376,7 +484,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t tempty_leader = CG == 2 ? peer_addr(tempty, 0) : 0;
         const int rloc = 128 * int(rank) + q * 32 + lane;  // row within the group's tile
         int acc = 0;
-        uint32_t acc_ph = 0;
+        uint32_t acc_ph = 0, eph = 0;
         SegIter sit(sk_mode, gid, G, num_kb, num_tiles, rg, sk_slices);
         for (Seg sg; sit.next(sg);) {
             const int t = sg.t, kb0 = sg.kb0, kb1 = sg.kb1;
@@ -399,26 +507,77 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 rs = rsqrtf(((a0 + a1) + (a2 + a3)) * ea.inv_dim + ea.eps);
             }
+            // residual rows of this warp's first two chunks, loaded while the MMAs run
+            float4 xin[2][8];
+            if constexpr (EPI == EPI_RESADD) {
+                if (kb0 == 0 && row < M) {
+#pragma unroll
+                    for (int i = 0; i < 2; ++i) {
+                        const int col = n0 + (half + 2 * i) * 32;
+                        if (half + 2 * i < BN / 32 && col < N) {
+                            const float4* src = reinterpret_cast<const float4*>(static_cast<const float*>(out) +
+                                                                                size_t(row) * ldo + col);
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) xin[i][j] = src[j];
+                        }
+                    }
+                }
+            }
             mbar_wait(&tfull[acc], acc_ph);
             tc_fence_after();
+            TRACE2(0);
             const uint32_t t_row = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN);
-            if (kb0 > 0) {
+            SegIter peek = sit;
+            Seg nx;
+            const bool last_seg = !peek.next(nx);
+            constexpr int kStg = ((BN / 32 + 1) / 2) * 1024;  // staging floats per epilogue warp
+            float* stg = reinterpret_cast<float*>(smem) + ew * kStg;
+            if (kb0 > 0 && last_seg) {
+                // non-head piece, ring idle: TMEM -> swizzled smem -> one 4 KB bulk store per chunk
+                int i = 0;
+#pragma unroll 1
+                for (int c = half; c < BN / 32; c += 2, ++i) {
+                    uint32_t v[32];
+                    tmem_ld32(t_row + uint32_t(c * 32), v);
+                    tmem_wait_ld();
+                    float4* s4 = reinterpret_cast<float4*>(stg + i * 1024 + lane * 32);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        s4[j ^ (lane & 7)] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                                         __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+                }
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    float* base = part + (size_t(gid) * CG + rank) * (128 * BN);
+                    i = 0;
+                    for (int c = half; c < BN / 32; c += 2, ++i)
+                        bulk_store_s2g(base + (size_t(c) * 128 + q * 32) * 32, stg + i * 1024, 4096);
+                    bulk_commit_wait_all();
+                    fence_proxy_async_global();
+                    __threadfence();
+                    st_release_gpu(&flags[(size_t(gid) * 2 + rank) * 8 + ew], epoch);
+                }
+                __syncwarp();
+                TRACE2(3);
+            } else if (kb0 > 0) {
                 // non-head piece of a split tile: publish the partial accumulator
-                float* dst = part + (size_t(gid) * Cfg::TILE_M + rloc) * BN;
+                float* dst = part + (size_t(gid) * CG + rank) * (128 * BN) + (q * 32 + lane) * 32;
 #pragma unroll 1
                 for (int c = half; c < BN / 32; c += 2) {
                     uint32_t v[32];
                     tmem_ld32(t_row + uint32_t(c * 32), v);
                     tmem_wait_ld();
-                    float4* d4 = reinterpret_cast<float4*>(dst + c * 32);
+                    float4* d4 = reinterpret_cast<float4*>(dst + size_t(c) * 128 * 32);
 #pragma unroll
                     for (int j = 0; j < 8; ++j)
-                        d4[j] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                        d4[j ^ (lane & 7)] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
                                             __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
                 }
                 __threadfence();
                 __syncwarp();
                 if (lane == 0) st_release_gpu(&flags[(size_t(gid) * 2 + rank) * 8 + ew], epoch);
+                TRACE2(3);
             } else {
                 // head or whole tile: add the other groups' pieces in group order
                 const long tile_end = long(t + 1) * num_kb;
@@ -433,6 +592,48 @@ __global__ void __launch_bounds__(kThreads, 1)
                     uint32_t spins = 0;
                     while (ld_acquire_gpu(f) != epoch)
                         if (++spins == (1u << 28)) __trap();
+                }
+                TRACE2(1);
+                if (g_last > gid && last_seg) {
+                    // ring idle: bulk-load each piece's chunks (fixed group order) and
+                    // accumulate into TMEM; the epilogue below then reads final sums
+                    const int nmine = (BN / 32 - half + 1) / 2;
+                    for (int g = gid + 1; g <= g_last; ++g) {
+                        if (lane == 0) {
+                            fence_proxy_async_global();
+                            const float* base = part + (size_t(g) * CG + rank) * (128 * BN);
+                            mbar_arrive_expect_tx(&ebar[ew], uint32_t(nmine) * 4096u);
+                            int i = 0;
+                            for (int c = half; c < BN / 32; c += 2, ++i)
+                                bulk_load(stg + i * 1024, base + (size_t(c) * 128 + q * 32) * 32, 4096, &ebar[ew]);
+                        }
+                        mbar_wait(&ebar[ew], eph);
+                        eph ^= 1;
+                        int i = 0;
+#pragma unroll 1
+                        for (int c = half; c < BN / 32; c += 2, ++i) {
+                            uint32_t v[32];
+                            tmem_ld32(t_row + uint32_t(c * 32), v);
+                            tmem_wait_ld();
+                            const float4* s4 = reinterpret_cast<const float4*>(stg + i * 1024 + lane * 32);
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) {
+                                const float4 a = s4[j ^ (lane & 7)];
+                                v[4 * j + 0] = __float_as_uint(__uint_as_float(v[4 * j + 0]) + a.x);
+                                v[4 * j + 1] = __float_as_uint(__uint_as_float(v[4 * j + 1]) + a.y);
+                                v[4 * j + 2] = __float_as_uint(__uint_as_float(v[4 * j + 2]) + a.z);
+                                v[4 * j + 3] = __float_as_uint(__uint_as_float(v[4 * j + 3]) + a.w);
+                            }
+                            tmem_st32(t_row + uint32_t(c * 32), v);
+                        }
+                        tmem_wait_st();
+                        __syncwarp();  // every lane done with stg before the next piece lands
+                    }
+                    // the two warps of this TMEM quarter swap chunk sets in the epilogue
+                    tc_fence_before();
+                    named_bar(1 + q, 64);
+                    tc_fence_after();
+                    g_last = gid;
                 }
                 if constexpr (EPI == EPI_QKV) {
                     // chunk pairs (c, c + ps) hold the rotate-half partners i, i + hd/2 of one head
@@ -449,9 +650,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                         tmem_ld32(t_row + uint32_t((c + ps) * 32), x2);
                         tmem_wait_ld();
                         for (int g = gid + 1; g <= g_last; ++g) {
-                            const float* src = part + (size_t(g) * Cfg::TILE_M + rloc) * BN;
-                            add_partial(x1, src + c * 32);
-                            add_partial(x2, src + (c + ps) * 32);
+                            const float* src = part + (size_t(g) * CG + rank) * (128 * BN) + (q * 32 + lane) * 32;
+                            add_partial(x1, src + size_t(c) * 4096, lane);
+                            add_partial(x2, src + size_t(c + ps) * 4096, lane);
                         }
                         const int col = n0 + c * 32;
                         if (!row_ok || col >= N) continue;
@@ -494,9 +695,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                         tmem_ld32(t_row + uint32_t((c + 1) * 32), ut);
                         tmem_wait_ld();
                         for (int g = gid + 1; g <= g_last; ++g) {
-                            const float* src = part + (size_t(g) * Cfg::TILE_M + rloc) * BN;
-                            add_partial(gt, src + c * 32);
-                            add_partial(ut, src + (c + 1) * 32);
+                            const float* src = part + (size_t(g) * CG + rank) * (128 * BN) + (q * 32 + lane) * 32;
+                            add_partial(gt, src + size_t(c) * 4096, lane);
+                            add_partial(ut, src + size_t(c + 1) * 4096, lane);
                         }
                         const int col = n0 + c * 32;
                         if (row < M && col < N) {
@@ -514,28 +715,36 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                     }
                 } else {
-#pragma unroll 1
-                    for (int c = half; c < BN / 32; c += 2) {
+#pragma unroll
+                    for (int i = 0; i < (BN / 32 + 1) / 2; ++i) {  // unrolled: xin stays in registers
+                        const int c = half + 2 * i;
+                        if (c >= BN / 32) break;
                         uint32_t v[32];
                         tmem_ld32(t_row + uint32_t(c * 32), v);
                         tmem_wait_ld();
                         for (int g = gid + 1; g <= g_last; ++g)
-                            add_partial(v, part + (size_t(g) * Cfg::TILE_M + rloc) * BN + c * 32);
+                            add_partial(v, part + (size_t(g) * CG + rank) * (128 * BN) + size_t(c) * 4096 + (q * 32 + lane) * 32, lane);
                         if (ea.ssq_in) {
 #pragma unroll
                             for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) * rs);
                         }
                         const int col = n0 + c * 32;
-                        if (row < M && col < N) epi_store<EPI>(v, row, col, out, ldo, ea);
+                        if (row < M && col < N) {
+                            if constexpr (EPI == EPI_RESADD) {
+                                if (i < 2) {
+                                    epi_resadd(v, row, col, out, ldo, ea, xin[i < 2 ? i : 0]);
+                                    continue;
+                                }
+                            }
+                            epi_store<EPI>(v, row, col, out, ldo, ea);
+                        }
                     }
                 }
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) {
-                if constexpr (CG == 1) mbar_arrive(&tempty[acc]);
-                else mbar_arrive_cluster(tempty_leader + uint32_t(acc * 8));
-            }
+            TRACE2(2);
+            if (lane == 0) mbar_arrive_cluster_relaxed(CG == 1 ? smem_u32(&tempty[acc]) : tempty_leader + uint32_t(acc * 8));
             if (++acc == 2) {
                 acc = 0;
                 acc_ph ^= 1;
@@ -549,6 +758,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         tmem_dealloc_cg<CG>(tmem_base, Cfg::TMEM_COLS);
     }
+    if (threadIdx.x == 0) TRACE(7);
 }
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -734,3 +944,18 @@ cudaError_t gemm_launch(const GemmPlan& p, cudaStream_t st) {
 }
 
 }  // namespace ssk
+
+#ifdef SS_GEMM_TRACE
+extern "C" __attribute__((visibility("default"))) int ss_debug_gemm_trace(unsigned long long* out, int n) {
+    if (cudaDeviceSynchronize() != cudaSuccess) return -1;
+    if (n > 1024) {  // second table: epilogue-warp stamps of the last segment
+        return cudaMemcpyFromSymbol(out, ssk::g_gemm_trace2, sizeof(unsigned long long) * 4 * 1024) == cudaSuccess
+                   ? 0
+                   : -1;
+    }
+    return cudaMemcpyFromSymbol(out, ssk::g_gemm_trace, sizeof(unsigned long long) * 8 * (n < 1024 ? n : 1024)) ==
+                   cudaSuccess
+               ? 0
+               : -1;
+}
+#endif

@@ -77,6 +77,45 @@ def test_gemm_stream_k_shapes(small, M, N, K):
     torch.testing.assert_close(D, A.float() @ B.float().T, rtol=2e-4, atol=2e-4)
 
 
+@pytest.mark.parametrize("env", [{"SS_GEMM_SK": "1"}, {"SS_GEMM_BN": "256", "SS_GEMM_SPLITS": "2"},
+                                 {"SS_GEMM_SPLITS": "4"}, {"SS_GEMM_BN": "128", "SS_GEMM_SPLITS": "3"}])
+@pytest.mark.parametrize("epi", [0, 1, 2, 3])
+def test_gemm_forced_split_schedules(small, monkeypatch, env, epi):
+    """Every epilogue through the split-K fixups (stream-K; lockstep split of the ragged
+    wave with the staged smem/bulk-copy reduction): values and bitwise repeatability."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    M, N, K = 512, 28672 if epi == 2 else 4096, 4096
+    A = _rand((M, K), 1.0, 11)
+    B = _rand((N, K), 1.0 / math.sqrt(K), 12)
+    ref = A.float() @ B.float().T
+    outs = []
+    for _ in range(2):
+        if epi == 0:
+            D = torch.empty((M, N), dtype=torch.bfloat16, device="cuda")
+        elif epi == 1:
+            D = torch.ones((M, N), device="cuda")
+        elif epi == 2:
+            D = torch.empty((M, N // 2), dtype=torch.bfloat16, device="cuda")
+        else:
+            D = torch.empty((M, N), dtype=torch.float32, device="cuda")
+        small.k_gemm(A, B, D, M, N, K, epi)
+        torch.cuda.synchronize()
+        outs.append(D)
+    assert torch.equal(outs[0], outs[1])
+    D = outs[0]
+    if epi == 0:
+        torch.testing.assert_close(D.float(), ref, rtol=1e-2, atol=1e-2)
+    elif epi == 1:
+        torch.testing.assert_close(D, 1.0 + ref, rtol=1e-4, atol=1e-4)
+    elif epi == 2:
+        r = ref.view(M, N // 64, 2, 32)
+        want = (torch.nn.functional.silu(r[:, :, 0]) * r[:, :, 1]).reshape(M, N // 2)
+        torch.testing.assert_close(D.float(), want, rtol=2e-2, atol=2e-2)
+    else:
+        torch.testing.assert_close(D, ref, rtol=2e-4, atol=2e-4)
+
+
 def test_rmsnorm(small):
     M, h = 77, 4096
     x = torch.randn((M, h), device="cuda") * 3
