@@ -17,6 +17,7 @@
  *   ssh_next_chunk_size   <- get_next_chunk_size           sched.cpp:97-103
  *   ssh_percentile        <- percentile                    metrics.cpp:13-21
  *   ssh_decode_reference_time <- decode_reference_time     costmodel.cpp:83-85
+ *   ssh_calibrate         <- servesim::calibrate           calibrate.cpp:121-193
  *
  * No exceptions cross this boundary: every call returns an ss_status and the
  * message of the last failure is available from ssh_last_error().
@@ -144,6 +145,30 @@ double ssh_iteration_time(const ssh_entry* entries, int32_t n, const ssh_cost_pa
 double ssh_decode_reference_time(const ssh_cost_params* p);
 ss_status ssh_compute_token_budget(double t_max_ms, const ssh_cost_params* p, int32_t pp_degree,
                                    int32_t* out_budget);
+/* servesim::CalibrationAnchor (costmodel.hpp:78-81): a batch + its observed ms. */
+typedef struct {
+    const ssh_entry* entries;
+    int32_t n_entries;
+    double observed_ms;
+} ssh_anchor;
+
+/* servesim::CalibrationOptions (costmodel.hpp:91-95); NULL = the defaults
+ * (tile 256, penalty 0.32, saturation swept over 1..2048). */
+typedef struct {
+    int32_t tile_size;
+    double tile_penalty_frac;
+    int32_t max_saturation_tokens;
+} ssh_calib_opts;
+
+/* servesim::calibrate (calibrate.cpp:121-193): fits the cost-model constants to
+ * observed timings (e.g. B200 forwards of anchor batches). predicted_ms and
+ * relative_error (nullable) receive n values; zeroed_mask (nullable) gets bit t
+ * set for every term pinned to zero, t in order (fixed_overhead, per_token_linear,
+ * attn_prefill_quad, attn_kv_read, attn_decode_per_kv). SS_CALIBRATION carries
+ * the reference's CalibrationError message. */
+ss_status ssh_calibrate(const ssh_anchor* anchors, int32_t n, const ssh_calib_opts* opts,
+                        ssh_cost_params* out, double* predicted_ms, double* relative_error,
+                        double* max_relative_error, int32_t* zeroed_mask);
 int32_t ssh_next_chunk_size(int32_t prompt_tokens, int32_t prefill_done, int32_t token_budget,
                             int32_t packed_tokens, int32_t chunk_align);
 ss_status ssh_percentile(const double* series, int64_t n, double p, double* out);

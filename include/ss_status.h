@@ -6,6 +6,7 @@
  *   SS_INVALID_ARG  -> servesim::ContractViolation (a std::logic_error)
  *   SS_OUT_OF_KV    -> servesim::OutOfKvBlocks
  *   SS_INFEASIBLE   -> servesim::InfeasibleSlo
+ *   SS_CALIBRATION  -> servesim::CalibrationError (costmodel.hpp:74-76)
  * plus device-side failures the reference cannot have (CUDA, NCCL, OOM).
  */
 #ifndef SS_STATUS_H
@@ -23,7 +24,8 @@ typedef enum {
     SS_OUT_OF_MEMORY = 4,
     SS_CUDA_ERROR = 5,
     SS_NCCL_ERROR = 6,
-    SS_INTERNAL = 7
+    SS_INTERNAL = 7,
+    SS_CALIBRATION = 8
 } ss_status;
 
 #ifdef __cplusplus

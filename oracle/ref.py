@@ -46,6 +46,9 @@ def lib():
         L.ref_token_budget.restype = I32
         L.ref_decode_reference_time.argtypes = [C.POINTER(_lib.CostParams)]
         L.ref_decode_reference_time.restype = D
+        L.ref_calibrate.argtypes = [C.POINTER(_lib.AnchorRow), I32, C.POINTER(_lib.CalibOpts), C.POINTER(_lib.CostParams),
+                                    C.POINTER(D), C.POINTER(D), C.POINTER(I32)]
+        L.ref_calibrate.restype = I32
         L.ref_last_error.argtypes = []
         L.ref_last_error.restype = C.c_char_p
         _ref = L
@@ -98,3 +101,13 @@ def token_budget(t_max_ms: float, params: _lib.CostParams, pp: int):
 
 def decode_reference_time(params: _lib.CostParams) -> float:
     return lib().ref_decode_reference_time(C.byref(params))
+
+
+def calibrate(anchor_rows, n: int, opts: _lib.CalibOpts):
+    """The reference's servesim::calibrate on ssh_anchor rows: (status, params, predicted, max_rel, zeroed_mask)."""
+    out = _lib.CostParams()
+    pred = (C.c_double * max(1, n))()
+    mx = C.c_double()
+    mask = C.c_int32()
+    st = lib().ref_calibrate(anchor_rows, n, C.byref(opts), C.byref(out), pred, C.byref(mx), C.byref(mask))
+    return st, out, list(pred[:n]), mx.value, mask.value

@@ -12,6 +12,7 @@
 //   ref_iteration_time  -> servesim::iteration_time (costmodel.cpp:39-56)
 //   ref_token_budget    -> servesim::compute_token_budget (sched.cpp:154-175)
 //   ref_cost_preset     -> servesim::model_preset (presets.cpp:71-77)
+//   ref_calibrate       -> servesim::calibrate (calibrate.cpp:121-193)
 #include <cstring>
 #include <string>
 
@@ -161,6 +162,58 @@ int ref_token_budget(double t_max_ms, const ssh_cost_params* p, int pp, int* out
     try {
         *out = compute_token_budget(t_max_ms, to_params(*p), pp);
         return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return code_of(e);
+    }
+}
+
+// Same argument layout as ssh_calibrate; returns 0, or 8 with the reference's
+// CalibrationError message in ref_last_error().
+int ref_calibrate(const ssh_anchor* anchors, int n, const ssh_calib_opts* opts, ssh_cost_params* out,
+                  double* predicted_ms, double* max_rel, int* zeroed_mask) {
+    try {
+        std::vector<CalibrationAnchor> an;
+        for (int i = 0; i < n; ++i) {
+            Batch b;
+            for (int j = 0; j < anchors[i].n_entries; ++j) {
+                const ssh_entry& e = anchors[i].entries[j];
+                BatchEntry be;
+                be.request_id = e.request_id;
+                be.kind = e.kind ? EntryKind::PrefillChunk : EntryKind::Decode;
+                be.chunk_tokens = e.chunk_tokens;
+                be.prefix_tokens = e.prefix_tokens;
+                b.entries.push_back(be);
+            }
+            an.push_back(CalibrationAnchor{b, anchors[i].observed_ms});
+        }
+        CalibrationOptions o;
+        if (opts) {
+            o.tile_size = opts->tile_size;
+            o.tile_penalty_frac = opts->tile_penalty_frac;
+            o.max_saturation_tokens = opts->max_saturation_tokens;
+        }
+        const CalibrationResult r = calibrate(an, o);
+        const CostModelParams& q = r.params;
+        *out = ssh_cost_params{q.per_token_linear_ms, q.saturation_tokens, q.attn_prefill_quad_ms, q.attn_kv_read_ms,
+                               q.attn_decode_per_kv_ms, q.fixed_overhead_ms, q.tp_comm_ms, q.pp_send_ms,
+                               q.tile_size, q.tile_penalty_frac};
+        for (int i = 0; i < n; ++i)
+            if (predicted_ms) predicted_ms[i] = r.predicted_ms[size_t(i)];
+        if (max_rel) *max_rel = r.max_relative_error;
+        if (zeroed_mask) {
+            static const char* const names[5] = {"fixed_overhead_ms", "per_token_linear_ms", "attn_prefill_quad_ms",
+                                                 "attn_kv_read_ms", "attn_decode_per_kv_ms"};
+            int m = 0;
+            for (const auto& z : r.zeroed_terms)
+                for (int t = 0; t < 5; ++t)
+                    if (z == names[t]) m |= 1 << t;
+            *zeroed_mask = m;
+        }
+        return 0;
+    } catch (const CalibrationError& e) {
+        g_err = e.what();
+        return 8;
     } catch (const std::exception& e) {
         g_err = e.what();
         return code_of(e);

@@ -13,7 +13,8 @@ PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 GPU_SO = os.path.join(PKG_DIR, "libss_gpu.so")
 HOST_SO = os.path.join(PKG_DIR, "libss_host.so")
 
-SS_OK, SS_INVALID_ARG, SS_OUT_OF_KV, SS_INFEASIBLE, SS_OUT_OF_MEMORY, SS_CUDA_ERROR, SS_NCCL_ERROR, SS_INTERNAL = range(8)
+(SS_OK, SS_INVALID_ARG, SS_OUT_OF_KV, SS_INFEASIBLE, SS_OUT_OF_MEMORY, SS_CUDA_ERROR, SS_NCCL_ERROR, SS_INTERNAL,
+ SS_CALIBRATION) = range(9)
 
 
 class SSError(RuntimeError):
@@ -34,10 +35,15 @@ class InfeasibleSlo(SSError):
     """servesim::InfeasibleSlo (reference core.hpp:26-28)."""
 
 
+class CalibrationError(SSError):
+    """servesim::CalibrationError (reference costmodel.hpp:74-76)."""
+
+
 def raise_for(status: int, msg: str) -> None:
     if status == SS_OK:
         return
-    cls = {SS_INVALID_ARG: ContractViolation, SS_OUT_OF_KV: OutOfKvBlocks, SS_INFEASIBLE: InfeasibleSlo}.get(status, SSError)
+    cls = {SS_INVALID_ARG: ContractViolation, SS_OUT_OF_KV: OutOfKvBlocks, SS_INFEASIBLE: InfeasibleSlo,
+           SS_CALIBRATION: CalibrationError}.get(status, SSError)
     raise cls(status, msg)
 
 
@@ -62,12 +68,20 @@ class CostParams(C.Structure):
     ]
 
 
+class CalibOpts(C.Structure):
+    _fields_ = [("tile_size", C.c_int32), ("tile_penalty_frac", C.c_double), ("max_saturation_tokens", C.c_int32)]
+
+
 class TraceRow(C.Structure):
     _fields_ = [("arrival_us", C.c_int64), ("prompt_tokens", C.c_int32), ("output_tokens", C.c_int32)]
 
 
 class EntryRow(C.Structure):
     _fields_ = [("request_id", C.c_int32), ("kind", C.c_int32), ("chunk_tokens", C.c_int32), ("prefix_tokens", C.c_int64)]
+
+
+class AnchorRow(C.Structure):
+    _fields_ = [("entries", C.POINTER(EntryRow)), ("n_entries", C.c_int32), ("observed_ms", C.c_double)]
 
 
 class Latency(C.Structure):
@@ -174,6 +188,8 @@ def host_lib():
         _sig(lib, "ssh_iteration_time", D, [C.POINTER(EntryRow), I32, C.POINTER(CostParams), I32, I32])
         _sig(lib, "ssh_decode_reference_time", D, [C.POINTER(CostParams)])
         _sig(lib, "ssh_compute_token_budget", I32, [D, C.POINTER(CostParams), I32, C.POINTER(I32)])
+        _sig(lib, "ssh_calibrate", I32, [C.POINTER(AnchorRow), I32, C.POINTER(CalibOpts), C.POINTER(CostParams),
+                                         C.POINTER(D), C.POINTER(D), C.POINTER(D), C.POINTER(I32)])
         _sig(lib, "ssh_next_chunk_size", I32, [I32, I32, I32, I32, I32])
         _sig(lib, "ssh_percentile", I32, [C.POINTER(D), I64, D, C.POINTER(D)])
         _sig(lib, "ssh_desc_build", I32, [C.POINTER(EntryRow), I32, P, I32, I32, C.c_uint64, C.POINTER(P)])
@@ -207,7 +223,7 @@ HOST_EXPORTS = [
     "ssh_replica_default", "ssh_cost_preset", "ssh_make_trace", "ssh_make_trace_spec", "ssh_simulate",
     "ssh_report_event_log", "ssh_report_summary", "ssh_report_num_microbatches", "ssh_report_microbatch",
     "ssh_report_peak_blocks", "ssh_report_free", "ssh_iteration_time", "ssh_decode_reference_time",
-    "ssh_compute_token_budget", "ssh_next_chunk_size", "ssh_percentile", "ssh_desc_build", "ssh_desc_canonical",
+    "ssh_compute_token_budget", "ssh_calibrate", "ssh_next_chunk_size", "ssh_percentile", "ssh_desc_build", "ssh_desc_canonical",
     "ssh_desc_view", "ssh_desc_pool_blocks", "ssh_desc_free", "ssh_session_create", "ssh_session_step",
     "ssh_session_release", "ssh_session_peak_blocks", "ssh_session_free", "ssh_last_error",
 ]

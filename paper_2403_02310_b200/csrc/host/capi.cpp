@@ -5,6 +5,7 @@
 #include <string>
 
 #include "../../../include/ss_host.h"
+#include "calibrate.hpp"
 #include "costmodel.hpp"
 #include "descriptor.hpp"
 #include "engine.hpp"
@@ -46,6 +47,9 @@ ss_status guarded(F&& f) {
     } catch (const ss::InfeasibleSlo& e) {
         g_err = e.what();
         return SS_INFEASIBLE;
+    } catch (const ss::CalibrationError& e) {
+        g_err = e.what();
+        return SS_CALIBRATION;
     } catch (const ss::ContractViolation& e) {
         g_err = e.what();
         return SS_INVALID_ARG;
@@ -275,6 +279,52 @@ double ssh_iteration_time(const ssh_entry* entries, int32_t n, const ssh_cost_pa
 }
 
 double ssh_decode_reference_time(const ssh_cost_params* p) { return ss::decode_reference_time(to_params(*p)); }
+
+ss_status ssh_calibrate(const ssh_anchor* anchors, int32_t n, const ssh_calib_opts* opts, ssh_cost_params* out,
+                        double* predicted_ms, double* relative_error, double* max_relative_error,
+                        int32_t* zeroed_mask) {
+    return guarded([&] {
+        if (!out || n < 0 || (n > 0 && !anchors)) throw ss::ContractViolation("null calibration argument");
+        std::vector<ss::Anchor> an;
+        for (int32_t i = 0; i < n; ++i) {
+            if (anchors[i].n_entries > 0 && !anchors[i].entries) throw ss::ContractViolation("null anchor entries");
+            an.push_back(ss::Anchor{to_batch(anchors[i].entries, anchors[i].n_entries), anchors[i].observed_ms});
+        }
+        ss::CalibrationOptions o;
+        if (opts) {
+            o.tile_size = opts->tile_size;
+            o.tile_penalty_frac = opts->tile_penalty_frac;
+            o.max_saturation_tokens = opts->max_saturation_tokens;
+        }
+        const ss::Calibration c = ss::calibrate(an, o);
+        ssh_cost_params r{};
+        r.per_token_linear_ms = c.params.per_token_linear_ms;
+        r.saturation_tokens = c.params.saturation_tokens;
+        r.attn_prefill_quad_ms = c.params.attn_prefill_quad_ms;
+        r.attn_kv_read_ms = c.params.attn_kv_read_ms;
+        r.attn_decode_per_kv_ms = c.params.attn_decode_per_kv_ms;
+        r.fixed_overhead_ms = c.params.fixed_overhead_ms;
+        r.tp_comm_ms = c.params.tp_comm_ms;
+        r.pp_send_ms = c.params.pp_send_ms;
+        r.tile_size = c.params.tile_size;
+        r.tile_penalty_frac = c.params.tile_penalty_frac;
+        *out = r;
+        for (int32_t i = 0; i < n; ++i) {
+            if (predicted_ms) predicted_ms[i] = c.predicted_ms[size_t(i)];
+            if (relative_error) relative_error[i] = c.relative_error[size_t(i)];
+        }
+        if (max_relative_error) *max_relative_error = c.max_relative_error;
+        if (zeroed_mask) {
+            static const char* const names[5] = {"fixed_overhead_ms", "per_token_linear_ms", "attn_prefill_quad_ms",
+                                                 "attn_kv_read_ms", "attn_decode_per_kv_ms"};
+            int32_t m = 0;
+            for (const std::string& z : c.zeroed_terms)
+                for (int t = 0; t < 5; ++t)
+                    if (z == names[t]) m |= 1 << t;
+            *zeroed_mask = m;
+        }
+    });
+}
 
 ss_status ssh_compute_token_budget(double t_max_ms, const ssh_cost_params* p, int32_t pp, int32_t* out) {
     return guarded([&] { *out = ss::token_budget_for(t_max_ms, to_params(*p), pp); });

@@ -11,10 +11,10 @@ from __future__ import annotations
 
 import ctypes as C
 from dataclasses import dataclass, field, fields
-from typing import Iterable, List, Optional, Sequence
+from typing import Iterable, List, Optional, Sequence, Tuple
 
 from . import _lib
-from ._lib import ContractViolation, InfeasibleSlo, OutOfKvBlocks, host_check, host_lib  # noqa: F401
+from ._lib import CalibrationError, ContractViolation, InfeasibleSlo, OutOfKvBlocks, host_check, host_lib  # noqa: F401
 
 POLICIES = {"request_level": 0, "vllm": 1, "orca": 2, "stall_free": 3}
 
@@ -202,6 +202,51 @@ def compute_token_budget(t_max_ms: float, params: CostModelParams, pp_degree: in
     out = C.c_int32()
     host_check(host_lib().ssh_compute_token_budget(t_max_ms, C.byref(params._c()), pp_degree, C.byref(out)))
     return out.value
+
+
+@dataclass
+class CalibrationResult:
+    """servesim::CalibrationResult (costmodel.hpp:83-89)."""
+    params: CostModelParams
+    predicted_ms: List[float]
+    relative_error: List[float]
+    max_relative_error: float
+    zeroed_terms: List[str]
+
+
+CALIBRATION_TERMS = ["fixed_overhead_ms", "per_token_linear_ms", "attn_prefill_quad_ms", "attn_kv_read_ms",
+                     "attn_decode_per_kv_ms"]
+
+
+def _anchor_rows(anchors):
+    keep = []
+    rows = (_lib.AnchorRow * max(1, len(anchors)))()
+    for i, (entries, ms) in enumerate(anchors):
+        arr = (_lib.EntryRow * max(1, len(entries)))(*[e._c() for e in entries])
+        keep.append(arr)
+        rows[i].entries = C.cast(arr, C.POINTER(_lib.EntryRow))
+        rows[i].n_entries = len(entries)
+        rows[i].observed_ms = ms
+    return rows, keep
+
+
+def calibrate(anchors: Sequence[Tuple[Sequence[BatchEntry], float]], tile_size: int = 256,
+              tile_penalty_frac: float = 0.32, max_saturation_tokens: int = 2048) -> CalibrationResult:
+    """servesim::calibrate (calibrate.cpp:121-193): least-squares fit of the cost-model
+    constants to (batch, observed ms) anchors — the measured B200 clock.
+    Raises _lib.CalibrationError exactly where the reference throws CalibrationError."""
+    rows, _keep = _anchor_rows(anchors)
+    n = len(anchors)
+    opts = _lib.CalibOpts(tile_size, tile_penalty_frac, max_saturation_tokens)
+    out = _lib.CostParams()
+    pred = (C.c_double * max(1, n))()
+    rel = (C.c_double * max(1, n))()
+    mx = C.c_double()
+    mask = C.c_int32()
+    host_check(host_lib().ssh_calibrate(rows, n, C.byref(opts), C.byref(out), pred, rel, C.byref(mx), C.byref(mask)))
+    params = CostModelParams(**{f.name: getattr(out, f.name) for f in fields(CostModelParams)})
+    return CalibrationResult(params, list(pred[:n]), list(rel[:n]), mx.value,
+                             [t for i, t in enumerate(CALIBRATION_TERMS) if mask.value >> i & 1])
 
 
 def get_next_chunk_size(prompt_tokens: int, prefill_done: int, token_budget: int, packed_tokens: int,
