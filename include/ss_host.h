@@ -18,6 +18,8 @@
  *   ssh_percentile        <- percentile                    metrics.cpp:13-21
  *   ssh_decode_reference_time <- decode_reference_time     costmodel.cpp:83-85
  *   ssh_calibrate         <- servesim::calibrate           calibrate.cpp:121-193
+ *   ssh_capacity_search   <- servesim::capacity_search     metrics.cpp:70-138
+ *                            (probe = make_trace + simulate + summarize, cli.cpp:434-439)
  *
  * No exceptions cross this boundary: every call returns an ss_status and the
  * message of the last failure is available from ssh_last_error().
@@ -169,6 +171,34 @@ typedef struct {
 ss_status ssh_calibrate(const ssh_anchor* anchors, int32_t n, const ssh_calib_opts* opts,
                         ssh_cost_params* out, double* predicted_ms, double* relative_error,
                         double* max_relative_error, int32_t* zeroed_mask);
+/* servesim::CapacityOptions (metrics.hpp:45-49) plus the number of ladder rungs
+ * probed concurrently (the reference uses omp_get_max_threads(); 1 with a GPU). */
+typedef struct {
+    double qps_low;
+    double max_qps;
+    double rel_width;
+    int32_t parallel;
+} ssh_capacity_opts;
+
+/* servesim::CapacityProbe (metrics.hpp:51-55) */
+typedef struct {
+    double qps;
+    int32_t pass;
+    ssh_latency report;
+} ssh_capacity_probe;
+
+/* Maximum sustainable qps under slo_ms (P99 TBT) with median scheduling delay
+ * <= 2 s (meets_slo, metrics.cpp:65-67): every probe runs the reference
+ * workload preset trace make_trace(workload, qps, probe_requests, seed) through
+ * the engine with the cost model `params` — or, when sim->gpu is set, real
+ * forwards on that context (then opts->parallel must be 1). SS_INFEASIBLE when
+ * qps_low fails. probes (nullable) receives up to cap probes in search order. */
+ss_status ssh_capacity_search(const ssh_replica_cfg* cfg, const ssh_cost_params* params,
+                              const char* workload, int32_t probe_requests, uint64_t seed,
+                              double slo_ms, const ssh_capacity_opts* opts, const ssh_sim_opts* sim,
+                              double* qps_out, int32_t* monotone_warning,
+                              ssh_capacity_probe* probes, int32_t cap, int32_t* n_probes);
+
 int32_t ssh_next_chunk_size(int32_t prompt_tokens, int32_t prefill_done, int32_t token_budget,
                             int32_t packed_tokens, int32_t chunk_align);
 ss_status ssh_percentile(const double* series, int64_t n, double p, double* out);

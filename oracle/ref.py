@@ -49,6 +49,9 @@ def lib():
         L.ref_calibrate.argtypes = [C.POINTER(_lib.AnchorRow), I32, C.POINTER(_lib.CalibOpts), C.POINTER(_lib.CostParams),
                                     C.POINTER(D), C.POINTER(D), C.POINTER(I32)]
         L.ref_calibrate.restype = I32
+        L.ref_capacity.argtypes = [C.POINTER(_lib.ReplicaCfg), C.POINTER(_lib.CostParams), C.c_char_p, I32, C.c_uint64,
+                                   D, C.POINTER(_lib.CapacityOpts), C.POINTER(D), C.POINTER(I32), P, I32, C.POINTER(I32)]
+        L.ref_capacity.restype = I32
         L.ref_last_error.argtypes = []
         L.ref_last_error.restype = C.c_char_p
         _ref = L
@@ -111,3 +114,18 @@ def calibrate(anchor_rows, n: int, opts: _lib.CalibOpts):
     mask = C.c_int32()
     st = lib().ref_calibrate(anchor_rows, n, C.byref(opts), C.byref(out), pred, C.byref(mx), C.byref(mask))
     return st, out, list(pred[:n]), mx.value, mask.value
+
+
+def capacity(cfg: _lib.ReplicaCfg, params: _lib.CostParams, workload: str, n: int, seed: int, slo_ms: float,
+             opts: _lib.CapacityOpts):
+    """The reference's capacity_search with the CLI probe: (status, qps, monotone, probes)."""
+    qps = C.c_double()
+    mono = C.c_int32()
+    cap = 256
+    probes = (_lib.CapacityProbe * cap)()
+    npr = C.c_int32()
+    st = lib().ref_capacity(C.byref(cfg), C.byref(params), workload.encode(), n, seed, slo_ms, C.byref(opts),
+                            C.byref(qps), C.byref(mono), probes, cap, C.byref(npr))
+    out = [(p.qps, bool(p.pass_), {f: getattr(p.report, f) for f, _ in _lib.Latency._fields_})
+           for p in probes[:min(npr.value, cap)]]
+    return st, qps.value, bool(mono.value), out

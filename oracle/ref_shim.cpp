@@ -13,6 +13,8 @@
 //   ref_token_budget    -> servesim::compute_token_budget (sched.cpp:154-175)
 //   ref_cost_preset     -> servesim::model_preset (presets.cpp:71-77)
 //   ref_calibrate       -> servesim::calibrate (calibrate.cpp:121-193)
+//   ref_capacity        -> servesim::capacity_search with the CLI's probe
+//                          (metrics.cpp:70-138, cli.cpp:434-439)
 #include <cstring>
 #include <string>
 
@@ -214,6 +216,46 @@ int ref_calibrate(const ssh_anchor* anchors, int n, const ssh_calib_opts* opts, 
     } catch (const CalibrationError& e) {
         g_err = e.what();
         return 8;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return code_of(e);
+    }
+}
+
+// Same layout as ssh_capacity_search (no GPU). The reference is built here
+// without OpenMP, so its ladder probes one rung at a time (opts->parallel unused).
+int ref_capacity(const ssh_replica_cfg* cfg, const ssh_cost_params* params, const char* workload, int probe_requests,
+                 uint64_t seed, double slo_ms, const ssh_capacity_opts* opts, double* qps_out, int* monotone,
+                 ssh_capacity_probe* probes, int cap, int* n_probes) {
+    try {
+        const auto w = workload_preset(workload);
+        if (!w) throw ContractViolation("unknown workload preset");
+        const ReplicaConfig rc = to_cfg(*cfg);
+        const CostModelParams cp = to_params(*params);
+        CapacityOptions o;
+        o.qps_low = opts->qps_low;
+        o.max_qps = opts->max_qps;
+        o.rel_width = opts->rel_width;
+        const ProbeFn probe = [&](double qps) {
+            SimOptions so;
+            so.keep_events = false;
+            so.keep_microbatches = false;
+            so.keep_kv_series = false;
+            return summarize(simulate(rc, cp, make_trace(*w, qps, probe_requests, seed), so));
+        };
+        const CapacityResult r = capacity_search(probe, slo_ms, o);
+        *qps_out = r.qps;
+        *monotone = r.monotone_warning;
+        *n_probes = int(r.probes.size());
+        for (size_t i = 0; i < r.probes.size() && int(i) < cap; ++i) {
+            const LatencyReport& L = r.probes[i].report;
+            probes[i] = ssh_capacity_probe{r.probes[i].qps, r.probes[i].pass,
+                                           ssh_latency{L.ttft_median_ms, L.tbt_p99_ms, L.tbt_median_ms,
+                                                       L.sched_delay_median_ms, L.throughput_tps,
+                                                       L.bubble_fraction, L.makespan_ms, L.tbt_samples,
+                                                       L.n_requests}};
+        }
+        return 0;
     } catch (const std::exception& e) {
         g_err = e.what();
         return code_of(e);

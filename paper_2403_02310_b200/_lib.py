@@ -80,6 +80,10 @@ class EntryRow(C.Structure):
     _fields_ = [("request_id", C.c_int32), ("kind", C.c_int32), ("chunk_tokens", C.c_int32), ("prefix_tokens", C.c_int64)]
 
 
+class CapacityOpts(C.Structure):
+    _fields_ = [("qps_low", C.c_double), ("max_qps", C.c_double), ("rel_width", C.c_double), ("parallel", C.c_int32)]
+
+
 class AnchorRow(C.Structure):
     _fields_ = [("entries", C.POINTER(EntryRow)), ("n_entries", C.c_int32), ("observed_ms", C.c_double)]
 
@@ -99,6 +103,10 @@ class Latency(C.Structure):
 class SimOpts(C.Structure):
     _fields_ = [("keep_events", C.c_int32), ("max_events", C.c_int64), ("gpu", C.c_void_p),
                 ("token_seed", C.c_uint64), ("check_block_tables", C.c_int32)]
+
+
+class CapacityProbe(C.Structure):
+    _fields_ = [("qps", C.c_double), ("pass_", C.c_int32), ("report", Latency)]
 
 
 class ModelCfg(C.Structure):
@@ -188,6 +196,9 @@ def host_lib():
         _sig(lib, "ssh_iteration_time", D, [C.POINTER(EntryRow), I32, C.POINTER(CostParams), I32, I32])
         _sig(lib, "ssh_decode_reference_time", D, [C.POINTER(CostParams)])
         _sig(lib, "ssh_compute_token_budget", I32, [D, C.POINTER(CostParams), I32, C.POINTER(I32)])
+        _sig(lib, "ssh_capacity_search", I32, [C.POINTER(ReplicaCfg), C.POINTER(CostParams), C.c_char_p, I32,
+                                               C.c_uint64, D, C.POINTER(CapacityOpts), C.POINTER(SimOpts), C.POINTER(D),
+                                               C.POINTER(I32), P, I32, C.POINTER(I32)])
         _sig(lib, "ssh_calibrate", I32, [C.POINTER(AnchorRow), I32, C.POINTER(CalibOpts), C.POINTER(CostParams),
                                          C.POINTER(D), C.POINTER(D), C.POINTER(D), C.POINTER(I32)])
         _sig(lib, "ssh_next_chunk_size", I32, [I32, I32, I32, I32, I32])
@@ -223,7 +234,7 @@ HOST_EXPORTS = [
     "ssh_replica_default", "ssh_cost_preset", "ssh_make_trace", "ssh_make_trace_spec", "ssh_simulate",
     "ssh_report_event_log", "ssh_report_summary", "ssh_report_num_microbatches", "ssh_report_microbatch",
     "ssh_report_peak_blocks", "ssh_report_free", "ssh_iteration_time", "ssh_decode_reference_time",
-    "ssh_compute_token_budget", "ssh_calibrate", "ssh_next_chunk_size", "ssh_percentile", "ssh_desc_build", "ssh_desc_canonical",
+    "ssh_compute_token_budget", "ssh_calibrate", "ssh_capacity_search", "ssh_next_chunk_size", "ssh_percentile", "ssh_desc_build", "ssh_desc_canonical",
     "ssh_desc_view", "ssh_desc_pool_blocks", "ssh_desc_free", "ssh_session_create", "ssh_session_step",
     "ssh_session_release", "ssh_session_peak_blocks", "ssh_session_free", "ssh_last_error",
 ]

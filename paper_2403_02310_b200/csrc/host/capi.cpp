@@ -6,6 +6,7 @@
 
 #include "../../../include/ss_host.h"
 #include "calibrate.hpp"
+#include "capacity.hpp"
 #include "costmodel.hpp"
 #include "descriptor.hpp"
 #include "engine.hpp"
@@ -322,6 +323,49 @@ ss_status ssh_calibrate(const ssh_anchor* anchors, int32_t n, const ssh_calib_op
                 for (int t = 0; t < 5; ++t)
                     if (z == names[t]) m |= 1 << t;
             *zeroed_mask = m;
+        }
+    });
+}
+
+ss_status ssh_capacity_search(const ssh_replica_cfg* cfg, const ssh_cost_params* params, const char* workload,
+                              int32_t probe_requests, uint64_t seed, double slo_ms, const ssh_capacity_opts* opts,
+                              const ssh_sim_opts* sim, double* qps_out, int32_t* monotone_warning,
+                              ssh_capacity_probe* probes, int32_t cap, int32_t* n_probes) {
+    return guarded([&] {
+        if (!cfg || !params || !qps_out) throw ss::ContractViolation("null argument");
+        const auto w = ss::workload_preset(workload ? workload : "");
+        if (!w) throw ss::ContractViolation("unknown workload preset");
+        const ss::ReplicaConfig rc = to_cfg(*cfg);
+        const ss::CostParams cp = to_params(*params);
+        ss::CapacityOptions o;
+        if (opts) {
+            o.qps_low = opts->qps_low;
+            o.max_qps = opts->max_qps;
+            o.rel_width = opts->rel_width;
+            o.parallel = opts->parallel;
+        }
+        ss_ctx* gpu = sim ? sim->gpu : nullptr;
+        if (gpu && o.parallel != 1) throw ss::ContractViolation("GPU capacity probes run one at a time (parallel = 1)");
+        const std::uint64_t token_seed = sim ? sim->token_seed : 0;
+        const ss::Probe probe = [&](double qps) {
+            const std::vector<ss::Request> trace = ss::make_trace(*w, qps, probe_requests, seed);
+            ss::SimOptions so;
+            so.keep_events = false;  // probe_sim_options, cli.cpp:373-379
+            std::unique_ptr<ss::StepExecutor> exec;
+            if (gpu) exec = std::make_unique<GpuExecutor>(gpu, token_seed);
+            else exec = std::make_unique<ss::CostModelExecutor>(cp, rc.tp, rc.pp);
+            return ss::summarize(ss::simulate(rc, cp, trace, *exec, so));
+        };
+        const ss::CapacityResult r = ss::capacity_search(probe, slo_ms, o);
+        *qps_out = r.qps;
+        if (monotone_warning) *monotone_warning = r.monotone_warning;
+        if (n_probes) *n_probes = int32_t(r.probes.size());
+        for (std::size_t i = 0; probes && i < r.probes.size() && int32_t(i) < cap; ++i) {
+            const ss::Latency& L = r.probes[i].report;
+            probes[i] = ssh_capacity_probe{r.probes[i].qps, r.probes[i].pass,
+                                           ssh_latency{L.ttft_median_ms, L.tbt_p99_ms, L.tbt_median_ms,
+                                                       L.sched_delay_median_ms, L.throughput_tps, L.bubble_fraction,
+                                                       L.makespan_ms, L.tbt_samples, L.n_requests}};
         }
     });
 }

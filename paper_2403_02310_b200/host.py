@@ -249,6 +249,50 @@ def calibrate(anchors: Sequence[Tuple[Sequence[BatchEntry], float]], tile_size: 
                              [t for i, t in enumerate(CALIBRATION_TERMS) if mask.value >> i & 1])
 
 
+@dataclass
+class CapacityProbe:
+    qps: float
+    passed: bool
+    report: dict
+
+
+@dataclass
+class CapacityResult:
+    """servesim::CapacityResult (metrics.hpp:57-61)."""
+    qps: float
+    monotone_warning: bool
+    probes: List[CapacityProbe]
+
+
+def slo_thresholds(params: CostModelParams) -> Tuple[float, float]:
+    """metrics.cpp:60-63: (strict, relaxed) = (5x, 25x) the 32x4k decode iteration."""
+    ref = decode_reference_time(params)
+    return 5.0 * ref, 25.0 * ref
+
+
+def capacity_search(cfg: ReplicaConfig, params: CostModelParams, workload: str, probe_requests: int, seed: int,
+                    slo_ms: float, *, qps_low: float = 0.01, max_qps: float = 1024.0, rel_width: float = 0.05,
+                    parallel: int = 1, gpu=None, token_seed: int = 0) -> CapacityResult:
+    """servesim::capacity_search (metrics.cpp:70-138) with the CLI's probe (cli.cpp:434-439):
+    make_trace(workload, qps, probe_requests, seed) -> simulate -> summarize -> meets_slo.
+    params is the clock (a reference preset, or a calibrated B200 clock from clock.py);
+    with gpu (a gpu.HybridForward) every probe runs real forwards. Raises InfeasibleSlo
+    when qps_low fails."""
+    opts = _lib.CapacityOpts(qps_low, max_qps, rel_width, parallel)
+    sim = _lib.SimOpts(0, 0, gpu.handle.value if gpu is not None else None, token_seed, 0)
+    qps = C.c_double()
+    mono = C.c_int32()
+    cap = 256
+    probes = (_lib.CapacityProbe * cap)()
+    n = C.c_int32()
+    host_check(host_lib().ssh_capacity_search(C.byref(cfg._c()), C.byref(params._c()), workload.encode(),
+                                              probe_requests, seed, slo_ms, C.byref(opts), C.byref(sim),
+                                              C.byref(qps), C.byref(mono), probes, cap, C.byref(n)))
+    out = [CapacityProbe(p.qps, bool(p.pass_), {f: getattr(p.report, f) for f, _ in _lib.Latency._fields_})
+           for p in probes[:min(n.value, cap)]]
+    return CapacityResult(qps.value, bool(mono.value), out)
+
+
 def get_next_chunk_size(prompt_tokens: int, prefill_done: int, token_budget: int, packed_tokens: int,
                         chunk_align: int) -> int:
     return host_lib().ssh_next_chunk_size(prompt_tokens, prefill_done, token_budget, packed_tokens, chunk_align)
