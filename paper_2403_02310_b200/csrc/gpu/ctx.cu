@@ -179,7 +179,7 @@ struct ss_ctx {
     float *part_o = nullptr, *part_ml = nullptr;
     int32_t* comb_count = nullptr;  // split-KV group counters (self-resetting)
     int fused_combine = 0;          // in-kernel split merge (measured slower at 8 splits; off)
-    int decode_split = 1536;        // target keys per split-KV piece for decode-like items (measured)
+    int decode_split = 0;           // dev override (SS_ATTN_SPLIT): fixed keys per decode split; 0 = adaptive
     int fuse_rope = 1;              // RoPE + KV append in the QKV GEMM epilogue (else the K2 kernel)
     float* sk_part = nullptr;       // stream-K GEMM partial accumulators
     uint32_t* sk_flags = nullptr;   // stream-K ready flags
@@ -369,7 +369,7 @@ void build_items(const ss_ctx* ctx, const ss_batch_desc* d, std::vector<AttnItem
         int e, row0, nr, extent;
     };
     std::vector<Tile> tiles;
-    int prefill_items = 0;
+    int prefill_items = 0, decode_pairs = 0;
     for (int e = 0; e < d->num_entries; ++e) {
         const int ntok = d->cu_q[e + 1] - d->cu_q[e];
         const int prefix = d->ctx_len[e] - ntok;
@@ -378,14 +378,30 @@ void build_items(const ss_ctx* ctx, const ss_batch_desc* d, std::vector<AttnItem
             const int nr = std::min(64, rows - row0);
             tiles.push_back(Tile{e, row0, nr, prefix + (row0 + nr - 1) / G + 1});
             if (nr > 16) prefill_items += ctx->nkv_l;
+            else decode_pairs += ctx->nkv_l;
         }
     }
     const int long_split = prefill_items < ctx->num_sms ? 2048 : (1 << 30);
     part_rows = 0;
     for (const Tile& t : tiles) {
-        const int split = t.nr <= 16 ? ctx->decode_split : long_split;
+        // Decodes: split a (sequence, kv head) pair's keys only when there are
+        // fewer pairs than SMs (one streaming CTA per SM already saturates HBM;
+        // measured on the canonical batch, 256 unsplit pairs beat 768 splits +
+        // combine by 2%); never below 512 keys per split.
+        // SS_ATTN_SPLIT (dev) forces a fixed split length instead.
+        int ns;
+        if (t.nr <= 16) {
+            if (ctx->decode_split > 0) {
+                ns = std::max(1, (t.extent + ctx->decode_split / 2) / ctx->decode_split);
+            } else {
+                const int target = ctx->num_sms;
+                ns = decode_pairs >= target ? 1 : (target + decode_pairs - 1) / decode_pairs;
+                ns = std::max(1, std::min(ns, t.extent / 512));
+            }
+        } else {
+            ns = long_split >= (1 << 30) ? 1 : std::max(1, (t.extent + long_split / 2) / long_split);
+        }
         // balanced splits on 64-key boundaries (no 1-key tail splits)
-        const int ns = split >= (1 << 30) ? 1 : std::max(1, (t.extent + split / 2) / split);
         auto bound = [&](int s) { return s >= ns ? t.extent : int((int64_t(s) * t.extent / ns) & ~int64_t(63)); };
         for (int h = 0; h < ctx->nkv_l; ++h) {
             if (ns <= 1) {

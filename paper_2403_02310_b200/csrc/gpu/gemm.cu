@@ -948,6 +948,14 @@ cudaError_t gemm_launch(const GemmPlan& p, cudaStream_t st) {
 #ifdef SS_GEMM_TRACE
 extern "C" __attribute__((visibility("default"))) int ss_debug_gemm_trace(unsigned long long* out, int n) {
     if (cudaDeviceSynchronize() != cudaSuccess) return -1;
+    if (n < 0) {  // clear both tables
+        static unsigned long long zeros[1024 * 8] = {};
+        return cudaMemcpyToSymbol(ssk::g_gemm_trace, zeros, sizeof(zeros)) == cudaSuccess &&
+                       cudaMemcpyToSymbol(ssk::g_gemm_trace2, zeros, sizeof(unsigned long long) * 4 * 1024) ==
+                           cudaSuccess
+                   ? 0
+                   : -1;
+    }
     if (n > 1024) {  // second table: epilogue-warp stamps of the last segment
         return cudaMemcpyFromSymbol(out, ssk::g_gemm_trace2, sizeof(unsigned long long) * 4 * 1024) == cudaSuccess
                    ? 0

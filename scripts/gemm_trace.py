@@ -14,6 +14,8 @@ flush = torch.empty(512 * 1024 * 1024 // 4, device="cuda", dtype=torch.float32)
 shapes = [("qkv", 512, 6144, 4096, 0), ("o", 512, 4096, 4096, 1), ("gate_up", 512, 28672, 4096, 2),
           ("down", 512, 4096, 14336, 1)]
 only = os.environ.get("ONLY")
+if os.environ.get("M"):
+    shapes = [(n, int(os.environ["M"]), N, K, e) for n, _, N, K, e in shapes]
 for name, M, N, K, epi in shapes:
     if only and name not in only.split(","):
         continue
@@ -25,7 +27,7 @@ for name, M, N, K, epi in shapes:
     if cold:
         flush.fill_(1.0)
     torch.cuda.synchronize()
-    zero = np.zeros((1024, 8), np.uint64)
+    lib.ss_debug_gemm_trace(None, -1)  # clear both tables
     f.k_gemm(A, B, D, M, N, K, epi)
     tr = np.zeros((1024, 8), np.uint64)
     assert lib.ss_debug_gemm_trace(tr.ctypes.data_as(C.POINTER(C.c_ulonglong)), 1024) == 0
