@@ -523,6 +523,27 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
             }
+            // QKV: this row's position/slot and the RoPE factors of the warp's first
+            // chunk pair, also fetched while the MMAs run (a dependent load chain)
+            int q_pos = 0;
+            int64_t q_slot = 0;
+            float2 rc[32];
+            if constexpr (EPI == EPI_QKV) {
+                if (kb0 == 0 && row < M) {
+                    q_pos = ea.pos[row];
+                    q_slot = ea.slot[row];
+                    const int ps = ea.hd / 64;
+                    if (half < (BN / ea.hd) * ps) {
+                        const int c = (half / ps) * (2 * ps) + (half % ps);
+                        const int col = n0 + c * 32;
+                        if (col < N && col / ea.hd < ea.nq + ea.nkv) {
+                            const float2* cs = ea.rope + size_t(q_pos) * (ea.hd / 2) + col % ea.hd;
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) rc[j] = cs[j];
+                        }
+                    }
+                }
+            }
             mbar_wait(&tfull[acc], acc_ph);
             tc_fence_after();
             TRACE2(0);
@@ -639,8 +660,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     // chunk pairs (c, c + ps) hold the rotate-half partners i, i + hd/2 of one head
                     const int ps = ea.hd / 64;
                     const int row_ok = row < M;
-                    const int p_row = row_ok ? ea.pos[row] : 0;
-                    const int64_t s_row = row_ok ? ea.slot[row] : 0;
+                    const int p_row = q_pos;
+                    const int64_t s_row = q_slot;
                     const int64_t blk = s_row / ea.bs, off = s_row % ea.bs;
 #pragma unroll 1
                     for (int pi = half; pi < (BN / ea.hd) * ps; pi += 2) {
@@ -662,7 +683,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                             const float2* cs = ea.rope + size_t(p_row) * (ea.hd / 2) + i0;
 #pragma unroll
                             for (int j = 0; j < 16; ++j) {
-                                const float2 c0 = cs[2 * j], c1 = cs[2 * j + 1];
+                                const bool pre = pi == half;  // factors preloaded before the wait
+                                const float2 c0 = pre ? rc[2 * j] : cs[2 * j], c1 = pre ? rc[2 * j + 1] : cs[2 * j + 1];
                                 const float a0 = __uint_as_float(x1[2 * j]) * rs, a1 = __uint_as_float(x1[2 * j + 1]) * rs;
                                 const float b0 = __uint_as_float(x2[2 * j]) * rs, b1 = __uint_as_float(x2[2 * j + 1]) * rs;
                                 lo[j] = pack_bf16(a0 * c0.x - b0 * c0.y, a1 * c1.x - b1 * c1.y);
