@@ -133,6 +133,15 @@ __device__ __forceinline__ void commit_cg(uint64_t* bar) {
     }
 }
 
+// One lane of the (fully active) warp: the issuer of single-thread tcgen05 ops.
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}"
+        : "=r"(pred));
+    return pred != 0;
+}
+
 __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
     uint32_t v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -428,8 +437,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0 && leader) {  // ---------------- MMA issuer (leader CTA only)
+        // ---------------- MMA issuer (leader CTA only). The whole warp walks the
+        // schedule converged, so descriptors and counters are warp-uniform and
+        // live in uniform registers; one elected lane issues MMAs and commits
+        // (a lone-lane issuer compiles to a per-MMA waterfall of R2UR moves that
+        // starves the tensor core on narrow tiles).
+        if (leader) {
             constexpr uint32_t idesc = umma_idesc_bf16(Cfg::TILE_M, BN);
+            const uint64_t adesc0 = umma_desc_sw128(smem_u32(sA)), bdesc0 = umma_desc_sw128(smem_u32(sB));
             int s = 0;
             uint32_t ph = 0;
             int acc = 0;
@@ -445,29 +460,32 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t d_tmem = tmem_base + uint32_t(acc * BN);
                 const int nk = kb1 - kb0;
                 for (int i = 0; i < nk; ++i) {
-                    mbar_wait(&full[s], ph);
-                    tc_fence_after();
+                    mbar_wait(&full[s], ph);  // TMA (async proxy) -> MMA (async proxy): no fence
 #ifdef SS_GEMM_TRACE
-                    if (i == 0 && seg_no == 0) TRACE(2);
+                    if (i == 0 && seg_no == 0 && lane == 0) TRACE(2);
 #endif
-                    const uint32_t a_addr = smem_u32(sA + s * Cfg::A_BYTES);
-                    const uint32_t b_addr = smem_u32(sB + s * Cfg::B_BYTES);
-#if defined(SS_GEMM_EXP) && SS_GEMM_EXP == 2  // dev experiment: loads only, no MMA
-                    if (false)
-#endif
+                    // descriptor start field is addr >> 4: stage / K-step offsets add directly
+                    const uint64_t ad = adesc0 + uint64_t((s * Cfg::A_BYTES) >> 4);
+                    const uint64_t bd = bdesc0 + uint64_t((s * Cfg::B_BYTES) >> 4);
+                    if (elect_one()) {
+#if !(defined(SS_GEMM_EXP) && SS_GEMM_EXP == 2)  // dev experiment 2: loads only
 #pragma unroll
-                    for (int k = 0; k < BK / 16; ++k)
-                        mma_cg<CG>(d_tmem, umma_desc_sw128(a_addr + 32 * k), umma_desc_sw128(b_addr + 32 * k), idesc,
-                                   (i > 0 || k > 0) ? 1u : 0u);
-                    commit_cg<CG>(&empty[s]);  // smem slot free (in both CTAs) once these MMAs retire
+                        for (int k = 0; k < BK / 16; ++k)
+                            mma_cg<CG>(d_tmem, ad + uint64_t(2 * k), bd + uint64_t(2 * k), idesc,
+                                       (i > 0 || k > 0) ? 1u : 0u);
+#endif
+                        commit_cg<CG>(&empty[s]);  // slot free (in both CTAs) once these MMAs retire
+                    }
+                    __syncwarp();
                     if (++s == STAGES) {
                         s = 0;
                         ph ^= 1;
                     }
                 }
-                commit_cg<CG>(&tfull[acc]);  // accumulator ready for both CTAs' epilogues
+                if (elect_one()) commit_cg<CG>(&tfull[acc]);  // accumulator ready for both CTAs' epilogues
+                __syncwarp();
 #ifdef SS_GEMM_TRACE
-                if (seg_no < 4) TRACE(3 + seg_no);
+                if (seg_no < 4 && lane == 0) TRACE(3 + seg_no);
                 ++seg_no;
 #endif
                 if (++acc == 2) {
