@@ -166,6 +166,17 @@ def run_ours(args):
 
     for _ in range(args.warmup):
         fwd.enqueue(batch)
+    if args.profile_step:
+        # one steady-state step bracketed by cudaProfilerStart/Stop, for
+        # `ncu --profile-from-start off` launch lists and captures
+        fwd.synchronize()
+        torch.cuda.profiler.start()
+        fwd.enqueue(batch)
+        fwd.synchronize()
+        torch.cuda.profiler.stop()
+        batch.free()
+        fwd.close()
+        return
     clock = ClockSampler(local)
     clock.start()
     time.sleep(0.2)
@@ -413,6 +424,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--tbt-requests", type=int, default=48, help="closed-loop P99 TBT trace size (0: skip)")
     ap.add_argument("--tbt-qps", type=float, default=4.0)
+    ap.add_argument("--profile-step", action="store_true",
+                    help="profiling only: after warm-up run one step between cudaProfilerStart/Stop and exit")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
