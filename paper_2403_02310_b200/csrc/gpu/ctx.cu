@@ -416,8 +416,11 @@ void build_items(const ss_ctx* ctx, const ss_batch_desc* d, std::vector<AttnItem
             part_rows += ns * t.nr;
         }
     }
-    // longest items first so the tail of the launch is short
+    // longest items first so the tail of the launch is short (SS_ATTN_ORDER=1,
+    // dev: prefill row tiles first)
+    static const int order = getenv("SS_ATTN_ORDER") ? atoi(getenv("SS_ATTN_ORDER")) : 0;
     std::stable_sort(items.begin(), items.end(), [](const AttnItem& a, const AttnItem& b) {
+        if (order == 1 && (a.nrows > 16) != (b.nrows > 16)) return a.nrows > 16;
         const long ca = long(a.key1 - a.key0) * (a.nrows <= 16 ? 16 : 64);
         const long cb = long(b.key1 - b.key0) * (b.nrows <= 16 ? 16 : 64);
         return ca > cb;
@@ -556,10 +559,21 @@ ss_status gemm(ss_ctx* ctx, int cls, const CUtensorMap& ta, WMaps& tb, int M, in
     p.ldo = ldo;
     p.epi = epi;
     p.num_sms = ctx->num_sms;
-    const GemmShape s = gemm_pick(M, N, K, epi, ctx->num_sms);
+    GemmShape s = gemm_pick(M, N, K, epi, ctx->num_sms);
+    {  // dev tuning: SS_GEMM_<class>=mode,bn[,splits] overrides the pick for one projection
+        static const char* names[] = {"QKV", "O", "GATEUP", "DOWN", "LMHEAD"};
+        const int idx = cls == SS_K_GEMM_QKV ? 0 : cls == SS_K_GEMM_O ? 1 : cls == SS_K_GEMM_GATEUP ? 2
+                      : cls == SS_K_GEMM_DOWN ? 3 : 4;
+        const std::string var = std::string("SS_GEMM_") + names[idx];
+        if (const char* f = getenv(var.c_str())) {
+            int md = s.mode, bn = s.bn, sp = 1;
+            if (sscanf(f, "%d,%d,%d", &md, &bn, &sp) >= 2) s = GemmShape{M > 128 ? 2 : 1, bn, sp, md};
+        }
+    }
     p.cg = s.cg;
     p.bn = s.bn;
     p.splits = s.splits;
+    p.sk_mode = s.mode;
     p.tmA = ta;
     const CUtensorMap* mb = tb.get(p.bn / p.cg);
     if (!mb) return fail(ctx, SS_CUDA_ERROR, "cuTensorMapEncodeTiled failed (weight tile map)");
@@ -1118,7 +1132,8 @@ SS_API ss_status ss_k_gemm(ss_ctx* ctx, const void* A, const void* B, void* D, i
                            int32_t epi) {
     if (!ctx || epi < 0 || epi > 3) return fail(ctx, SS_INVALID_ARG, "bad gemm arguments");
     GemmPlan p;
-    const int ldo = epi == EPI_SWIGLU ? N / 2 : N;
+    int ldo = epi == EPI_SWIGLU ? N / 2 : N;
+    if (const char* f = getenv("SS_GEMM_LDO_PAD")) ldo += atoi(f);  // dev: padded output rows
     if (!gemm_prepare(p, A, uint64_t(M), B, M, N, K, D, ldo, epi, ctx->num_sms))
         return fail(ctx, SS_INVALID_ARG, "gemm shape unsupported (N%32, K%8, SwiGLU N%64) or tensor map failed");
     p.part = ctx->sk_part;

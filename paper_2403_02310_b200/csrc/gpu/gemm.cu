@@ -35,7 +35,8 @@ namespace {
 
 constexpr int BK = 64;  // 128 B of bf16: one SWIZZLE_128B row
 constexpr int kThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue
-constexpr int kSmemBudget = 200 * 1024;
+constexpr int kSmemMax = 232448;                         // 227 KB opt-in per CTA
+constexpr int kSmemBudget = kSmemMax - 1024 - 1024 - 8 * 4096;  // operand ring
 
 template <int CG, int BN>
 struct GemmCfg {
@@ -46,7 +47,9 @@ struct GemmCfg {
     static constexpr int STAGES_FIT = kSmemBudget / STAGE_BYTES;
     static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
     static constexpr int TMEM_COLS = 2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512);
-    static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + 256;
+    // + barriers (1 KB slot) + the epilogue warps' 4 KB staging buffers
+    static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + 1024 + 8 * 4096;
+    static_assert(SMEM <= kSmemMax, "shared memory over the per-CTA limit");
     static constexpr int TILE_M = 128 * CG;
 };
 
@@ -168,6 +171,12 @@ __device__ __forceinline__ long sk_start(int g, int G, long total) { return long
 // Work segments of one group. mode 0: whole tiles round-robin (tile g, g+G, ...:
 // concurrently active tiles are neighbours, so B/A tiles are shared in L2);
 // mode 1: the group's stream-K range cut at tile boundaries.
+// mode 3: M-lockstep stream-K. The groups form super-groups of P = num_mt
+// consecutive groups, member m owning M-tile m; stream-K runs over the
+// (N-tile, k-block) space of the super-groups, so the P members walk identical
+// B k-blocks at the same time (each weight byte leaves HBM once, the P reads
+// meet in L2) and every group gets the same number of k-blocks whatever the
+// tile count — no wave quantisation for the under-filled M = 256..2048 shapes.
 struct Seg {
     int t, kb0, kb1;
 };
@@ -176,10 +185,10 @@ struct Seg {
 // every group walks the same K offsets at the same time (A k-blocks shared in
 // L2) and a tile's pieces sit on consecutive groups.
 struct SegIter {
-    int mode, G, num_kb, num_tiles, t_rr, S;
+    int mode, G, num_kb, num_tiles, t_rr, S, P, mem;
     long i, i1;
-    __device__ SegIter(int m, int gid, int G_, int nkb, int nt, SkRange r, int S_)
-        : mode(m), G(G_), num_kb(nkb), num_tiles(nt), t_rr(gid), S(S_), i(r.i0), i1(r.i1) {}
+    __device__ SegIter(int m, int gid, int G_, int nkb, int nt, SkRange r, int S_, int P_)
+        : mode(m), G(G_), num_kb(nkb), num_tiles(nt), t_rr(gid), S(S_), P(P_), mem(gid % P_), i(r.i0), i1(r.i1) {}
     __device__ __forceinline__ bool next(Seg& s) {
         if (mode == 0) {
             if (t_rr >= num_tiles) return false;
@@ -205,7 +214,7 @@ struct SegIter {
             return true;
         }
         if (i >= i1) return false;
-        s.t = int(i / num_kb);
+        s.t = int(i / num_kb) * P + mem;  // mode 3: N-tile i / num_kb, this member's M-tile
         s.kb0 = int(i % num_kb);
         s.kb1 = int(s.kb0 + (i1 - i) < num_kb ? s.kb0 + (i1 - i) : num_kb);
         i += s.kb1 - s.kb0;
@@ -218,67 +227,26 @@ struct SegIter {
 // entry, after pdl_wait, first full stage, last MMA of the first segment,
 // accumulator seen by the epilogue, first segment stored, exit.
 __device__ unsigned long long g_gemm_trace[1024][8];
+__device__ int g_trace_epi = -1;  // >= 0: record only launches with this epilogue
 __device__ __forceinline__ void trace(int i) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     if (blockIdx.x < 1024) g_gemm_trace[blockIdx.x][i] = t;
 }
-__device__ unsigned long long g_gemm_trace2[1024][4];
+__device__ unsigned long long g_gemm_trace2[1024][16];
 __device__ __forceinline__ void trace2(int i) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     if (blockIdx.x < 1024) g_gemm_trace2[blockIdx.x][i] = t;
 }
-#define TRACE(i) trace(i)
+#define TRACE(i) \
+    if (g_trace_epi < 0 || g_trace_epi == EPI) trace(i)
 #define TRACE2(i) \
-    if (warp == 2 && lane == 0) trace2(i)
+    if (warp == 2 && lane == 0 && (g_trace_epi < 0 || g_trace_epi == EPI)) trace2(i)
 #else
 #define TRACE(i)
 #define TRACE2(i)
 #endif
-
-template <int EPI>
-__device__ __forceinline__ void epi_store(const uint32_t (&v)[32], int row, int col, void* out, int ldo,
-                                          const EpiArgs& ea) {
-    if constexpr (EPI == EPI_BF16) {
-        __nv_bfloat16* o = static_cast<__nv_bfloat16*>(out) + size_t(row) * ldo + col;
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-            reinterpret_cast<uint4*>(o)[j] =
-                make_uint4(pack_bf16(__uint_as_float(v[8 * j + 0]), __uint_as_float(v[8 * j + 1])),
-                           pack_bf16(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3])),
-                           pack_bf16(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5])),
-                           pack_bf16(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7])));
-    } else if constexpr (EPI == EPI_RESADD) {
-        float4* o = reinterpret_cast<float4*>(static_cast<float*>(out) + size_t(row) * ldo + col);
-        float ss = 0.f;
-        uint32_t pk[16];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            float4 x = o[j];
-            x.x += __uint_as_float(v[4 * j + 0]);
-            x.y += __uint_as_float(v[4 * j + 1]);
-            x.z += __uint_as_float(v[4 * j + 2]);
-            x.w += __uint_as_float(v[4 * j + 3]);
-            o[j] = x;
-            ss += x.x * x.x + x.y * x.y + x.z * x.z + x.w * x.w;
-            pk[2 * j] = pack_bf16(x.x, x.y);
-            pk[2 * j + 1] = pack_bf16(x.z, x.w);
-        }
-        if (ea.xb_out) {  // feed the next norm-folded GEMM: bf16 row copy + chunk sum of squares
-            uint4* xb = reinterpret_cast<uint4*>(ea.xb_out + size_t(row) * ldo + col);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) xb[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
-            ea.ssq_out[size_t(row) * (ldo / 32) + col / 32] = ss;
-        }
-    } else {  // EPI_F32
-        float4* o = reinterpret_cast<float4*>(static_cast<float*>(out) + size_t(row) * ldo + col);
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-            o[j] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]), __uint_as_float(v[4 * j + 2]),
-                               __uint_as_float(v[4 * j + 3]));
-    }
-}
 
 // ---- staged split-K fixup (last segment of a group: the smem ring is idle)
 // Partial layout per (group, CTA rank): [chunk c][row 0..127][32 fp32], a warp's
@@ -310,42 +278,21 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
 }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
-// p = this thread's 32-float row slice of one chunk in the partial layout above
-// EPI_RESADD with the residual already in registers (x_in = the row's 32 floats at col)
-__device__ __forceinline__ void epi_resadd(const uint32_t (&v)[32], int row, int col, void* out, int ldo,
-                                           const EpiArgs& ea, const float4 (&x_in)[8]) {
-    float4* o = reinterpret_cast<float4*>(static_cast<float*>(out) + size_t(row) * ldo + col);
-    float ss = 0.f;
-    uint32_t pk[16];
+// Per-warp epilogue staging buffer: 32 rows x 128 B, 16-byte chunk j of row r at
+// slot r * 8 + (j ^ (r & 7)). stage_rows writes this thread's row (thread = row);
+// add_rows adds the staged fp32 row to v.
+__device__ __forceinline__ void stage_rows(uint4* ep, const uint32_t (&v)[32], int lane) {
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        float4 x = x_in[j];
-        x.x += __uint_as_float(v[4 * j + 0]);
-        x.y += __uint_as_float(v[4 * j + 1]);
-        x.z += __uint_as_float(v[4 * j + 2]);
-        x.w += __uint_as_float(v[4 * j + 3]);
-        o[j] = x;
-        ss += x.x * x.x + x.y * x.y + x.z * x.z + x.w * x.w;
-        pk[2 * j] = pack_bf16(x.x, x.y);
-        pk[2 * j + 1] = pack_bf16(x.z, x.w);
-    }
-    if (ea.xb_out) {
-        uint4* xb = reinterpret_cast<uint4*>(ea.xb_out + size_t(row) * ldo + col);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) xb[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
-        ea.ssq_out[size_t(row) * (ldo / 32) + col / 32] = ss;
-    }
+    for (int j = 0; j < 8; ++j) ep[lane * 8 + (j ^ (lane & 7))] = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
 }
-
-__device__ __forceinline__ void add_partial(uint32_t (&v)[32], const float* p, int lane) {
-    const float4* q = reinterpret_cast<const float4*>(p);
+__device__ __forceinline__ void add_rows(uint32_t (&v)[32], const uint4* ep, int lane) {
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-        const float4 a = q[j ^ (lane & 7)];
-        v[4 * j + 0] = __float_as_uint(__uint_as_float(v[4 * j + 0]) + a.x);
-        v[4 * j + 1] = __float_as_uint(__uint_as_float(v[4 * j + 1]) + a.y);
-        v[4 * j + 2] = __float_as_uint(__uint_as_float(v[4 * j + 2]) + a.z);
-        v[4 * j + 3] = __float_as_uint(__uint_as_float(v[4 * j + 3]) + a.w);
+        const uint4 a = ep[lane * 8 + (j ^ (lane & 7))];
+        v[4 * j + 0] = __float_as_uint(__uint_as_float(v[4 * j + 0]) + __uint_as_float(a.x));
+        v[4 * j + 1] = __float_as_uint(__uint_as_float(v[4 * j + 1]) + __uint_as_float(a.y));
+        v[4 * j + 2] = __float_as_uint(__uint_as_float(v[4 * j + 2]) + __uint_as_float(a.z));
+        v[4 * j + 3] = __float_as_uint(__uint_as_float(v[4 * j + 3]) + __uint_as_float(a.w));
     }
 }
 
@@ -375,8 +322,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t rank = CG == 2 ? cluster_rank() : 0;
     const bool leader = rank == 0;
     const int gid = blockIdx.x / CG, G = gridDim.x / CG;
-    const long total = long(num_tiles) * num_kb;
-    const SkRange rg = sk_range(gid, G, total);
+    // stream-K super-group size (mode 3: one member per M-tile; else 1)
+    const int P = sk_mode == 3 ? num_mt : 1;
+    const long total = long(num_tiles / P) * num_kb;
+    const SkRange rg = sk_range(gid / P, G / P, total);
     if (threadIdx.x == 0) TRACE(0);
 
     if (threadIdx.x == 0) {
@@ -400,34 +349,64 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     pdl_launch_dependents();
-    pdl_wait();  // A (activations) and the residual come from the preceding kernels
-    if (threadIdx.x == 0) TRACE(1);
+    // Programmatic dependent launch: A (activations) and the residual come from the
+    // preceding kernels, so the producer and the epilogue warps wait for them; the
+    // MMA warp only consumes shared memory and needs no wait.
 
     if (warp == 0) {
         if (lane == 0) {  // ---------------- TMA producer (both CTAs)
             const uint32_t full_leader = CG == 2 ? peer_addr(full, 0) : 0;
-            int s = 0;
+            // The weights (B) do not depend on the preceding kernels: the first
+            // stages' B tiles are requested before the grid-dependency wait, so
+            // their HBM latency overlaps the previous kernel's tail.
+            int npre = 0;
+            {
+                SegIter pit(sk_mode, gid, G, num_kb, num_tiles, rg, sk_slices, P);
+                Seg sg;
+                if (pit.next(sg)) {
+                    const int n0 = (sg.t / num_mt) * BN + Cfg::B_ROWS * int(rank);
+                    npre = sg.kb1 - sg.kb0 < STAGES ? sg.kb1 - sg.kb0 : STAGES;
+                    for (int j = 0; j < npre; ++j) {
+                        const int kb = sg.kb0 + j;
+                        if constexpr (CG == 1) {
+                            mbar_arrive_expect_tx(&full[j], Cfg::STAGE_BYTES);
+                            tma_load_2d(sB + j * Cfg::B_BYTES, &tmB, kb * BK, n0, &full[j]);
+                        } else {
+                            if (leader) mbar_arrive_expect_tx(&full[j], 2 * Cfg::STAGE_BYTES);
+                            tma_load_2d_cg2(sB + j * Cfg::B_BYTES, &tmB, kb * BK, n0, full_leader + uint32_t(j * 8));
+                        }
+                    }
+                }
+            }
+            pdl_wait();
+            TRACE(1);
+            int s = 0, it = 0;
             uint32_t ph = 0;
-            SegIter sit(sk_mode, gid, G, num_kb, num_tiles, rg, sk_slices);
+            SegIter sit(sk_mode, gid, G, num_kb, num_tiles, rg, sk_slices, P);
             for (Seg sg; sit.next(sg);) {
                 const int t = sg.t, kb0 = sg.kb0, kb1 = sg.kb1;
                 const int m0 = (t % num_mt) * Cfg::TILE_M + 128 * int(rank);
                 const int n0 = (t / num_mt) * BN + Cfg::B_ROWS * int(rank);
-                for (int kb = kb0; kb < kb1; ++kb) {
-                    mbar_wait(&empty[s], ph ^ 1);
+                for (int kb = kb0; kb < kb1; ++kb, ++it) {
+                    const bool pre = it < npre;  // B already in flight, slot fresh
+                    if (!pre) mbar_wait(&empty[s], ph ^ 1);
 #if defined(SS_GEMM_EXP) && SS_GEMM_EXP == 1  // dev experiment: no loads (MMA on stale smem)
                     if (leader) mbar_arrive(&full[s]);
                     if (false)
 #endif
                     if constexpr (CG == 1) {
-                        mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
+                        if (!pre) {
+                            mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
+                            tma_load_2d(sB + s * Cfg::B_BYTES, &tmB, kb * BK, n0, &full[s]);
+                        }
                         tma_load_2d(sA + s * Cfg::A_BYTES, &tmA, kb * BK, m0, &full[s]);
-                        tma_load_2d(sB + s * Cfg::B_BYTES, &tmB, kb * BK, n0, &full[s]);
                     } else {
-                        if (leader) mbar_arrive_expect_tx(&full[s], 2 * Cfg::STAGE_BYTES);
                         const uint32_t fb = full_leader + uint32_t(s * 8);
+                        if (!pre) {
+                            if (leader) mbar_arrive_expect_tx(&full[s], 2 * Cfg::STAGE_BYTES);
+                            tma_load_2d_cg2(sB + s * Cfg::B_BYTES, &tmB, kb * BK, n0, fb);
+                        }
                         tma_load_2d_cg2(sA + s * Cfg::A_BYTES, &tmA, kb * BK, m0, fb);
-                        tma_load_2d_cg2(sB + s * Cfg::B_BYTES, &tmB, kb * BK, n0, fb);
                     }
                     if (++s == STAGES) {
                         s = 0;
@@ -449,7 +428,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t ph = 0;
             int acc = 0;
             uint32_t acc_ph = 0;
-            SegIter sit(sk_mode, gid, G, num_kb, num_tiles, rg, sk_slices);
+            SegIter sit(sk_mode, gid, G, num_kb, num_tiles, rg, sk_slices, P);
 #ifdef SS_GEMM_TRACE
             int seg_no = 0;
 #endif
@@ -495,48 +474,83 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else {  // ---------------------------- epilogue warps 2..9
+        pdl_wait();
         // two warps per TMEM lane quarter (warp % 4 selects the quarter), splitting
         // the tile's 32-column chunks (pairs for SwiGLU) between them
         const int q = warp & 3;
         const int ew = warp - 2, half = ew >> 2;
         const uint32_t tempty_leader = CG == 2 ? peer_addr(tempty, 0) : 0;
         const int rloc = 128 * int(rank) + q * 32 + lane;  // row within the group's tile
+        // Stores leave through a per-warp 4 KB staging buffer: the accumulator arrives
+        // one row per thread (tcgen05.ld 32x32b), is written to smem as 32 rows x 128 B
+        // (16-byte chunks XOR-swizzled by row: conflict-free both ways) and read back
+        // warp-coalesced (lane l of step j: row 4j + l/8, chunk l%8), so every global
+        // access covers whole 32-byte sectors of few lines instead of one 16-byte
+        // piece of 32 different lines.
+        uint4* ep = reinterpret_cast<uint4*>(smem + STAGES * Cfg::STAGE_BYTES + 1024 + ew * 4096);
+        const int crow = lane >> 3, cch = lane & 7;  // coalesced layout: row-in-step, chunk
         int acc = 0;
         uint32_t acc_ph = 0, eph = 0;
-        SegIter sit(sk_mode, gid, G, num_kb, num_tiles, rg, sk_slices);
+        SegIter sit(sk_mode, gid, G, num_kb, num_tiles, rg, sk_slices, P);
         for (Seg sg; sit.next(sg);) {
             const int t = sg.t, kb0 = sg.kb0, kb1 = sg.kb1;
             const int m0 = (t % num_mt) * Cfg::TILE_M, n0 = (t / num_mt) * BN;
             const int row = m0 + rloc;
+            const int rbase = row - lane;  // first row of this warp
             // RMSNorm of the A row, folded in: scale = rsqrt(mean(x^2) + eps). The
             // sums of squares come from the previous kernel, so this overlaps the
-            // tile's main loop (computed before waiting for the accumulator).
+            // tile's main loop (computed before waiting for the accumulator). Loads are
+            // coalesced (lane l takes float4 l, l + 32, ... of each of the warp's rows);
+            // a 31-shuffle transpose-reduce leaves row `lane`'s total in lane `lane`.
             float rs = 1.f;
-            if (ea.ssq_in && row < M) {
-                const float4* q4 = reinterpret_cast<const float4*>(ea.ssq_in + size_t(row) * ea.ssq_in_n);
-                float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-#pragma unroll 8
-                for (int i = 0; i < ea.ssq_in_n / 4; ++i) {
-                    const float4 w = __ldg(q4 + i);
-                    a0 += w.x;
-                    a1 += w.y;
-                    a2 += w.z;
-                    a3 += w.w;
+            if (ea.ssq_in && kb0 == 0) {
+                const int n4 = ea.ssq_in_n >> 2;
+                float a[32];
+#pragma unroll
+                for (int r = 0; r < 32; ++r) a[r] = 0.f;
+                for (int i = lane; i - lane < n4; i += 32) {  // warp-uniform trip count
+                    // 32 independent loads in flight per step (one per row)
+#pragma unroll
+                    for (int r = 0; r < 32; ++r) {
+                        if (i < n4 && rbase + r < M) {
+                            const float4 w = __ldg(reinterpret_cast<const float4*>(ea.ssq_in + size_t(rbase + r) * ea.ssq_in_n) + i);
+                            a[r] += (w.x + w.y) + (w.z + w.w);
+                        }
+                    }
                 }
-                rs = rsqrtf(((a0 + a1) + (a2 + a3)) * ea.inv_dim + ea.eps);
+#pragma unroll
+                for (int off = 16; off >= 1; off >>= 1) {
+                    const bool up = lane & off;
+#pragma unroll
+                    for (int i = 0; i < off; ++i) {
+                        const float send = up ? a[i] : a[i + off];
+                        const float keep = up ? a[i + off] : a[i];
+                        a[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+                    }
+                }
+                rs = rsqrtf(a[0] * ea.inv_dim + ea.eps);
             }
-            // residual rows of this warp's first two chunks, loaded while the MMAs run
+            // residual of this warp's first two chunks (coalesced layout), loaded
+            // while the MMAs run
             float4 xin[2][8];
             if constexpr (EPI == EPI_RESADD) {
-                if (kb0 == 0 && row < M) {
+                if (kb0 == 0) {
+                    // the later chunks' residual lines (this lane's row) go to L2 now
+                    for (int c2 = half + 4; c2 < BN / 32; c2 += 2)
+                        if (row < M && n0 + c2 * 32 < N)
+                            asm volatile("prefetch.global.L2 [%0];" ::"l"(static_cast<const float*>(out) +
+                                                                         size_t(row) * ldo + n0 + c2 * 32));
 #pragma unroll
                     for (int i = 0; i < 2; ++i) {
-                        const int col = n0 + (half + 2 * i) * 32;
+                        const int col = n0 + (half + 2 * i) * 32 + cch * 4;
                         if (half + 2 * i < BN / 32 && col < N) {
-                            const float4* src = reinterpret_cast<const float4*>(static_cast<const float*>(out) +
-                                                                                size_t(row) * ldo + col);
 #pragma unroll
-                            for (int j = 0; j < 8; ++j) xin[i][j] = src[j];
+                            for (int j = 0; j < 8; ++j) {
+                                const int r = rbase + 4 * j + crow;
+                                if (r < M)
+                                    xin[i][j] = *reinterpret_cast<const float4*>(static_cast<const float*>(out) +
+                                                                                 size_t(r) * ldo + col);
+                            }
                         }
                     }
                 }
@@ -545,7 +559,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             // chunk pair, also fetched while the MMAs run (a dependent load chain)
             int q_pos = 0;
             int64_t q_slot = 0;
-            float2 rc[32];
+            float4 rc[16];
             if constexpr (EPI == EPI_QKV) {
                 if (kb0 == 0 && row < M) {
                     q_pos = ea.pos[row];
@@ -555,9 +569,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const int c = (half / ps) * (2 * ps) + (half % ps);
                         const int col = n0 + c * 32;
                         if (col < N && col / ea.hd < ea.nq + ea.nkv) {
-                            const float2* cs = ea.rope + size_t(q_pos) * (ea.hd / 2) + col % ea.hd;
+                            const float4* cs = reinterpret_cast<const float4*>(ea.rope + size_t(q_pos) * (ea.hd / 2) + col % ea.hd);
 #pragma unroll
-                            for (int j = 0; j < 32; ++j) rc[j] = cs[j];
+                            for (int j = 0; j < 16; ++j) rc[j] = __ldg(cs + j);
                         }
                     }
                 }
@@ -600,18 +614,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                 __syncwarp();
                 TRACE2(3);
             } else if (kb0 > 0) {
-                // non-head piece of a split tile: publish the partial accumulator
-                float* dst = part + (size_t(gid) * CG + rank) * (128 * BN) + (q * 32 + lane) * 32;
+                // non-head piece of a split tile: publish the partial accumulator (the
+                // swizzled staging image, copied out linearly: coalesced 512 B per step)
+                uint4* dst = reinterpret_cast<uint4*>(part + (size_t(gid) * CG + rank) * (128 * BN) + (q * 32) * 32);
 #pragma unroll 1
                 for (int c = half; c < BN / 32; c += 2) {
                     uint32_t v[32];
                     tmem_ld32(t_row + uint32_t(c * 32), v);
                     tmem_wait_ld();
-                    float4* d4 = reinterpret_cast<float4*>(dst + size_t(c) * 128 * 32);
+                    stage_rows(ep, v, lane);
+                    __syncwarp();
+                    uint4* d = dst + size_t(c) * 128 * 8;
 #pragma unroll
-                    for (int j = 0; j < 8; ++j)
-                        d4[j ^ (lane & 7)] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
-                                            __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+                    for (int j = 0; j < 8; ++j) d[j * 32 + lane] = ep[j * 32 + lane];
+                    __syncwarp();
                 }
                 __threadfence();
                 __syncwarp();
@@ -619,14 +635,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                 TRACE2(3);
             } else {
                 // head or whole tile: add the other groups' pieces in group order
-                const long tile_end = long(t + 1) * num_kb;
+                // (groups gid + P, gid + 2P, ... hold them: the same member of the
+                // following super-groups)
                 int g_last = gid;  // last group holding a piece of this tile
                 if (kb1 < num_kb) {
-                    if (sk_mode == 2) g_last = gid + sk_slices - 1;
-                    else
-                        while (g_last + 1 < G && sk_start(g_last + 1, G, total) < tile_end) ++g_last;
+                    if (sk_mode == 2) {
+                        g_last = gid + sk_slices - 1;
+                    } else {
+                        const long tile_end = long(t / P + 1) * num_kb;
+                        const int Gs = G / P;
+                        int s_last = gid / P;
+                        while (s_last + 1 < Gs && sk_start(s_last + 1, Gs, total) < tile_end) ++s_last;
+                        g_last = s_last * P + gid % P;
+                    }
                 }
-                for (int g = gid + 1; g <= g_last; ++g) {
+                for (int g = gid + P; g <= g_last; g += P) {
                     const uint32_t* f = &flags[(size_t(g) * 2 + rank) * 8 + ew];
                     uint32_t spins = 0;
                     while (ld_acquire_gpu(f) != epoch)
@@ -637,7 +660,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     // ring idle: bulk-load each piece's chunks (fixed group order) and
                     // accumulate into TMEM; the epilogue below then reads final sums
                     const int nmine = (BN / 32 - half + 1) / 2;
-                    for (int g = gid + 1; g <= g_last; ++g) {
+                    for (int g = gid + P; g <= g_last; g += P) {
                         if (lane == 0) {
                             fence_proxy_async_global();
                             const float* base = part + (size_t(g) * CG + rank) * (128 * BN);
@@ -647,6 +670,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 bulk_load(stg + i * 1024, base + (size_t(c) * 128 + q * 32) * 32, 4096, &ebar[ew]);
                         }
                         mbar_wait(&ebar[ew], eph);
+                        if (g == gid + P) TRACE2(4);
                         eph ^= 1;
                         int i = 0;
 #pragma unroll 1
@@ -669,18 +693,30 @@ __global__ void __launch_bounds__(kThreads, 1)
                         __syncwarp();  // every lane done with stg before the next piece lands
                     }
                     // the two warps of this TMEM quarter swap chunk sets in the epilogue
+                    TRACE2(5);
                     tc_fence_before();
                     named_bar(1 + q, 64);
                     tc_fence_after();
+                    TRACE2(6);
                     g_last = gid;
                 }
+                // pieces of other groups not staged above (tile not in the last segment):
+                // coalesced copy of each piece's chunk into ep, then added per row
+                auto add_pieces = [&](uint32_t (&v)[32], int c) {
+                    for (int g = gid + P; g <= g_last; g += P) {
+                        const uint4* src = reinterpret_cast<const uint4*>(part + (size_t(g) * CG + rank) * (128 * BN) +
+                                                                          (size_t(c) * 128 + q * 32) * 32);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) ep[j * 32 + lane] = __ldcg(src + j * 32 + lane);
+                        __syncwarp();
+                        add_rows(v, ep, lane);
+                        __syncwarp();
+                    }
+                };
                 if constexpr (EPI == EPI_QKV) {
                     // chunk pairs (c, c + ps) hold the rotate-half partners i, i + hd/2 of one head
                     const int ps = ea.hd / 64;
-                    const int row_ok = row < M;
-                    const int p_row = q_pos;
-                    const int64_t s_row = q_slot;
-                    const int64_t blk = s_row / ea.bs, off = s_row % ea.bs;
+                    const int64_t blk = q_slot / ea.bs, off = q_slot % ea.bs;
 #pragma unroll 1
                     for (int pi = half; pi < (BN / ea.hd) * ps; pi += 2) {
                         const int c = (pi / ps) * (2 * ps) + (pi % ps);
@@ -688,25 +724,23 @@ __global__ void __launch_bounds__(kThreads, 1)
                         tmem_ld32(t_row + uint32_t(c * 32), x1);
                         tmem_ld32(t_row + uint32_t((c + ps) * 32), x2);
                         tmem_wait_ld();
-                        for (int g = gid + 1; g <= g_last; ++g) {
-                            const float* src = part + (size_t(g) * CG + rank) * (128 * BN) + (q * 32 + lane) * 32;
-                            add_partial(x1, src + size_t(c) * 4096, lane);
-                            add_partial(x2, src + size_t(c + ps) * 4096, lane);
-                        }
+                        add_pieces(x1, c);
+                        add_pieces(x2, c + ps);
                         const int col = n0 + c * 32;
-                        if (!row_ok || col >= N) continue;
+                        if (col >= N) continue;  // warp-uniform
                         const int hh = col / ea.hd, i0 = col % ea.hd;  // i0 < hd/2
+                        // this row's packed bf16 result: lo = columns i0.., hi = i0 + hd/2..
                         uint32_t lo[16], hi[16];
                         if (hh < ea.nq + ea.nkv) {  // q or k head: rotate
-                            const float2* cs = ea.rope + size_t(p_row) * (ea.hd / 2) + i0;
+                            const float4* cs = reinterpret_cast<const float4*>(ea.rope + size_t(q_pos) * (ea.hd / 2) + i0);
+                            const bool pre = pi == half;  // factors preloaded before the wait
 #pragma unroll
                             for (int j = 0; j < 16; ++j) {
-                                const bool pre = pi == half;  // factors preloaded before the wait
-                                const float2 c0 = pre ? rc[2 * j] : cs[2 * j], c1 = pre ? rc[2 * j + 1] : cs[2 * j + 1];
+                                const float4 f = pre ? rc[j] : (row < M ? __ldg(cs + j) : make_float4(0.f, 0.f, 0.f, 0.f));
                                 const float a0 = __uint_as_float(x1[2 * j]) * rs, a1 = __uint_as_float(x1[2 * j + 1]) * rs;
                                 const float b0 = __uint_as_float(x2[2 * j]) * rs, b1 = __uint_as_float(x2[2 * j + 1]) * rs;
-                                lo[j] = pack_bf16(a0 * c0.x - b0 * c0.y, a1 * c1.x - b1 * c1.y);
-                                hi[j] = pack_bf16(b0 * c0.x + a0 * c0.y, b1 * c1.x + a1 * c1.y);
+                                lo[j] = pack_bf16(a0 * f.x - b0 * f.y, a1 * f.z - b1 * f.w);
+                                hi[j] = pack_bf16(b0 * f.x + a0 * f.y, b1 * f.z + a1 * f.w);
                             }
                         } else {
 #pragma unroll
@@ -715,69 +749,129 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 hi[j] = pack_bf16(__uint_as_float(x2[2 * j]) * rs, __uint_as_float(x2[2 * j + 1]) * rs);
                             }
                         }
-                        __nv_bfloat16* dst;
-                        if (hh < ea.nq) dst = ea.q_out + (size_t(row) * ea.nq + hh) * ea.hd;
-                        else if (hh < ea.nq + ea.nkv) dst = ea.kc + ((size_t(blk) * ea.nkv + (hh - ea.nq)) * ea.bs + off) * ea.hd;
-                        else dst = ea.vc + ((size_t(blk) * ea.nkv + (hh - ea.nq - ea.nkv)) * ea.bs + off) * ea.hd;
-                        uint4* d1 = reinterpret_cast<uint4*>(dst + i0);
-                        uint4* d2 = reinterpret_cast<uint4*>(dst + i0 + ea.hd / 2);
+                        __nv_bfloat16* dst = nullptr;
+                        if (row < M) {
+                            if (hh < ea.nq) dst = ea.q_out + (size_t(row) * ea.nq + hh) * ea.hd;
+                            else if (hh < ea.nq + ea.nkv) dst = ea.kc + ((size_t(blk) * ea.nkv + (hh - ea.nq)) * ea.bs + off) * ea.hd;
+                            else dst = ea.vc + ((size_t(blk) * ea.nkv + (hh - ea.nq - ea.nkv)) * ea.bs + off) * ea.hd;
+                            dst += i0;
+                        }
+                        // staged row = [lo 64 B | hi 64 B]; chunk k < 4 -> dst + 8k, else dst + hd/2 + 8(k-4)
 #pragma unroll
                         for (int j = 0; j < 4; ++j) {
-                            d1[j] = make_uint4(lo[4 * j], lo[4 * j + 1], lo[4 * j + 2], lo[4 * j + 3]);
-                            d2[j] = make_uint4(hi[4 * j], hi[4 * j + 1], hi[4 * j + 2], hi[4 * j + 3]);
+                            ep[lane * 8 + (j ^ (lane & 7))] = make_uint4(lo[4 * j], lo[4 * j + 1], lo[4 * j + 2], lo[4 * j + 3]);
+                            ep[lane * 8 + ((j + 4) ^ (lane & 7))] = make_uint4(hi[4 * j], hi[4 * j + 1], hi[4 * j + 2], hi[4 * j + 3]);
                         }
-                    }
-                } else if constexpr (EPI == EPI_SWIGLU) {
-#pragma unroll 1
-                    for (int c = 2 * half; c < BN / 32; c += 4) {
-                        uint32_t gt[32], ut[32];
-                        tmem_ld32(t_row + uint32_t(c * 32), gt);
-                        tmem_ld32(t_row + uint32_t((c + 1) * 32), ut);
-                        tmem_wait_ld();
-                        for (int g = gid + 1; g <= g_last; ++g) {
-                            const float* src = part + (size_t(g) * CG + rank) * (128 * BN) + (q * 32 + lane) * 32;
-                            add_partial(gt, src + size_t(c) * 4096, lane);
-                            add_partial(ut, src + size_t(c + 1) * 4096, lane);
-                        }
-                        const int col = n0 + c * 32;
-                        if (row < M && col < N) {
-                            __nv_bfloat16* o = static_cast<__nv_bfloat16*>(out) + size_t(row) * ldo + col / 2;
-                            uint32_t pk[16];
+                        __syncwarp();
+                        const uint64_t dp = reinterpret_cast<uint64_t>(dst);
 #pragma unroll
-                            for (int j = 0; j < 16; ++j)
-                                pk[j] = pack_bf16(
-                                    silu(__uint_as_float(gt[2 * j]) * rs) * (__uint_as_float(ut[2 * j]) * rs),
-                                    silu(__uint_as_float(gt[2 * j + 1]) * rs) * (__uint_as_float(ut[2 * j + 1]) * rs));
-#pragma unroll
-                            for (int j = 0; j < 4; ++j)
-                                reinterpret_cast<uint4*>(o)[j] =
-                                    make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+                        for (int j = 0; j < 8; ++j) {
+                            const int r = 4 * j + crow;
+                            const uint64_t d = (uint64_t(__shfl_sync(0xffffffffu, uint32_t(dp >> 32), r)) << 32) |
+                                               __shfl_sync(0xffffffffu, uint32_t(dp), r);
+                            if (d) {
+                                __nv_bfloat16* p = reinterpret_cast<__nv_bfloat16*>(d) + (cch < 4 ? cch * 8 : ea.hd / 2 + (cch - 4) * 8);
+                                *reinterpret_cast<uint4*>(p) = ep[r * 8 + (cch ^ (r & 7))];
+                            }
                         }
+                        __syncwarp();
                     }
                 } else {
+                    // chunks of this warp: c = half, half + 2, ... (SwiGLU: gate/up pairs
+                    // (c, c + 1) with c = 2 * half, 2 * half + 4, ...)
+                    constexpr int kStep = EPI == EPI_SWIGLU ? 4 : 2;
 #pragma unroll
-                    for (int i = 0; i < (BN / 32 + 1) / 2; ++i) {  // unrolled: xin stays in registers
-                        const int c = half + 2 * i;
+                    for (int i = 0; i < (BN / 32 + kStep - 1) / kStep; ++i) {  // unrolled: xin stays in registers
+                        const int c = (EPI == EPI_SWIGLU ? 2 * half : half) + kStep * i;
                         if (c >= BN / 32) break;
                         uint32_t v[32];
-                        tmem_ld32(t_row + uint32_t(c * 32), v);
-                        tmem_wait_ld();
-                        for (int g = gid + 1; g <= g_last; ++g)
-                            add_partial(v, part + (size_t(g) * CG + rank) * (128 * BN) + size_t(c) * 4096 + (q * 32 + lane) * 32, lane);
-                        if (ea.ssq_in) {
+                        if constexpr (EPI == EPI_SWIGLU) {
+                            uint32_t ut[32];
+                            tmem_ld32(t_row + uint32_t(c * 32), v);
+                            tmem_ld32(t_row + uint32_t((c + 1) * 32), ut);
+                            tmem_wait_ld();
+                            add_pieces(v, c);
+                            add_pieces(ut, c + 1);
 #pragma unroll
-                            for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) * rs);
+                            for (int j = 0; j < 32; ++j)
+                                v[j] = __float_as_uint(silu(__uint_as_float(v[j]) * rs) * (__uint_as_float(ut[j]) * rs));
+                        } else {
+                            tmem_ld32(t_row + uint32_t(c * 32), v);
+                            tmem_wait_ld();
+                            if (i == 0) TRACE2(7);
+                            add_pieces(v, c);
+                            if (ea.ssq_in) {
+#pragma unroll
+                                for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) * rs);
+                            }
                         }
+                        stage_rows(ep, v, lane);
+                        __syncwarp();
+                        if (i == 0) TRACE2(8);
                         const int col = n0 + c * 32;
-                        if (row < M && col < N) {
-                            if constexpr (EPI == EPI_RESADD) {
-                                if (i < 2) {
-                                    epi_resadd(v, row, col, out, ldo, ea, xin[i < 2 ? i : 0]);
-                                    continue;
+                        if (col < N) {  // warp-uniform
+                            const int ccol = (EPI == EPI_SWIGLU ? col / 2 : col) + cch * 4;
+                            float ss[8];
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) {
+                                const int r = 4 * j + crow, grow = rbase + r;
+                                const uint4 u = ep[r * 8 + (cch ^ (r & 7))];
+                                float4 d = make_float4(__uint_as_float(u.x), __uint_as_float(u.y), __uint_as_float(u.z),
+                                                       __uint_as_float(u.w));
+                                if constexpr (EPI == EPI_RESADD) {
+                                    const float4 x0 = xin[i & 1][j];
+                                    d.x += x0.x;
+                                    d.y += x0.y;
+                                    d.z += x0.z;
+                                    d.w += x0.w;
+                                    ss[j] = d.x * d.x + d.y * d.y + d.z * d.z + d.w * d.w;
+                                    if (grow < M) {
+                                        *reinterpret_cast<float4*>(static_cast<float*>(out) + size_t(grow) * ldo + ccol) = d;
+                                        if (ea.xb_out)
+                                            *reinterpret_cast<uint2*>(ea.xb_out + size_t(grow) * ldo + ccol) =
+                                                make_uint2(pack_bf16(d.x, d.y), pack_bf16(d.z, d.w));
+                                    }
+                                } else if (grow < M) {
+                                    if constexpr (EPI == EPI_F32) {
+                                        *reinterpret_cast<float4*>(static_cast<float*>(out) + size_t(grow) * ldo + ccol) = d;
+                                    } else {  // EPI_BF16, EPI_SWIGLU
+                                        *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(out) + size_t(grow) * ldo + ccol) =
+                                            make_uint2(pack_bf16(d.x, d.y), pack_bf16(d.z, d.w));
+                                    }
                                 }
                             }
-                            epi_store<EPI>(v, row, col, out, ldo, ea);
+                            if (i == 0) TRACE2(9);
+                            if constexpr (EPI == EPI_RESADD) {
+                                if (ea.xb_out) {
+                                    // per-(row, 32-column chunk) sums of squares: each row's 8 lanes
+                                    // reduce in a fixed butterfly order, the 8 rows' chains interleaved
+#pragma unroll
+                                    for (int m = 1; m <= 4; m <<= 1)
+#pragma unroll
+                                        for (int j = 0; j < 8; ++j) ss[j] += __shfl_xor_sync(0xffffffffu, ss[j], m);
+                                    if (cch == 0) {
+#pragma unroll
+                                        for (int j = 0; j < 8; ++j) {
+                                            const int grow = rbase + 4 * j + crow;
+                                            if (grow < M) ea.ssq_out[size_t(grow) * (ldo / 32) + col / 32] = ss[j];
+                                        }
+                                    }
+                                }
+                                if (i < 4) TRACE2(10 + i);
+                                // refill the used residual slot with chunk i + 2's (overlaps chunk i + 1)
+                                const int col2 = col + 4 * 32 + cch * 4;
+                                if (c + 4 < BN / 32 && col2 < N) {
+#pragma unroll
+                                    for (int j = 0; j < 8; ++j) {
+                                        const int r = rbase + 4 * j + crow;
+                                        if (r < M)
+                                            xin[i & 1][j] = *reinterpret_cast<const float4*>(static_cast<const float*>(out) +
+                                                                                             size_t(r) * ldo + col2);
+                                    }
+                                }
+                            }
                         }
+                        __syncwarp();
                     }
                 }
             }
@@ -841,7 +935,7 @@ cudaError_t launch_t(const GemmPlan& p, cudaStream_t st) {
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].val.programmaticStreamSerializationAllowed = pdl_allowed();
     cfg.attrs = attr;
     cfg.numAttrs = 2;
     // Groups that can be co-resident: stream-K heads spin on other groups, so the
@@ -858,6 +952,7 @@ cudaError_t launch_t(const GemmPlan& p, cudaStream_t st) {
     if (mode < 0) mode = S > 1 ? 2 : 0;
     if (const char* f = getenv("SS_GEMM_SK")) mode = atoi(f);
     if (const char* f = getenv("SS_GEMM_SPLITS")) S = atoi(f);
+    if (mode == 3 && (CG != 2 || num_mt > resident)) mode = 0;
     const int rem = tiles % resident;  // tiles of the ragged last wave
     if (mode == 2 && rem > 0 && long(rem) * S > resident) S = resident / rem;
     if (mode == 2 && (S < 2 || rem == 0)) mode = 0;  // nothing to split
@@ -865,6 +960,11 @@ cudaError_t launch_t(const GemmPlan& p, cudaStream_t st) {
     if (mode == 0 && tiles < groups) groups = tiles;
     if (mode == 1 && iters < groups) groups = int(iters);
     if (mode == 2 && tiles < resident) groups = tiles * S;
+    if (mode == 3) {  // whole super-groups (one member per M-tile), each with >= 1 k-block
+        long gs = resident / num_mt;
+        if (gs > long(num_n) * ((p.K + BK - 1) / BK)) gs = long(num_n) * ((p.K + BK - 1) / BK);
+        groups = int(gs) * num_mt;
+    }
     cfg.gridDim = dim3(CG * groups);
     if (getenv("SS_GEMM_DEBUG"))
         fprintf(stderr, "gemm cg=%d bn=%d epi=%d M=%d N=%d K=%d tiles=%d resident=%d mode=%d groups=%d\n", CG, BN,
@@ -896,18 +996,22 @@ GemmShape gemm_pick(int M, int N, int K, int epi, int num_sms) {
     if (const char* f = getenv("SS_GEMM_BN")) force_bn = atoi(f);  // tuning overrides (dev only)
     if (const char* f = getenv("SS_GEMM_CG")) force_cg = atoi(f);
     if (const char* f = getenv("SS_GEMM_SPLITS")) force_s = atoi(f);
+    int force_mode = -1;
+    if (const char* f = getenv("SS_GEMM_SK")) force_mode = atoi(f);
     const bool swiglu = epi == EPI_SWIGLU;
-    GemmShape best{M > 128 ? 2 : 1, swiglu ? 256 : 128, 1};
+    GemmShape best{M > 128 ? 2 : 1, swiglu ? 256 : 128, 1, -1};
     double best_cost = 1e30;
-    // Measured per-tile main-loop time (us per 64 k-blocks, B200,
-    // profiles/r01/gemm_tiles.txt): at these M the loop is bound by the L2 -> SM
-    // fill rate rather than the MMA pipe, so narrow tiles save less than their
-    // MMA share. Whole tiles go round-robin (groups stay in K-lockstep, sharing
-    // A k-blocks in L2); when one wave leaves groups idle, K is split into S
-    // aligned slices that still run in lockstep (mode 2), at a fixup cost.
+    // Cost model calibrated inside the Mistral forward (profiles/r01/gemm_class_sweep.txt,
+    // scripts/gemm_class_sweep.py): per 64 k-blocks a CTA-pair tile's main loop takes
+    // ~15 + 0.0135 * BN us in K-lockstep (L2 -> SM fill bound, so narrow tiles save
+    // little), 1.18x that in M-lockstep stream-K (the groups no longer share A
+    // k-blocks in L2); every launch pays ~3 + 0.07 * BN us of start-up and exposed
+    // last epilogue, stream-K ~6 us more (partial write + fixup of split tiles).
+    // Whole tiles go round-robin (mode 0); a ragged last wave can be split in K
+    // (mode 2); mode 3 balances every group exactly.
     auto tile_us = [](int c, int b) {
         if (c == 1) return b == 256 ? 28.6 : 20.4;
-        return b >= 224 ? 25.3 : (b >= 192 ? 23.2 : (b >= 160 ? 22.1 : (b >= 128 ? 21.1 : 20.0)));
+        return 15.0 + 0.0135 * b;
     };
     const double kscale = double((K + BK - 1) / BK) / 64.0;
     auto consider = [&](int cg, int bn) {
@@ -915,21 +1019,29 @@ GemmShape gemm_pick(int M, int N, int K, int epi, int num_sms) {
         if (epi == EPI_QKV && bn % 128) return;  // whole heads per tile (hd 64 or 128)
         if (force_bn && bn != force_bn) return;
         if (force_cg && cg != force_cg) return;
-        const long tiles = long((M + 128 * cg - 1) / (128 * cg)) * ((N + bn - 1) / bn);
+        const long num_mt = (M + 128 * cg - 1) / (128 * cg), num_n = (N + bn - 1) / bn;
+        const long tiles = num_mt * num_n;
         const long slots = num_sms / cg;
         const long full = tiles / slots, rem = tiles % slots;
+        const double t1 = tile_us(cg, bn) * kscale, epi_us = 3.0 + 0.07 * bn;
+        if (cg == 2 && num_mt <= slots && (force_mode < 0 || force_mode == 3)) {
+            const long gs = slots / num_mt, nkb = (K + BK - 1) / BK;
+            const long per = (num_n * nkb + gs - 1) / gs;
+            const double cost = double(per) / 64.0 * 1.18 * tile_us(cg, bn) + epi_us + 6.0;
+            if (cost < best_cost - 1e-9) {
+                best_cost = cost;
+                best = GemmShape{cg, bn, 1, 3};
+            }
+        }
+        if (force_mode == 3) return;
         for (int S = 1; S <= 4; ++S) {
             if (force_s && S != force_s) continue;
             if (S > 1 && (rem == 0 || rem * S > slots)) break;
-            // whole-tile waves + the ragged last wave, its tiles split S ways in K;
-            // + exposed epilogue (~6 us at the end); split-K adds the partial write
-            // and fixup read of a 256-wide fp32 tile (measured ~2.5x that)
-            const double t1 = tile_us(cg, bn) * kscale;
-            const double last = rem == 0 ? 0.0 : t1 / S + (S > 1 ? 3.5 * 6.0 : 0.0);
-            const double cost = double(full) * t1 + last + 6.0;
+            const double last = rem == 0 ? 0.0 : t1 / S + (S > 1 ? 8.0 + 2.0 * S : 0.0);
+            const double cost = double(full) * t1 + last + epi_us;
             if (cost < best_cost - 1e-9) {
                 best_cost = cost;
-                best = GemmShape{cg, bn, S};
+                best = GemmShape{cg, bn, S, S > 1 ? 2 : 0};
             }
         }
     };
@@ -956,6 +1068,7 @@ bool gemm_prepare(GemmPlan& p, const void* A, uint64_t a_rows, const void* B, in
     p.cg = s.cg;
     p.bn = bn ? bn : s.bn;
     p.splits = s.splits;
+    p.sk_mode = s.mode;
     if (!make_tmap_2d(&p.tmA, A, a_rows, uint64_t(K), 128, BK)) return false;
     if (!make_tmap_2d(&p.tmB, B, uint64_t(N), uint64_t(K), uint32_t(p.bn / p.cg), BK)) return false;
     return true;
@@ -988,16 +1101,20 @@ cudaError_t gemm_launch(const GemmPlan& p, cudaStream_t st) {
 #ifdef SS_GEMM_TRACE
 extern "C" __attribute__((visibility("default"))) int ss_debug_gemm_trace(unsigned long long* out, int n) {
     if (cudaDeviceSynchronize() != cudaSuccess) return -1;
+    if (n <= -2) {  // select the traced epilogue: -2 all, -3 - epi only that epilogue
+        const int e = n == -2 ? -1 : -3 - n;
+        return cudaMemcpyToSymbol(ssk::g_trace_epi, &e, sizeof(int)) == cudaSuccess ? 0 : -1;
+    }
     if (n < 0) {  // clear both tables
-        static unsigned long long zeros[1024 * 8] = {};
+        static unsigned long long zeros[1024 * 16] = {};
         return cudaMemcpyToSymbol(ssk::g_gemm_trace, zeros, sizeof(zeros)) == cudaSuccess &&
-                       cudaMemcpyToSymbol(ssk::g_gemm_trace2, zeros, sizeof(unsigned long long) * 4 * 1024) ==
+                       cudaMemcpyToSymbol(ssk::g_gemm_trace2, zeros, sizeof(unsigned long long) * 16 * 1024) ==
                            cudaSuccess
                    ? 0
                    : -1;
     }
     if (n > 1024) {  // second table: epilogue-warp stamps of the last segment
-        return cudaMemcpyFromSymbol(out, ssk::g_gemm_trace2, sizeof(unsigned long long) * 4 * 1024) == cudaSuccess
+        return cudaMemcpyFromSymbol(out, ssk::g_gemm_trace2, sizeof(unsigned long long) * 16 * 1024) == cudaSuccess
                    ? 0
                    : -1;
     }

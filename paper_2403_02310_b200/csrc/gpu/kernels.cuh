@@ -1,5 +1,6 @@
 // Launch interfaces of the sm_100a kernels (K1..K4) used by ctx.cu.
 #pragma once
+#include <cstdlib>
 
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -49,7 +50,8 @@ struct GemmPlan {
     float* part = nullptr;
     uint32_t* flags = nullptr;
     uint32_t epoch = 0;
-    int sk_mode = -1;  // -1 auto, 0 whole tiles round-robin, 1 stream-K, 2 lockstep split-K
+    int sk_mode = -1;  // -1 auto, 0 whole tiles round-robin, 1 stream-K, 2 lockstep split-K,
+                       // 3 M-lockstep stream-K (super-groups of num_mt CTA pairs)
     int splits = 1;    // K slices per tile for mode 2 (tiles * splits must fit one resident wave)
     EpiArgs ea;
 } __attribute__((aligned(64)));
@@ -59,7 +61,7 @@ inline size_t gemm_part_floats(int num_sms) { return size_t(num_sms) * 128 * 256
 inline size_t gemm_flag_words(int num_sms) { return size_t(num_sms) * 16; }
 
 struct GemmShape {
-    int cg, bn, splits;
+    int cg, bn, splits, mode;  // mode: GemmPlan::sk_mode
 };
 
 bool make_tmap_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
@@ -160,6 +162,11 @@ cudaError_t kv_fill_launch(__nv_bfloat16* kbase, __nv_bfloat16* vbase, int64_t l
 }  // namespace ssk
 
 namespace ssk {
+// SS_NO_PDL=1 (dev): launch without programmatic dependent launch.
+inline int pdl_allowed() {
+    static const int v = getenv("SS_NO_PDL") ? 0 : 1;
+    return v;
+}
 // Launch with the programmatic-stream-serialization attribute (PDL) and an
 // optional cluster shape. Every kernel in this library calls pdl_wait() before
 // its first global access, so PDL launches are always safe.
@@ -174,7 +181,7 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
     cudaLaunchAttribute attr[2];
     int n = 0;
     attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    attr[n].val.programmaticStreamSerializationAllowed = pdl_allowed();
     ++n;
     if (cluster_x > 1) {
         attr[n].id = cudaLaunchAttributeClusterDimension;

@@ -78,11 +78,14 @@ def test_gemm_stream_k_shapes(small, M, N, K):
 
 
 @pytest.mark.parametrize("env", [{"SS_GEMM_SK": "1"}, {"SS_GEMM_BN": "256", "SS_GEMM_SPLITS": "2"},
-                                 {"SS_GEMM_SPLITS": "4"}, {"SS_GEMM_BN": "128", "SS_GEMM_SPLITS": "3"}])
+                                 {"SS_GEMM_SPLITS": "4"}, {"SS_GEMM_BN": "128", "SS_GEMM_SPLITS": "3"},
+                                 {"SS_GEMM_SK": "0"}, {"SS_GEMM_SK": "3", "SS_GEMM_BN": "128"},
+                                 {"SS_GEMM_SK": "3", "SS_GEMM_BN": "256"}])
 @pytest.mark.parametrize("epi", [0, 1, 2, 3])
 def test_gemm_forced_split_schedules(small, monkeypatch, env, epi):
     """Every epilogue through the split-K fixups (stream-K; lockstep split of the ragged
-    wave with the staged smem/bulk-copy reduction): values and bitwise repeatability."""
+    wave with the staged smem/bulk-copy reduction; M-lockstep stream-K): values and
+    bitwise repeatability."""
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     M, N, K = 512, 28672 if epi == 2 else 4096, 4096
