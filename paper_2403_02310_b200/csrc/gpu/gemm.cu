@@ -53,7 +53,8 @@ struct GemmCfg {
     static constexpr int TILE_M = 128 * CG;
 };
 
-__device__ __forceinline__ float silu(float g) { return g / (1.0f + __expf(-g)); }
+// fast reciprocal division: the product is rounded to bf16 anyway
+__device__ __forceinline__ float silu(float g) { return __fdividef(g, 1.0f + __expf(-g)); }
 
 __device__ __forceinline__ uint32_t cluster_rank() {
     uint32_t r;
@@ -513,7 +514,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int r = 0; r < 32; ++r) {
                         if (i < n4 && rbase + r < M) {
-                            const float4 w = __ldg(reinterpret_cast<const float4*>(ea.ssq_in + size_t(rbase + r) * ea.ssq_in_n) + i);
+                            // volatile: issued here, before the accumulator wait, not sunk to the use
+                            float4 w;
+                            asm volatile("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                         : "=f"(w.x), "=f"(w.y), "=f"(w.z), "=f"(w.w)
+                                         : "l"(reinterpret_cast<const float4*>(ea.ssq_in + size_t(rbase + r) * ea.ssq_in_n) + i));
                             a[r] += (w.x + w.y) + (w.z + w.w);
                         }
                     }
@@ -547,16 +552,19 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                             for (int j = 0; j < 8; ++j) {
                                 const int r = rbase + 4 * j + crow;
-                                if (r < M)
-                                    xin[i][j] = *reinterpret_cast<const float4*>(static_cast<const float*>(out) +
-                                                                                 size_t(r) * ldo + col);
+                                if (r < M)  // volatile: issued before the accumulator wait
+                                    asm volatile("ld.global.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                                 : "=f"(xin[i][j].x), "=f"(xin[i][j].y), "=f"(xin[i][j].z), "=f"(xin[i][j].w)
+                                                 : "l"(static_cast<const float*>(out) + size_t(r) * ldo + col));
                             }
                         }
                     }
                 }
             }
-            // QKV: this row's position/slot and the RoPE factors of the warp's first
-            // chunk pair, also fetched while the MMAs run (a dependent load chain)
+            // QKV: this row's position/slot and its RoPE factors, also fetched while the
+            // MMAs run. Every chunk pair of a warp sits at the same offset i0 inside its
+            // head (pairs step by whole heads), so one set of factors serves them all;
+            // volatile loads keep the compiler from sinking them past the wait.
             int q_pos = 0;
             int64_t q_slot = 0;
             float4 rc[16];
@@ -571,7 +579,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                         if (col < N && col / ea.hd < ea.nq + ea.nkv) {
                             const float4* cs = reinterpret_cast<const float4*>(ea.rope + size_t(q_pos) * (ea.hd / 2) + col % ea.hd);
 #pragma unroll
-                            for (int j = 0; j < 16; ++j) rc[j] = __ldg(cs + j);
+                            for (int j = 0; j < 16; ++j)
+                                asm volatile("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                             : "=f"(rc[j].x), "=f"(rc[j].y), "=f"(rc[j].z), "=f"(rc[j].w)
+                                             : "l"(cs + j));
                         }
                     }
                 }
@@ -724,30 +735,34 @@ __global__ void __launch_bounds__(kThreads, 1)
                         tmem_ld32(t_row + uint32_t(c * 32), x1);
                         tmem_ld32(t_row + uint32_t((c + ps) * 32), x2);
                         tmem_wait_ld();
+                        if (pi < half + 4) TRACE2(7 + 3 * ((pi - half) >> 1));
                         add_pieces(x1, c);
                         add_pieces(x2, c + ps);
                         const int col = n0 + c * 32;
                         if (col >= N) continue;  // warp-uniform
                         const int hh = col / ea.hd, i0 = col % ea.hd;  // i0 < hd/2
-                        // this row's packed bf16 result: lo = columns i0.., hi = i0 + hd/2..
-                        uint32_t lo[16], hi[16];
-                        if (hh < ea.nq + ea.nkv) {  // q or k head: rotate
-                            const float4* cs = reinterpret_cast<const float4*>(ea.rope + size_t(q_pos) * (ea.hd / 2) + i0);
-                            const bool pre = pi == half;  // factors preloaded before the wait
+                        // this row's packed bf16 result, staged as [lo 64 B | hi 64 B] (lo = columns
+                        // i0.., hi = i0 + hd/2..), four 16-byte chunks at a time
+                        const bool rot = hh < ea.nq + ea.nkv;  // q or k head: rotate (warp-uniform)
 #pragma unroll
-                            for (int j = 0; j < 16; ++j) {
-                                const float4 f = pre ? rc[j] : (row < M ? __ldg(cs + j) : make_float4(0.f, 0.f, 0.f, 0.f));
+                        for (int jj = 0; jj < 4; ++jj) {
+                            uint32_t lo[4], hi[4];
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {
+                                const int j = 4 * jj + k;
                                 const float a0 = __uint_as_float(x1[2 * j]) * rs, a1 = __uint_as_float(x1[2 * j + 1]) * rs;
                                 const float b0 = __uint_as_float(x2[2 * j]) * rs, b1 = __uint_as_float(x2[2 * j + 1]) * rs;
-                                lo[j] = pack_bf16(a0 * f.x - b0 * f.y, a1 * f.z - b1 * f.w);
-                                hi[j] = pack_bf16(b0 * f.x + a0 * f.y, b1 * f.z + a1 * f.w);
+                                if (rot) {
+                                    const float4 f = rc[j];
+                                    lo[k] = pack_bf16(a0 * f.x - b0 * f.y, a1 * f.z - b1 * f.w);
+                                    hi[k] = pack_bf16(b0 * f.x + a0 * f.y, b1 * f.z + a1 * f.w);
+                                } else {
+                                    lo[k] = pack_bf16(a0, a1);
+                                    hi[k] = pack_bf16(b0, b1);
+                                }
                             }
-                        } else {
-#pragma unroll
-                            for (int j = 0; j < 16; ++j) {
-                                lo[j] = pack_bf16(__uint_as_float(x1[2 * j]) * rs, __uint_as_float(x1[2 * j + 1]) * rs);
-                                hi[j] = pack_bf16(__uint_as_float(x2[2 * j]) * rs, __uint_as_float(x2[2 * j + 1]) * rs);
-                            }
+                            ep[lane * 8 + (jj ^ (lane & 7))] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+                            ep[lane * 8 + ((jj + 4) ^ (lane & 7))] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
                         }
                         __nv_bfloat16* dst = nullptr;
                         if (row < M) {
@@ -756,13 +771,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                             else dst = ea.vc + ((size_t(blk) * ea.nkv + (hh - ea.nq - ea.nkv)) * ea.bs + off) * ea.hd;
                             dst += i0;
                         }
-                        // staged row = [lo 64 B | hi 64 B]; chunk k < 4 -> dst + 8k, else dst + hd/2 + 8(k-4)
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            ep[lane * 8 + (j ^ (lane & 7))] = make_uint4(lo[4 * j], lo[4 * j + 1], lo[4 * j + 2], lo[4 * j + 3]);
-                            ep[lane * 8 + ((j + 4) ^ (lane & 7))] = make_uint4(hi[4 * j], hi[4 * j + 1], hi[4 * j + 2], hi[4 * j + 3]);
-                        }
+                        // chunk k < 4 -> dst + 8k, else dst + hd/2 + 8(k-4)
                         __syncwarp();
+                        if (pi < half + 4) TRACE2(8 + 3 * ((pi - half) >> 1));
                         const uint64_t dp = reinterpret_cast<uint64_t>(dst);
 #pragma unroll
                         for (int j = 0; j < 8; ++j) {
@@ -775,6 +786,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             }
                         }
                         __syncwarp();
+                        if (pi < half + 4) TRACE2(9 + 3 * ((pi - half) >> 1));
                     }
                 } else {
                     // chunks of this warp: c = half, half + 2, ... (SwiGLU: gate/up pairs
@@ -864,9 +876,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                                     for (int j = 0; j < 8; ++j) {
                                         const int r = rbase + 4 * j + crow;
-                                        if (r < M)
-                                            xin[i & 1][j] = *reinterpret_cast<const float4*>(static_cast<const float*>(out) +
-                                                                                             size_t(r) * ldo + col2);
+                                        if (r < M)  // volatile: issued now, consumed two chunks later
+                                            asm volatile("ld.global.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                                         : "=f"(xin[i & 1][j].x), "=f"(xin[i & 1][j].y), "=f"(xin[i & 1][j].z),
+                                                           "=f"(xin[i & 1][j].w)
+                                                         : "l"(static_cast<const float*>(out) + size_t(r) * ldo + col2));
                                     }
                                 }
                             }
@@ -1107,7 +1121,7 @@ extern "C" __attribute__((visibility("default"))) int ss_debug_gemm_trace(unsign
     }
     if (n < 0) {  // clear both tables
         static unsigned long long zeros[1024 * 16] = {};
-        return cudaMemcpyToSymbol(ssk::g_gemm_trace, zeros, sizeof(zeros)) == cudaSuccess &&
+        return cudaMemcpyToSymbol(ssk::g_gemm_trace, zeros, sizeof(unsigned long long) * 8 * 1024) == cudaSuccess &&
                        cudaMemcpyToSymbol(ssk::g_gemm_trace2, zeros, sizeof(unsigned long long) * 16 * 1024) ==
                            cudaSuccess
                    ? 0

@@ -12,8 +12,8 @@ lib = gpu.gpu_lib()
 
 
 def clear(epi=None):
-    lib.ss_debug_gemm_trace(None, -1)
-    lib.ss_debug_gemm_trace(None, -2 if epi is None else -3 - epi)
+    assert lib.ss_debug_gemm_trace(None, -1) == 0
+    assert lib.ss_debug_gemm_trace(None, -2 if epi is None else -3 - epi) == 0
 
 
 def report(name):
@@ -37,8 +37,8 @@ def report(name):
     assert lib.ss_debug_gemm_trace(t2.ctypes.data_as(C.POINTER(C.c_ulonglong)), 4096) == 0
     t2 = t2.astype(np.int64)[live]
     for j, nm in enumerate(["tfull seen (last seg)", "flags done (heads)", "epilogue done", "published (pieces)",
-                              "staged 1st piece in", "staged done", "staged bar passed", "chunk0 tmem ld",
-                              "chunk0 staged", "chunk0 stored", "chunk0 ssq", "chunk1 ssq", "chunk2 ssq", "chunk3 ssq"]):
+                              "staged 1st piece in", "staged done", "staged bar passed", "7", "8", "9", "10", "11",
+                              "12", "13"]):
         v = t2[:, j]
         v = v[v >= t0]
         if len(v):
