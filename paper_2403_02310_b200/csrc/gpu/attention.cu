@@ -42,15 +42,29 @@ constexpr int kKeysPerTile = 64;
 constexpr int kRowsPerTile = 64;
 constexpr int kStages = 3;  // 2 CTAs/SM x 2 tiles in flight = 128 KB of K/V outstanding per SM
 
+constexpr int kTcRows = 128;  // rows of a tensor-core (prefill) item
+constexpr int cmax(int a, int b) { return a > b ? a : b; }
+
 template <int HD>
 struct AttnSmem {
     static constexpr int Q_BYTES = kRowsPerTile * HD * 2;
     static constexpr int KV_TILE = kKeysPerTile * HD * 2;  // [HD/64 halves][64 keys][128 B]
     static constexpr int STAGE = 2 * KV_TILE;              // K + V
     static constexpr int BAR_OFF = Q_BYTES + kStages * STAGE;
-    // 896 B of alignment slack (the dynamic window starts 1 KB-aligned in practice;
-    // checked at run time) keeps two CTAs per SM within 228 KB at hd = 128
-    static constexpr int TOTAL = BAR_OFF + 64 + 896;
+    // 256 B of barriers + 704 B of alignment slack (the dynamic window starts 1 KB-aligned
+    // in practice; checked at run time) keep two decode CTAs per SM within 228 KB at hd = 128
+    static constexpr int TOTAL = BAR_OFF + 256 + 704;
+    // tensor-core prefill kernel (tcgen05), one CTA per SM: Q [HD/64][128 rows][128 B],
+    // TC_STAGES K/V stages (deep: the K/V latency is the per-tile critical path), P [128
+    // rows][64 keys] bf16 — all SWIZZLE_128B, K-major (V read MN-major)
+    static constexpr int TC_Q = kTcRows * HD * 2;
+    static constexpr int TC_P_BYTES = 2 * kTcRows * kKeysPerTile * 2;  // double buffered
+    static constexpr int TC_STAGES_FIT = (232448 - 960 - 1024 - TC_Q - TC_P_BYTES) / STAGE;
+    static constexpr int TC_STAGES = TC_STAGES_FIT > 8 ? 8 : TC_STAGES_FIT;
+    static constexpr int TC_STAGE0 = TC_Q;
+    static constexpr int TC_P = TC_Q + TC_STAGES * STAGE;
+    static constexpr int TC_BAR = TC_P + TC_P_BYTES;
+    static constexpr int TC_TOTAL = TC_BAR + 256 + 704;
 };
 
 // Q tile: rows of HD*2 bytes, 16-byte chunks XOR-swizzled by row.
@@ -61,27 +75,6 @@ __device__ __forceinline__ uint32_t swz_q(int row, int c) {
 // K/V tile as written by TMA with SWIZZLE_128B: [c / 8 half][key][128 B].
 __device__ __forceinline__ uint32_t swz_kv(int key, int c) {
     return uint32_t((c >> 3) * (kKeysPerTile * 128) + key * 128 + (((c & 7) ^ (key & 7)) << 4));
-}
-
-template <int HD>
-__device__ __forceinline__ void issue_kv_tile(const AttnParams& p, const CUtensorMap* tmK, const CUtensorMap* tmV,
-                                              uint8_t* sK, uint8_t* sV, uint64_t* bar, int e, int h, int kbase) {
-    const int32_t* bt = p.block_table + size_t(e) * p.max_blocks;
-    const int nvalid = (p.ctx_len[e] + 15) >> 4;
-    mbar_arrive_expect_tx(bar, 2 * AttnSmem<HD>::KV_TILE);
-#pragma unroll
-    for (int pg = 0; pg < kKeysPerTile / 16; ++pg) {
-        const int lb = (kbase >> 4) + pg;
-        // pages past the context are masked; point them at a valid (finite) page
-        const int32_t blk = bt[lb < nvalid ? lb : 0];
-        const int32_t row = int32_t(p.layer_row0 + (int64_t(blk) * p.nkv_l + h) * 16);
-#pragma unroll
-        for (int hh = 0; hh < HD / 64; ++hh) {
-            const uint32_t off = uint32_t(hh * (kKeysPerTile * 128) + pg * 16 * 128);
-            tma_load_2d(sK + off, tmK, hh * 64, row, bar);
-            tma_load_2d(sV + off, tmV, hh * 64, row, bar);
-        }
-    }
 }
 
 // KPW = keys handled per warp per 64-key tile (64: row mode, 16: key mode).
@@ -120,7 +113,7 @@ __device__ __forceinline__ void attend(const AttnParams& p, const CUtensorMap* t
 #pragma unroll
     for (int dt = 0; dt < HD / 8; ++dt) O[dt][0] = O[dt][1] = O[dt][2] = O[dt][3] = 0.f;
 
-    uint64_t* empty = full + kStages;
+    uint64_t* empty = full + 8;  // barrier block layout: see attention_kernel
     const int ntiles = (it.key1 - it.key0 + kKeysPerTile - 1) / kKeysPerTile;
     for (int t = 0; t < ntiles; ++t) {
         const int kbase = it.key0 + t * kKeysPerTile;
@@ -275,41 +268,267 @@ __device__ __forceinline__ void emit_pair(const AttnParams& p, const AttnItem& i
     }
 }
 
+
+// ---- tensor-core prefill tile (tcgen05): 128 GQA-packed rows x 64-key tiles.
+// Warp 0 (one elected lane) issues S = Q K^T into a TMEM double buffer and O += P V
+// into a TMEM accumulator; each of the 4 warps' threads owns one row (TMEM lane), so
+// the online softmax is thread-local: no shuffles. The running max is refreshed only
+// when it grows by more than 2^8 (log2 units), which keeps rescales of the O row in
+// TMEM rare while every p = 2^(s - m) stays <= 256 (exact in fp32, relative in bf16).
+__device__ __forceinline__ void tmem_st32_attn(uint32_t taddr, const uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+        "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+        "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+        : "memory");
+}
+__device__ __forceinline__ float ex2_approx(float x) {  // 2^x, -inf -> 0
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ bool elect_lane() {
+    uint32_t pred;
+    asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}" : "=r"(pred));
+    return pred != 0;
+}
+// MN-major SWIZZLE_128B operand (V as B of O += P V: N = head dim contiguous, K = keys):
+// 8-key groups 1 KB apart (SBO), 64-column halves of the head dim LBO apart.
+__device__ __forceinline__ uint64_t umma_desc_sw128_mn(uint32_t smem_addr, uint32_t lbo) {
+    return (uint64_t((smem_addr >> 4) & 0x3FFFu)) | (uint64_t((lbo >> 4) & 0x3FFFu) << 16) |
+           (uint64_t(1024 >> 4) << 32) | (uint64_t(1) << 46) | (uint64_t(2) << 61);
+}
+
+// Warp roles of the tensor-core kernel: warps 0-3 softmax (thread = row = TMEM
+// lane), warp 4 TMA producer, warp 5 MMA issuer. Per 64-key tile t the issuer runs
+// S(t) = Q K(t)^T into TMEM buffer t & 1 and, once the softmax warps have published
+// P(t - 1) (mbarrier, one arrival per warp), O += P(t - 1) V(t - 1); P is double
+// buffered in smem, so softmax(t) overlaps PV(t - 1) and S(t + 1).
 template <int HD>
-__global__ void __launch_bounds__((kWarps + 1) * 32) attention_kernel(const AttnParams p,
+__device__ __forceinline__ void mma_warp_tc(const AttnItem& it, uint8_t* smem, uint64_t* full, uint64_t* empty,
+                                            uint64_t* sbar, uint64_t* obar, uint64_t* pready, uint32_t tbase) {
+    using S = AttnSmem<HD>;
+    constexpr int NST = S::TC_STAGES;
+    const int nt = (it.key1 - it.key0 + kKeysPerTile - 1) / kKeysPerTile;
+    constexpr uint32_t idS = umma_idesc_bf16(kTcRows, kKeysPerTile);
+    constexpr uint32_t idO = umma_idesc_bf16(kTcRows, HD) | (1u << 16);  // B (V) MN-major
+    const uint32_t qa = smem_u32(smem), sa = smem_u32(smem + S::TC_STAGE0), pa = smem_u32(smem + S::TC_P);
+    const uint32_t tO = tbase + 128;
+    auto issue_pv = [&](int u) {  // O += P(u) V(u)
+        mbar_wait(&pready[u & 1], uint32_t((u >> 1) & 1));
+        tc_fence_after();
+        if (elect_lane()) {
+            const uint32_t va = sa + (u % NST) * S::STAGE + S::KV_TILE;
+            const uint32_t pb = pa + (u & 1) * (kTcRows * kKeysPerTile * 2);
+#pragma unroll
+            for (int kk = 0; kk < kKeysPerTile / 16; ++kk)
+                umma_bf16(tO, umma_desc_sw128(pb) + uint64_t(2 * kk),
+                          umma_desc_sw128_mn(va + kk * 16 * 128, kKeysPerTile * 128), idO, (u > 0 || kk > 0) ? 1u : 0u);
+            umma_commit(&obar[u & 1]);
+            umma_commit(&empty[u % NST]);  // K/V stage free once S(u) and PV(u) retire
+        }
+        __syncwarp();
+    };
+    for (int t = 0; t < nt; ++t) {
+        const int st = t % NST;
+        // (S buffer t & 1 was last read by softmax(t - 2): P(t - 2) was awaited before PV(t - 2))
+        mbar_wait(&full[st], uint32_t((t / NST) & 1));
+        tc_fence_after();
+        if (elect_lane()) {
+            const uint32_t ka = sa + st * S::STAGE;
+#pragma unroll
+            for (int ks = 0; ks < HD / 16; ++ks) {
+                const int hh = ks >> 2, kk = ks & 3;
+                umma_bf16(tbase + uint32_t((t & 1) * 64), umma_desc_sw128(qa + hh * kTcRows * 128) + uint64_t(2 * kk),
+                          umma_desc_sw128(ka + hh * kKeysPerTile * 128) + uint64_t(2 * kk), idS, ks > 0 ? 1u : 0u);
+            }
+            umma_commit(&sbar[t & 1]);
+        }
+        __syncwarp();
+        if (t >= 1) issue_pv(t - 1);
+    }
+    if (nt > 0) issue_pv(nt - 1);
+}
+
+template <int HD>
+__device__ __forceinline__ void softmax_warps_tc(const AttnParams& p, const AttnItem& it, uint8_t* smem,
+                                                 uint64_t* sbar, uint64_t* obar, uint64_t* pready, uint32_t tbase,
+                                                 int warp, int lane) {
+    using S = AttnSmem<HD>;
+    const int r = warp * 32 + lane;  // row of the tile == TMEM lane
+    const int e = it.entry;
+    const int tok0 = p.cu_q[e];
+    const int ntok = p.cu_q[e + 1] - tok0;
+    const int prefix = p.ctx_len[e] - ntok;
+    const int lim = r < it.nrows ? prefix + (it.row0 + r) / p.group : -1;  // last visible key
+    const int nt = (it.key1 - it.key0 + kKeysPerTile - 1) / kKeysPerTile;
+    const uint32_t lane_base = uint32_t(warp * 32) << 16;
+    const uint32_t tO = tbase + 128;
+    float m = -INFINITY, l = 0.f;
+    for (int t = 0; t < nt; ++t) {
+        mbar_wait(&sbar[t & 1], uint32_t((t >> 1) & 1));
+        tc_fence_after();
+        uint32_t sv[64];
+        tmem_ld32(tbase + lane_base + uint32_t((t & 1) * 64), *reinterpret_cast<uint32_t(*)[32]>(&sv[0]));
+        tmem_ld32(tbase + lane_base + uint32_t((t & 1) * 64 + 32), *reinterpret_cast<uint32_t(*)[32]>(&sv[32]));
+        tmem_wait_ld();
+        const int kb = it.key0 + t * kKeysPerTile;
+        const int kend = min(lim + 1, it.key1) - kb;  // keys [kb, kb + kend) are visible to this row
+        // raw-score max (the scale is positive); the mask pass runs only where a row's
+        // causal limit or the range end cuts this tile
+        if (__any_sync(0xffffffffu, kend < 64)) {
+#pragma unroll
+            for (int j = 0; j < 64; ++j)
+                if (j >= kend) sv[j] = __float_as_uint(-INFINITY);
+        }
+        float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < 64; j += 2) {
+            mx0 = fmaxf(mx0, __uint_as_float(sv[j]));
+            mx1 = fmaxf(mx1, __uint_as_float(sv[j + 1]));
+        }
+        const float mx = fmaxf(mx0, mx1) * p.scale_log2;
+        // lazy max: refresh only on first sight or growth by > 2^8
+        float alpha = 1.f;
+        if (mx > m + 8.f) {
+            alpha = m == -INFINITY ? 1.f : ex2_approx(m - mx);
+            m = mx;
+        }
+        const float msub = m == -INFINITY ? 0.f : m;
+        float ls0 = 0.f, ls1 = 0.f;
+        uint32_t pk[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            const float p0 = ex2_approx(fmaf(__uint_as_float(sv[2 * j]), p.scale_log2, -msub));
+            const float p1 = ex2_approx(fmaf(__uint_as_float(sv[2 * j + 1]), p.scale_log2, -msub));
+            ls0 += p0;
+            ls1 += p1;
+            pk[j] = pack_bf16(p0, p1);
+        }
+        l = l * alpha + (ls0 + ls1);
+        // P buffer t & 1 was read by PV(t - 2); a rescale of O needs PV(t - 1) retired
+        if (t >= 2) {
+            mbar_wait(&obar[t & 1], uint32_t(((t - 2) >> 1) & 1));
+            tc_fence_after();
+        }
+        if (__any_sync(0xffffffffu, alpha != 1.f)) {
+            mbar_wait(&obar[(t - 1) & 1], uint32_t(((t - 1) >> 1) & 1));
+            tc_fence_after();
+#pragma unroll 1
+            for (int c = 0; c < HD / 32; ++c) {
+                uint32_t ov[32];
+                tmem_ld32(tO + lane_base + uint32_t(c * 32), ov);
+                tmem_wait_ld();
+#pragma unroll
+                for (int j = 0; j < 32; ++j) ov[j] = __float_as_uint(__uint_as_float(ov[j]) * alpha);
+                tmem_st32_attn(tO + lane_base + uint32_t(c * 32), ov);
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        }
+        // P row -> smem (K-major SWIZZLE_128B: 16-byte chunk j of row r at j ^ (r & 7))
+        uint4* prow = reinterpret_cast<uint4*>(smem + S::TC_P + (t & 1) * (kTcRows * kKeysPerTile * 2) + r * 128);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) prow[j ^ (r & 7)] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&pready[t & 1]);  // one arrival per softmax warp
+    }
+    // the last PV retires -> O row / l -> bf16 (final) or the unnormalised partial
+    mbar_wait(&obar[(nt - 1) & 1], uint32_t(((nt - 1) >> 1) & 1));
+    tc_fence_after();
+    const bool live = r < it.nrows;
+    const int gr = it.row0 + r;
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+#pragma unroll 1
+    for (int c = 0; c < HD / 32; ++c) {
+        uint32_t ov[32];
+        tmem_ld32(tO + lane_base + uint32_t(c * 32), ov);
+        tmem_wait_ld();
+        if (!live) continue;
+        if (it.part < 0) {
+            __nv_bfloat16* dst = p.o + (size_t(tok0 + gr / p.group) * p.nq_l + it.kv_head * p.group + gr % p.group) * HD + c * 32;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                reinterpret_cast<uint4*>(dst)[j] = make_uint4(
+                    pack_bf16(__uint_as_float(ov[8 * j + 0]) * inv, __uint_as_float(ov[8 * j + 1]) * inv),
+                    pack_bf16(__uint_as_float(ov[8 * j + 2]) * inv, __uint_as_float(ov[8 * j + 3]) * inv),
+                    pack_bf16(__uint_as_float(ov[8 * j + 4]) * inv, __uint_as_float(ov[8 * j + 5]) * inv),
+                    pack_bf16(__uint_as_float(ov[8 * j + 6]) * inv, __uint_as_float(ov[8 * j + 7]) * inv));
+        } else {
+            float4* dst = reinterpret_cast<float4*>(p.part_o + size_t(it.part + r) * HD + c * 32);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                dst[j] = make_float4(__uint_as_float(ov[4 * j]), __uint_as_float(ov[4 * j + 1]),
+                                     __uint_as_float(ov[4 * j + 2]), __uint_as_float(ov[4 * j + 3]));
+            if (c == 0) *reinterpret_cast<float2*>(p.part_ml + size_t(it.part + r) * 2) = make_float2(m, l);
+        }
+    }
+}
+
+template <int HD, bool TC>
+__global__ void __launch_bounds__((kWarps + 1 + TC) * 32) attention_kernel(const AttnParams p,
                                                                       const __grid_constant__ CUtensorMap tmK,
                                                                       const __grid_constant__ CUtensorMap tmV) {
     using S = AttnSmem<HD>;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t pad = ((raw + 1023u) & ~1023u) - raw;
-    if (pad > 896u) __trap();  // SWIZZLE_128B tiles need 1 KB alignment
+    if (pad > 704u) __trap();  // SWIZZLE_128B tiles need 1 KB alignment
     uint8_t* smem = smem_raw + pad;
     const AttnItem it = p.items[blockIdx.x];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const bool key_mode = it.nrows <= 16;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
-    uint64_t* empty = full + kStages;
+    const bool key_mode = !TC && it.nrows <= 16;
+    constexpr bool tc = TC;  // prefill row tile on the tensor cores
+    // barrier block (256 B): full[8] empty[8] | split flag | S-ready[2] | PV-done[2] | P-ready[2] | TMEM slot
+    constexpr int kMaxSt = 8;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (TC ? S::TC_BAR : S::BAR_OFF));
+    uint64_t* empty = full + kMaxSt;
+    int* split_flag = reinterpret_cast<int*>(full + 2 * kMaxSt);
+    uint64_t* sbar = full + 2 * kMaxSt + 1;
+    uint64_t* obar = sbar + 2;    // [2]
+    uint64_t* pready = obar + 2;  // [2] softmax warps -> MMA warp: P(t) published (by t & 1)
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(pready + 2);
+    const int nst = tc ? S::TC_STAGES : kStages;
+    const int st0 = tc ? S::TC_STAGE0 : S::Q_BYTES;
 
     if (threadIdx.x == 0) {
         tma_prefetch(&tmK);
         tma_prefetch(&tmV);
-        for (int s = 0; s < kStages; ++s) {
+        for (int s = 0; s < nst; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kWarps);
+            mbar_init(&empty[s], tc ? 1 : kWarps);  // tc: released by a tcgen05.commit
         }
+        mbar_init(&sbar[0], 1);
+        mbar_init(&sbar[1], 1);
+        mbar_init(&obar[0], 1);
+        mbar_init(&obar[1], 1);
+        mbar_init(&pready[0], kWarps);
+        mbar_init(&pready[1], kWarps);
         mbar_fence_init();
     }
-    pdl_launch_dependents();
-    pdl_wait();  // q / KV of this layer come from the preceding kernels
+    if constexpr (TC) {
+        if (warp == 0) tmem_alloc<256>(tslot);  // S double buffer (2 x 64 cols) + O (HD cols)
+        pdl_wait();  // q / KV of this layer come from the preceding kernels
+        pdl_launch_dependents();  // only now: the decode launch relies on this wait
+    } else {
+        pdl_launch_dependents();
+        if (!p.wait_at_end) pdl_wait();
+    }
     // stage the Q tile (rows beyond nrows are zero)
     {
         constexpr int CH = HD / 8;
         const int e = it.entry, tok0 = p.cu_q[e];
-        const int nr = key_mode ? 16 : kRowsPerTile;
-        for (int idx = threadIdx.x; idx < nr * CH; idx += (kWarps + 1) * 32) {
+        const int nr = key_mode ? 16 : (tc ? kTcRows : kRowsPerTile);
+        for (int idx = threadIdx.x; idx < nr * CH; idx += blockDim.x) {
             const int r = idx / CH, c = idx % CH;
-            const uint32_t so = smem_u32(smem) + swz_q<HD>(r, c);
+            // tc: UMMA K-major SWIZZLE_128B image [c / 8][row][128 B]
+            const uint32_t so = smem_u32(smem) + (tc ? uint32_t((c >> 3) * (kTcRows * 128) + r * 128 + (((c & 7) ^ (r & 7)) << 4))
+                                                   : swz_q<HD>(r, c));
             if (r < it.nrows) {
                 const int gr = it.row0 + r;
                 const __nv_bfloat16* src =
@@ -321,23 +540,70 @@ __global__ void __launch_bounds__((kWarps + 1) * 32) attention_kernel(const Attn
         }
         cp_async_commit();
         cp_async_wait<0>();
-        __syncthreads();
+        if constexpr (TC) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // Q is read by tcgen05.mma
+            tc_fence_before();
+            __syncthreads();
+            tc_fence_after();
+        } else {
+            __syncthreads();
+        }
     }
 
     if (warp == kWarps) {  // ---- producer warp: K/V pages by TMA into the ring
-        if (lane == 0) {
-            const int ntiles = (it.key1 - it.key0 + kKeysPerTile - 1) / kKeysPerTile;
-            for (int t = 0; t < ntiles; ++t) {
-                const int st = t % kStages;
-                if (t >= kStages) mbar_wait(&empty[st], uint32_t(((t / kStages) - 1) & 1));
-                uint8_t* sk = smem + S::Q_BYTES + st * S::STAGE;
-                issue_kv_tile<HD>(p, &tmK, &tmV, sk, sk + S::KV_TILE, &full[st], it.entry, it.kv_head,
-                                  it.key0 + t * kKeysPerTile);
+        // Block ids come 32 pages (8 tiles) at a time from one coalesced warp load,
+        // fetched a batch ahead, and reach the issuing lane by shuffle: no dependent
+        // global load sits between two tiles' TMA issues.
+        const int ntiles = (it.key1 - it.key0 + kKeysPerTile - 1) / kKeysPerTile;
+        const int32_t* bt = p.block_table + size_t(it.entry) * p.max_blocks;
+        const int nvalid = (p.ctx_len[it.entry] + 15) >> 4;
+        const int pg0 = it.key0 >> 4;  // key0 is a multiple of 64
+        auto batch = [&](int b) {
+            const int lb = pg0 + 32 * b + lane;
+            return __ldg(bt + (lb < nvalid ? lb : 0));  // pages past the context: a valid page, masked
+        };
+        int32_t cur = batch(0), nxt = ntiles > 8 ? batch(1) : 0;
+        for (int t = 0; t < ntiles; ++t) {
+            if (t > 0 && (t & 7) == 0) {
+                cur = nxt;
+                if (t + 8 < ntiles) nxt = batch((t >> 3) + 1);
             }
+            int32_t blk[4];
+#pragma unroll
+            for (int pg = 0; pg < 4; ++pg) blk[pg] = __shfl_sync(0xffffffffu, cur, ((t & 7) << 2) + pg);
+            const int st = t % nst;
+            // one box per lane: a tile's 4 pages x HD/64 halves x {K, V} loads issue in
+            // parallel (a single issuing thread serialises them: measured 1.5x slower)
+            constexpr int kOps = 4 * (HD / 64) * 2;
+            if (t >= nst) mbar_wait(&empty[st], uint32_t(((t / nst) - 1) & 1));
+            if (lane < kOps) {
+                if (lane == 0) mbar_arrive_expect_tx(&full[st], 2 * S::KV_TILE);
+                const int kv = lane & 1, hh = (lane >> 1) % (HD / 64), pg = lane / (2 * (HD / 64));
+                const int32_t row = int32_t(p.layer_row0 + (int64_t(blk[pg]) * p.nkv_l + it.kv_head) * 16);
+                uint8_t* dst = smem + st0 + st * S::STAGE + kv * S::KV_TILE + hh * (kKeysPerTile * 128) + pg * 16 * 128;
+                tma_load_2d(dst, kv ? &tmV : &tmK, hh * 64, row, &full[st]);
+            }
+            __syncwarp();
         }
+        if (!TC && p.wait_at_end) pdl_wait();
         return;
     }
 
+    if constexpr (TC) {
+        if (warp == kWarps + 1) {
+            mma_warp_tc<HD>(it, smem, full, empty, sbar, obar, pready, *tslot);
+            return;
+        }
+        softmax_warps_tc<HD>(p, it, smem, sbar, obar, pready, *tslot, warp, lane);
+        if (p.fused_combine) finish_split<HD>(p, it, split_flag);
+        tc_fence_before();
+        asm volatile("bar.sync 1, %0;" ::"n"(kWarps * 32) : "memory");
+        if (warp == 0) {
+            tc_fence_after();
+            tmem_dealloc<256>(*tslot);
+        }
+        return;
+    } else {
     float O[HD / 8][4], m[2], l[2];
     if (!key_mode) {
         attend<HD, 64>(p, &tmK, &tmV, it, smem, warp * 16, 0, O, m, l);
@@ -348,7 +614,8 @@ __global__ void __launch_bounds__((kWarps + 1) * 32) attention_kernel(const Attn
             emit_pair<HD>(p, it, r0, d, O[dt][0], O[dt][1], m[0], l[0]);
             emit_pair<HD>(p, it, r0 + 8, d, O[dt][2], O[dt][3], m[1], l[1]);
         }
-        if (p.fused_combine) finish_split<HD>(p, it, reinterpret_cast<int*>(smem + S::BAR_OFF + 2 * kStages * 8));
+        if (p.fused_combine) finish_split<HD>(p, it, split_flag);
+        if (p.wait_at_end) pdl_wait();
         return;
     }
 
@@ -391,7 +658,9 @@ __global__ void __launch_bounds__((kWarps + 1) * 32) attention_kernel(const Attn
         }
         emit_pair<HD>(p, it, r, d, o0, o1, M, L);
     }
-    if (p.fused_combine) finish_split<HD>(p, it, reinterpret_cast<int*>(smem + S::BAR_OFF + 2 * kStages * 8));
+    if (p.fused_combine) finish_split<HD>(p, it, split_flag);
+    if (p.wait_at_end) pdl_wait();
+    }
 }
 
 template <int HD>
@@ -422,14 +691,29 @@ template <int HD>
 cudaError_t launch_hd(const AttnParams& p, const CUtensorMap& tk, const CUtensorMap& tv, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(attention_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             AttnSmem<HD>::TOTAL);
+        cudaError_t e = cudaFuncSetAttribute(attention_kernel<HD, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             AttnSmem<HD>::TC_TOTAL);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(attention_kernel<HD, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     AttnSmem<HD>::TOTAL);
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    return p.n_items > 0 ? launch_pdl(attention_kernel<HD>, dim3(p.n_items), dim3((kWarps + 1) * 32), AttnSmem<HD>::TOTAL,
-                                      st, 1, p, tk, tv)
-                         : cudaSuccess;
+    // items[0, n_tc): tensor-core prefill tiles; the rest: decode / mma.sync items
+    const int n_tc = p.tc ? p.n_tc : 0, n_rest = p.n_items - n_tc;
+    if (n_tc > 0) {
+        cudaError_t e = launch_pdl(attention_kernel<HD, true>, dim3(n_tc), dim3((kWarps + 2) * 32),
+                                   AttnSmem<HD>::TC_TOTAL, st, 1, p, tk, tv);
+        if (e != cudaSuccess) return e;
+    }
+    if (n_rest > 0) {
+        AttnParams q = p;
+        q.items = p.items + n_tc;
+        q.wait_at_end = n_tc > 0;
+        return launch_pdl(attention_kernel<HD, false>, dim3(n_rest), dim3((kWarps + 1) * 32), AttnSmem<HD>::TOTAL, st,
+                          1, q, tk, tv);
+    }
+    return cudaSuccess;
 }
 
 }  // namespace

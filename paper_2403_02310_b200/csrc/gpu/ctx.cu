@@ -109,7 +109,7 @@ struct ss_batch {
     int64_t* slot = nullptr;
     AttnItem* items = nullptr;
     AttnCombine* combs = nullptr;
-    int n_items = 0, n_combs = 0, part_rows = 0;
+    int n_items = 0, n_combs = 0, part_rows = 0, n_tc = 0;
 };
 
 // Tensor parallelism on ONE device, for validating the sharded forward where only
@@ -179,6 +179,7 @@ struct ss_ctx {
     float *part_o = nullptr, *part_ml = nullptr;
     int32_t* comb_count = nullptr;  // split-KV group counters (self-resetting)
     int fused_combine = 0;          // in-kernel split merge (measured slower at 8 splits; off)
+    int attn_tc = 1;                // prefill row tiles on tcgen05 (128 rows); 0: mma.sync (64 rows)
     int decode_split = 0;           // dev override (SS_ATTN_SPLIT): fixed keys per decode split; 0 = adaptive
     int fuse_rope = 1;              // RoPE + KV append in the QKV GEMM epilogue (else the K2 kernel)
     float* sk_part = nullptr;       // stream-K GEMM partial accumulators
@@ -363,7 +364,7 @@ ss_status ensure_workspace(ss_ctx* ctx, int T, int n_out, int part_rows) {
 
 // Work list of the mixed attention launch (see attention.cu).
 void build_items(const ss_ctx* ctx, const ss_batch_desc* d, std::vector<AttnItem>& items,
-                 std::vector<AttnCombine>& combs, int& part_rows) {
+                 std::vector<AttnCombine>& combs, int& part_rows, int& n_tc) {
     const int G = ctx->G;
     struct Tile {
         int e, row0, nr, extent;
@@ -374,8 +375,9 @@ void build_items(const ss_ctx* ctx, const ss_batch_desc* d, std::vector<AttnItem
         const int ntok = d->cu_q[e + 1] - d->cu_q[e];
         const int prefix = d->ctx_len[e] - ntok;
         const int rows = ntok * G;
-        for (int row0 = 0; row0 < rows; row0 += 64) {
-            const int nr = std::min(64, rows - row0);
+        const int tile = rows <= 16 ? 16 : (ctx->attn_tc ? 128 : 64);
+        for (int row0 = 0; row0 < rows; row0 += tile) {
+            const int nr = std::min(tile, rows - row0);
             tiles.push_back(Tile{e, row0, nr, prefix + (row0 + nr - 1) / G + 1});
             if (nr > 16) prefill_items += ctx->nkv_l;
             else decode_pairs += ctx->nkv_l;
@@ -419,12 +421,21 @@ void build_items(const ss_ctx* ctx, const ss_batch_desc* d, std::vector<AttnItem
     // longest items first so the tail of the launch is short (SS_ATTN_ORDER=1,
     // dev: prefill row tiles first)
     static const int order = getenv("SS_ATTN_ORDER") ? atoi(getenv("SS_ATTN_ORDER")) : 0;
-    std::stable_sort(items.begin(), items.end(), [](const AttnItem& a, const AttnItem& b) {
+    const bool tc_items = ctx->attn_tc != 0;
+    std::stable_sort(items.begin(), items.end(), [tc_items](const AttnItem& a, const AttnItem& b) {
         if (order == 1 && (a.nrows > 16) != (b.nrows > 16)) return a.nrows > 16;
-        const long ca = long(a.key1 - a.key0) * (a.nrows <= 16 ? 16 : 64);
-        const long cb = long(b.key1 - b.key0) * (b.nrows <= 16 ? 16 : 64);
+        // per-key cost: decode streaming ~16, mma.sync row tile ~64, tcgen05 row tile ~8
+        auto wt = [tc_items](const AttnItem& x) { return x.nrows <= 16 ? 16 : (tc_items ? 8 : 64); };
+        const long ca = long(a.key1 - a.key0) * wt(a);
+        const long cb = long(b.key1 - b.key0) * wt(b);
         return ca > cb;
     });
+    // tensor-core row tiles first: they are the first of the two attention launches
+    n_tc = 0;
+    if (tc_items) {
+        auto mid = std::stable_partition(items.begin(), items.end(), [](const AttnItem& x) { return x.nrows > 16; });
+        n_tc = int(mid - items.begin());
+    }
 }
 
 ss_status validate(ss_ctx* ctx, const ss_batch_desc* d) {
@@ -465,8 +476,8 @@ ss_status upload(ss_ctx* ctx, const ss_batch_desc* d, ss_batch* b) {
     if (ss_status s = validate(ctx, d)) return s;
     std::vector<AttnItem> items;
     std::vector<AttnCombine> combs;
-    int part_rows = 0;
-    build_items(ctx, d, items, combs, part_rows);
+    int part_rows = 0, n_tc = 0;
+    build_items(ctx, d, items, combs, part_rows, n_tc);
     const int E = d->num_entries, T = d->num_tokens;
     struct Seg {
         const void* src;
@@ -516,6 +527,7 @@ ss_status upload(ss_ctx* ctx, const ss_batch_desc* d, ss_batch* b) {
     b->n_out = d->n_out;
     b->max_blocks = d->max_blocks;
     b->n_items = int(items.size());
+    b->n_tc = n_tc;
     b->n_combs = int(combs.size());
     b->part_rows = part_rows;
     return ensure_workspace(ctx, T, std::max(d->n_out, 1), part_rows);
@@ -533,10 +545,13 @@ AttnParams attn_params(const ss_ctx* ctx, const ss_batch* b, const bf16* q, bf16
     p.max_blocks = b->max_blocks;
     p.items = b->items;
     p.n_items = b->n_items;
+    p.n_tc = b->n_tc;
+    p.wait_at_end = 0;
     p.part_o = ctx->part_o;
     p.part_ml = ctx->part_ml;
     p.comb_count = ctx->comb_count;
     p.fused_combine = ctx->fused_combine;
+    p.tc = ctx->attn_tc;
     p.combines = b->combs;
     p.n_combines = b->n_combs;
     p.nq_l = ctx->nq_l;
@@ -804,6 +819,7 @@ static ss_status create_impl(const ss_model_cfg* cfg, int32_t tp_rank, int32_t t
     ctx->grp = grp;
     if (const char* f = getenv("SS_ATTN_SPLIT")) ctx->decode_split = std::max(64, atoi(f) / 64 * 64);  // dev tuning
     if (const char* f = getenv("SS_ATTN_FUSED_COMBINE")) ctx->fused_combine = atoi(f);
+    if (const char* f = getenv("SS_ATTN_TC")) ctx->attn_tc = atoi(f);  // dev: 0 = mma.sync prefill tiles
     if (const char* f = getenv("SS_FUSE_ROPE")) ctx->fuse_rope = atoi(f);
     if (cudaMalloc(&ctx->sk_part, gemm_part_floats(ctx->num_sms) * 4) != cudaSuccess ||
         cudaMalloc(&ctx->sk_flags, gemm_flag_words(ctx->num_sms) * 4) != cudaSuccess ||

@@ -16,7 +16,10 @@ cases = {
     "chunk2016@0": [host.BatchEntry(0, P, 2016, 0)],
     "decodes64": [host.BatchEntry(i, D, 1, 4096) for i in range(64)],
 }
+only = os.environ.get("ONLY")
 for cname, ents in cases.items():
+    if only and cname not in only.split(","):
+        continue
     d = host.Descriptor.build(ents, vocab=shape.vocab)
     f.fill_descriptor_prefixes(d, seed=5)
     b = f.upload(d)
