@@ -684,7 +684,9 @@ ss_status enqueue_forward(ss_ctx* ctx, const ss_batch* b) {
             }));
         }
         const AttnParams ap = attn_params(ctx, b, ctx->q, ctx->o, l);
-        RUN(launch(ctx, SS_K_ATTN, 1, [&] { return attention_launch(ap, ctx->tm_k, ctx->tm_v, ctx->st); }));
+        // two kernels when the batch has both tensor-core prefill tiles and decode items
+        const int n_attn = (ap.tc && ap.n_tc > 0 && ap.n_items > ap.n_tc) ? 2 : 1;
+        RUN(launch(ctx, SS_K_ATTN, n_attn, [&] { return attention_launch(ap, ctx->tm_k, ctx->tm_v, ctx->st); }));
         if (b->n_combs && !ctx->fused_combine)
             RUN(launch(ctx, SS_K_ATTN_COMBINE, 1, [&] { return attention_combine_launch(ap, ctx->st); }));
         if (ctx->tp == 1) {

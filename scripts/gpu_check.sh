@@ -15,6 +15,8 @@ timeout 600 ncu --profile-from-start off --metrics gpu__time_duration.sum --cloc
     $PS > /dev/null 2>&1; echo "launches rc=$?"
 timeout 900 ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:gemm_tcgen05 -c 4 -o gpurun_out/prof_gemm -f \
     $PS > gpurun_out/ncu_gemm.log 2>&1; echo "ncu gemm rc=$?"
-timeout 600 ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:attention_kernel -c 1 -o gpurun_out/prof_attn -f \
-    $PS > gpurun_out/ncu_attn.log 2>&1; echo "ncu attn rc=$?"
+timeout 600 ncu --profile-from-start off --set full --clock-control none --import-source on --kernel-name-base mangled \
+    -k regex:attention_kernelILi128ELb0E -c 1 -o gpurun_out/prof_attn -f $PS > gpurun_out/ncu_attn.log 2>&1; echo "ncu attn rc=$?"
+timeout 600 ncu --profile-from-start off --set full --clock-control none --import-source on --kernel-name-base mangled \
+    -k regex:attention_kernelILi128ELb1E -c 1 -o gpurun_out/prof_attn_tc -f $PS > gpurun_out/ncu_attn_tc.log 2>&1; echo "ncu attn tc rc=$?"
 fi

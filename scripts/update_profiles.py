@@ -31,8 +31,10 @@ traffic = {}
 # the GEMM capture holds the 4 projections of one layer in forward order
 for cls, e in zip(["gemm_qkv", "gemm_o", "gemm_gate_up", "gemm_down"], d.get("prof_gemm.ncu-rep", [])):
     traffic[cls] = int(mb(e, "dram__bytes_read.sum") + mb(e, "dram__bytes_write.sum"))
-for e in d.get("prof_attn.ncu-rep", [])[:1]:
+for e in d.get("prof_attn.ncu-rep", [])[:1]:  # the decode (HBM-streaming) attention kernel
     traffic["attention"] = int(mb(e, "dram__bytes_read.sum") + mb(e, "dram__bytes_write.sum"))
+for e in d.get("prof_attn_tc.ncu-rep", [])[:1]:  # the tensor-core prefill attention kernel
+    traffic["attention_tc"] = int(mb(e, "dram__bytes_read.sum") + mb(e, "dram__bytes_write.sum"))
 out = {"_note": f"dram__bytes_read.sum + dram__bytes_write.sum per launch from `ncu --set full` captures "
                 f"(profiles/{rnd}/ncu_summary_{tag}.json); used by bench.py as roofline.traffic",
        "mistral7b": traffic}

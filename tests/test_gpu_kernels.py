@@ -199,15 +199,20 @@ ATTN_CASES = {
 }
 
 
+@pytest.mark.parametrize("tc", ["1", "0"])
 @pytest.mark.parametrize("case", list(ATTN_CASES))
-def test_mixed_attention(case):
+def test_mixed_attention(case, tc, monkeypatch):
+    """One launch pair over decodes, chunks at prefix 0 / 2500 / 5000 (the last split in
+    KV pieces + combine), a 1-token chunk and a short chunk. tc = 1: prefill row tiles
+    on the tcgen05 kernel (128 rows); tc = 0: the mma.sync row mode (64 rows)."""
+    monkeypatch.setenv("SS_ATTN_TC", tc)
     nq, nkv, hd = ATTN_CASES[case]
     shape = gpu.ModelShape("attn", 1, 256, nq, nkv, hd, 256, 512)
     f = gpu.HybridForward(shape, weight_seed=1)
     ents = [host.BatchEntry(0, "decode", 1, 4096), host.BatchEntry(1, "decode", 1, 37),
             host.BatchEntry(2, "decode", 1, 1000), host.BatchEntry(3, "prefill", 300, 0),
             host.BatchEntry(4, "prefill", 70, 2500), host.BatchEntry(5, "prefill", 1, 15),
-            host.BatchEntry(6, "prefill", 17, 0)]
+            host.BatchEntry(6, "prefill", 17, 0), host.BatchEntry(7, "prefill", 40, 5000)]
     d = host.Descriptor.build(ents, block_size=16, vocab=512)
     f.kv_alloc(d.pool_blocks + 8)
     kc, vc = f.kv_layer(0)
