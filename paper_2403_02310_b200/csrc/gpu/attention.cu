@@ -43,7 +43,6 @@ constexpr int kRowsPerTile = 64;
 constexpr int kStages = 3;  // 2 CTAs/SM x 2 tiles in flight = 128 KB of K/V outstanding per SM
 
 constexpr int kTcRows = 128;  // rows of a tensor-core (prefill) item
-constexpr int cmax(int a, int b) { return a > b ? a : b; }
 
 template <int HD>
 struct AttnSmem {
@@ -54,17 +53,27 @@ struct AttnSmem {
     // 256 B of barriers + 704 B of alignment slack (the dynamic window starts 1 KB-aligned
     // in practice; checked at run time) keep two decode CTAs per SM within 228 KB at hd = 128
     static constexpr int TOTAL = BAR_OFF + 256 + 704;
-    // tensor-core prefill kernel (tcgen05), one CTA per SM: Q [HD/64][128 rows][128 B],
-    // TC_STAGES K/V stages (deep: the K/V latency is the per-tile critical path), P [128
-    // rows][64 keys] bf16 — all SWIZZLE_128B, K-major (V read MN-major)
-    static constexpr int TC_Q = kTcRows * HD * 2;
-    static constexpr int TC_P_BYTES = 2 * kTcRows * kKeysPerTile * 2;  // double buffered
-    static constexpr int TC_STAGES_FIT = (232448 - 960 - 1024 - TC_Q - TC_P_BYTES) / STAGE;
-    static constexpr int TC_STAGES = TC_STAGES_FIT > 8 ? 8 : TC_STAGES_FIT;
-    static constexpr int TC_STAGE0 = TC_Q;
-    static constexpr int TC_P = TC_Q + TC_STAGES * STAGE;
-    static constexpr int TC_BAR = TC_P + TC_P_BYTES;
-    static constexpr int TC_TOTAL = TC_BAR + 256 + 704;
+};
+
+// Tensor-core prefill kernel smem: Q [HD/64][128 rows][128 B], STAGES K/V stages, NP
+// P buffers [128 rows][64 keys] bf16 — all SWIZZLE_128B, K-major (V read MN-major).
+// NP = 2 "deep": one CTA per SM, as many stages as fit (the K/V latency is the per-tile
+// critical path); NP = 1 "compact": the decode CTA's footprint, so it co-resides with the
+// decode kernel's CTAs and runs beside them.
+template <int HD, int NP>
+struct TcCfg {
+    using S = AttnSmem<HD>;
+    static constexpr int STAGE = S::STAGE;
+    static constexpr int Q = kTcRows * HD * 2;
+    static constexpr int P_ONE = kTcRows * kKeysPerTile * 2;
+    static constexpr int BUDGET = NP == 2 ? 232448 - 1024 : 115648;  // compact: half an SM
+    static constexpr int STAGES_FIT = (BUDGET - 960 - Q - NP * P_ONE) / STAGE;
+    static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
+    static constexpr int STAGE0 = Q;
+    static constexpr int P = Q + STAGES * STAGE;
+    static constexpr int BAR = P + NP * P_ONE;
+    static constexpr int TOTAL = BAR + 256 + 704;
+    static_assert(STAGES >= 2, "tensor-core attention needs two K/V stages");
 };
 
 // Q tile: rows of HD*2 bytes, 16-byte chunks XOR-swizzled by row.
@@ -308,22 +317,23 @@ __device__ __forceinline__ uint64_t umma_desc_sw128_mn(uint32_t smem_addr, uint3
 // S(t) = Q K(t)^T into TMEM buffer t & 1 and, once the softmax warps have published
 // P(t - 1) (mbarrier, one arrival per warp), O += P(t - 1) V(t - 1); P is double
 // buffered in smem, so softmax(t) overlaps PV(t - 1) and S(t + 1).
-template <int HD>
+template <int HD, int NP>
 __device__ __forceinline__ void mma_warp_tc(const AttnItem& it, uint8_t* smem, uint64_t* full, uint64_t* empty,
                                             uint64_t* sbar, uint64_t* obar, uint64_t* pready, uint32_t tbase) {
     using S = AttnSmem<HD>;
-    constexpr int NST = S::TC_STAGES;
+    using C = TcCfg<HD, NP>;
+    constexpr int NST = C::STAGES;
     const int nt = (it.key1 - it.key0 + kKeysPerTile - 1) / kKeysPerTile;
     constexpr uint32_t idS = umma_idesc_bf16(kTcRows, kKeysPerTile);
     constexpr uint32_t idO = umma_idesc_bf16(kTcRows, HD) | (1u << 16);  // B (V) MN-major
-    const uint32_t qa = smem_u32(smem), sa = smem_u32(smem + S::TC_STAGE0), pa = smem_u32(smem + S::TC_P);
+    const uint32_t qa = smem_u32(smem), sa = smem_u32(smem + C::STAGE0), pa = smem_u32(smem + C::P);
     const uint32_t tO = tbase + 128;
     auto issue_pv = [&](int u) {  // O += P(u) V(u)
         mbar_wait(&pready[u & 1], uint32_t((u >> 1) & 1));
         tc_fence_after();
         if (elect_lane()) {
             const uint32_t va = sa + (u % NST) * S::STAGE + S::KV_TILE;
-            const uint32_t pb = pa + (u & 1) * (kTcRows * kKeysPerTile * 2);
+            const uint32_t pb = pa + (u % NP) * C::P_ONE;
 #pragma unroll
             for (int kk = 0; kk < kKeysPerTile / 16; ++kk)
                 umma_bf16(tO, umma_desc_sw128(pb) + uint64_t(2 * kk),
@@ -354,11 +364,11 @@ __device__ __forceinline__ void mma_warp_tc(const AttnItem& it, uint8_t* smem, u
     if (nt > 0) issue_pv(nt - 1);
 }
 
-template <int HD>
+template <int HD, int NP>
 __device__ __forceinline__ void softmax_warps_tc(const AttnParams& p, const AttnItem& it, uint8_t* smem,
                                                  uint64_t* sbar, uint64_t* obar, uint64_t* pready, uint32_t tbase,
                                                  int warp, int lane) {
-    using S = AttnSmem<HD>;
+    using C = TcCfg<HD, NP>;
     const int r = warp * 32 + lane;  // row of the tile == TMEM lane
     const int e = it.entry;
     const int tok0 = p.cu_q[e];
@@ -410,9 +420,9 @@ __device__ __forceinline__ void softmax_warps_tc(const AttnParams& p, const Attn
             pk[j] = pack_bf16(p0, p1);
         }
         l = l * alpha + (ls0 + ls1);
-        // P buffer t & 1 was read by PV(t - 2); a rescale of O needs PV(t - 1) retired
-        if (t >= 2) {
-            mbar_wait(&obar[t & 1], uint32_t(((t - 2) >> 1) & 1));
+        // P buffer t % NP was read by PV(t - NP); a rescale of O needs PV(t - 1) retired
+        if (t >= NP) {
+            mbar_wait(&obar[(t - NP) & 1], uint32_t(((t - NP) >> 1) & 1));
             tc_fence_after();
         }
         if (__any_sync(0xffffffffu, alpha != 1.f)) {
@@ -430,7 +440,7 @@ __device__ __forceinline__ void softmax_warps_tc(const AttnParams& p, const Attn
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         }
         // P row -> smem (K-major SWIZZLE_128B: 16-byte chunk j of row r at j ^ (r & 7))
-        uint4* prow = reinterpret_cast<uint4*>(smem + S::TC_P + (t & 1) * (kTcRows * kKeysPerTile * 2) + r * 128);
+        uint4* prow = reinterpret_cast<uint4*>(smem + C::P + (t % NP) * C::P_ONE + r * 128);
 #pragma unroll
         for (int j = 0; j < 8; ++j) prow[j ^ (r & 7)] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -470,11 +480,15 @@ __device__ __forceinline__ void softmax_warps_tc(const AttnParams& p, const Attn
     }
 }
 
-template <int HD, bool TC>
-__global__ void __launch_bounds__((kWarps + 1 + TC) * 32) attention_kernel(const AttnParams p,
+// MODE 0: decode / mma.sync items; 1: tensor-core prefill, deep; 2: tensor-core prefill, compact.
+template <int HD, int MODE>
+__global__ void __launch_bounds__((kWarps + 1 + (MODE > 0)) * 32) attention_kernel(const AttnParams p,
                                                                       const __grid_constant__ CUtensorMap tmK,
                                                                       const __grid_constant__ CUtensorMap tmV) {
     using S = AttnSmem<HD>;
+    constexpr bool TC = MODE > 0;
+    constexpr int NP = MODE == 2 ? 1 : 2;
+    using C = TcCfg<HD, NP>;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t pad = ((raw + 1023u) & ~1023u) - raw;
@@ -486,15 +500,15 @@ __global__ void __launch_bounds__((kWarps + 1 + TC) * 32) attention_kernel(const
     constexpr bool tc = TC;  // prefill row tile on the tensor cores
     // barrier block (256 B): full[8] empty[8] | split flag | S-ready[2] | PV-done[2] | P-ready[2] | TMEM slot
     constexpr int kMaxSt = 8;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (TC ? S::TC_BAR : S::BAR_OFF));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (TC ? C::BAR : S::BAR_OFF));
     uint64_t* empty = full + kMaxSt;
     int* split_flag = reinterpret_cast<int*>(full + 2 * kMaxSt);
     uint64_t* sbar = full + 2 * kMaxSt + 1;
     uint64_t* obar = sbar + 2;    // [2]
     uint64_t* pready = obar + 2;  // [2] softmax warps -> MMA warp: P(t) published (by t & 1)
     uint32_t* tslot = reinterpret_cast<uint32_t*>(pready + 2);
-    const int nst = tc ? S::TC_STAGES : kStages;
-    const int st0 = tc ? S::TC_STAGE0 : S::Q_BYTES;
+    const int nst = tc ? C::STAGES : kStages;
+    const int st0 = tc ? C::STAGE0 : S::Q_BYTES;
 
     if (threadIdx.x == 0) {
         tma_prefetch(&tmK);
@@ -513,11 +527,16 @@ __global__ void __launch_bounds__((kWarps + 1 + TC) * 32) attention_kernel(const
     }
     if constexpr (TC) {
         if (warp == 0) tmem_alloc<256>(tslot);  // S double buffer (2 x 64 cols) + O (HD cols)
-        pdl_wait();  // q / KV of this layer come from the preceding kernels
-        pdl_launch_dependents();  // only now: the decode launch relies on this wait
-    } else {
+    }
+    // Grid dependencies (see attention_launch): the first of the two attention launches
+    // waits for the QKV kernel and triggers its dependent only after that wait; the second
+    // skips the start wait (its CTAs exist only once every CTA of the first has waited) and
+    // waits at its end, so its completion covers both.
+    if (p.wait_at_end) {
         pdl_launch_dependents();
-        if (!p.wait_at_end) pdl_wait();
+    } else {
+        pdl_wait();  // q / KV of this layer come from the preceding kernels
+        pdl_launch_dependents();
     }
     // stage the Q tile (rows beyond nrows are zero)
     {
@@ -585,16 +604,17 @@ __global__ void __launch_bounds__((kWarps + 1 + TC) * 32) attention_kernel(const
             }
             __syncwarp();
         }
-        if (!TC && p.wait_at_end) pdl_wait();
+        if (p.wait_at_end) pdl_wait();
         return;
     }
 
     if constexpr (TC) {
         if (warp == kWarps + 1) {
-            mma_warp_tc<HD>(it, smem, full, empty, sbar, obar, pready, *tslot);
+            mma_warp_tc<HD, NP>(it, smem, full, empty, sbar, obar, pready, *tslot);
             return;
         }
-        softmax_warps_tc<HD>(p, it, smem, sbar, obar, pready, *tslot, warp, lane);
+        softmax_warps_tc<HD, NP>(p, it, smem, sbar, obar, pready, *tslot, warp, lane);
+        if (p.wait_at_end) pdl_wait();
         if (p.fused_combine) finish_split<HD>(p, it, split_flag);
         tc_fence_before();
         asm volatile("bar.sync 1, %0;" ::"n"(kWarps * 32) : "memory");
@@ -691,29 +711,41 @@ template <int HD>
 cudaError_t launch_hd(const AttnParams& p, const CUtensorMap& tk, const CUtensorMap& tv, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(attention_kernel<HD, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             AttnSmem<HD>::TC_TOTAL);
+        cudaError_t e = cudaFuncSetAttribute(attention_kernel<HD, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             TcCfg<HD, 2>::TOTAL);
         if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(attention_kernel<HD, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            e = cudaFuncSetAttribute(attention_kernel<HD, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     TcCfg<HD, 1>::TOTAL);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(attention_kernel<HD, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      AttnSmem<HD>::TOTAL);
         if (e != cudaSuccess) return e;
         attr = true;
     }
     // items[0, n_tc): tensor-core prefill tiles; the rest: decode / mma.sync items
     const int n_tc = p.tc ? p.n_tc : 0, n_rest = p.n_items - n_tc;
-    if (n_tc > 0) {
-        cudaError_t e = launch_pdl(attention_kernel<HD, true>, dim3(n_tc), dim3((kWarps + 2) * 32),
-                                   AttnSmem<HD>::TC_TOTAL, st, 1, p, tk, tv);
+    AttnParams pt = p, pd = p;
+    pd.items = p.items + n_tc;
+    const dim3 bt((kWarps + 2) * 32), bd((kWarps + 1) * 32);
+    if (n_tc > 0 && n_rest >= p.num_sms) {
+        // enough HBM-streaming decode CTAs to fill the machine: they go first, and the
+        // compact prefill CTAs run beside them (in the SMs' remaining shared memory)
+        pd.wait_at_end = 0;
+        pt.wait_at_end = 1;
+        cudaError_t e = launch_pdl(attention_kernel<HD, 0>, dim3(n_rest), bd, AttnSmem<HD>::TOTAL, st, 1, pd, tk, tv);
         if (e != cudaSuccess) return e;
+        return launch_pdl(attention_kernel<HD, 2>, dim3(n_tc), bt, TcCfg<HD, 1>::TOTAL, st, 1, pt, tk, tv);
     }
-    if (n_rest > 0) {
-        AttnParams q = p;
-        q.items = p.items + n_tc;
-        q.wait_at_end = n_tc > 0;
-        return launch_pdl(attention_kernel<HD, false>, dim3(n_rest), dim3((kWarps + 1) * 32), AttnSmem<HD>::TOTAL, st,
-                          1, q, tk, tv);
+    if (n_tc > 0) {  // prefill-heavy: the deep prefill kernel first, the decodes beside / after it
+        pt.wait_at_end = 0;
+        cudaError_t e = launch_pdl(attention_kernel<HD, 1>, dim3(n_tc), bt, TcCfg<HD, 2>::TOTAL, st, 1, pt, tk, tv);
+        if (e != cudaSuccess || n_rest == 0) return e;
+        pd.wait_at_end = 1;
+    } else {
+        pd.wait_at_end = 0;
     }
-    return cudaSuccess;
+    return n_rest > 0 ? launch_pdl(attention_kernel<HD, 0>, dim3(n_rest), bd, AttnSmem<HD>::TOTAL, st, 1, pd, tk, tv)
+                      : cudaSuccess;
 }
 
 }  // namespace

@@ -547,6 +547,7 @@ AttnParams attn_params(const ss_ctx* ctx, const ss_batch* b, const bf16* q, bf16
     p.n_items = b->n_items;
     p.n_tc = b->n_tc;
     p.wait_at_end = 0;
+    p.num_sms = ctx->num_sms;
     p.part_o = ctx->part_o;
     p.part_ml = ctx->part_ml;
     p.comb_count = ctx->comb_count;

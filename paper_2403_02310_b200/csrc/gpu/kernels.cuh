@@ -118,7 +118,8 @@ struct AttnParams {
     int32_t fused_combine;       // 1: last split merges in-kernel; 0: attention_combine launch
     int32_t tc;                  // 1: prefill row tiles (128 rows) on tcgen05; 0: mma.sync (64 rows)
     int32_t n_tc;                // items[0, n_tc) are the tcgen05 tiles (launched first)
-    int32_t wait_at_end;         // set by attention_launch for the launch that follows the tc one
+    int32_t wait_at_end;         // set by attention_launch for the second of its two launches
+    int32_t num_sms;
 };
 // 2D TMA views [L * nblocks * nkv * 16][hd] of the K and V pools (box 16 x 64, SWIZZLE_128B).
 bool attention_tmaps(CUtensorMap* tk, CUtensorMap* tv, const void* kc, const void* vc, int64_t total_rows, int hd);
