@@ -966,7 +966,7 @@ cudaError_t launch_t(const GemmPlan& p, cudaStream_t st) {
     if (mode < 0) mode = S > 1 ? 2 : 0;
     if (const char* f = getenv("SS_GEMM_SK")) mode = atoi(f);
     if (const char* f = getenv("SS_GEMM_SPLITS")) S = atoi(f);
-    if (mode == 3 && (CG != 2 || num_mt > resident)) mode = 0;
+    if (mode == 3 && num_mt > resident) mode = 0;
     const int rem = tiles % resident;  // tiles of the ragged last wave
     if (mode == 2 && rem > 0 && long(rem) * S > resident) S = resident / rem;
     if (mode == 2 && (S < 2 || rem == 0)) mode = 0;  // nothing to split
@@ -1038,10 +1038,13 @@ GemmShape gemm_pick(int M, int N, int K, int epi, int num_sms) {
         const long slots = num_sms / cg;
         const long full = tiles / slots, rem = tiles % slots;
         const double t1 = tile_us(cg, bn) * kscale, epi_us = 3.0 + 0.07 * bn;
-        if (cg == 2 && num_mt <= slots && (force_mode < 0 || force_mode == 3)) {
+        if (num_mt <= slots && (force_mode < 0 || force_mode == 3)) {
             const long gs = slots / num_mt, nkb = (K + BK - 1) / BK;
             const long per = (num_n * nkb + gs - 1) / gs;
-            const double cost = double(per) / 64.0 * 1.18 * tile_us(cg, bn) + epi_us + 6.0;
+            // (single-CTA tiles at M <= 128 are weight-streaming bound per SM; their split
+            // partials cost ~10 us more than the spread saves unless K is long: decode-only
+            // sweep, profiles/r01/gemm_class_sweep.txt)
+            const double cost = double(per) / 64.0 * 1.18 * tile_us(cg, bn) + epi_us + 6.0 + (cg == 1 ? 10.0 : 0.0);
             if (cost < best_cost - 1e-9) {
                 best_cost = cost;
                 best = GemmShape{cg, bn, 1, 3};

@@ -7,14 +7,20 @@ model = sys.argv[1] if len(sys.argv) > 1 else "mistral7b"
 tau = sys.argv[2] if len(sys.argv) > 2 else "512"
 layers = sys.argv[3] if len(sys.argv) > 3 else "8"
 cands = [(0, 256), (0, 128), (0, 192), (0, 224), (3, 256), (3, 192), (3, 128), (3, 224), (2, 256, 2), (2, 256, 4), (2, 128, 2)]
-classes = {"QKV": ("gemm_qkv", 128), "O": ("gemm_o", 32), "GATEUP": ("gemm_gate_up", 64), "DOWN": ("gemm_down", 32)}
+if os.environ.get("CANDS"):
+    cands = [tuple(int(v) for v in c.split(",")) for c in os.environ["CANDS"].split(";")]
+classes = {"QKV": ("gemm_qkv", 128), "O": ("gemm_o", 32), "GATEUP": ("gemm_gate_up", 64), "DOWN": ("gemm_down", 32),
+           "LMHEAD": ("lm_head", 32)}
 code = r'''
 import sys, os, json
 sys.path.insert(0, os.environ["ROOT"])
 from paper_2403_02310_b200 import gpu, host
 shape = gpu.MODELS[sys.argv[1]].with_layers(int(sys.argv[3]))
 f = gpu.HybridForward(shape, weight_seed=1234)
-d = host.Descriptor.canonical(int(sys.argv[2]), 32, 4096, 0, vocab=shape.vocab)
+if int(sys.argv[2]) == 0:  # decode-only: 32 decodes at 4096
+    d = host.Descriptor.build([host.BatchEntry(i, "decode", 1, 4096) for i in range(32)], vocab=shape.vocab)
+else:
+    d = host.Descriptor.canonical(int(sys.argv[2]), 32, 4096, 0, vocab=shape.vocab)
 f.kv_alloc(d.pool_blocks)
 f.fill_descriptor_prefixes(d, seed=5)
 b = f.upload(d)
