@@ -55,26 +55,47 @@ struct AttnSmem {
     static constexpr int TOTAL = BAR_OFF + 256 + 704;
 };
 
-// Tensor-core prefill kernel smem: Q [HD/64][128 rows][128 B], STAGES K/V stages, NP
-// P buffers [128 rows][64 keys] bf16 — all SWIZZLE_128B, K-major (V read MN-major).
-// NP = 2 "deep": one CTA per SM, as many stages as fit (the K/V latency is the per-tile
-// critical path); NP = 1 "compact": the decode CTA's footprint, so it co-resides with the
-// decode kernel's CTAs and runs beside them.
-template <int HD, int NP>
+// Tensor-core prefill kernel smem: NH halves of 128 rows, each with its Q [HD/64][128
+// rows][128 B] and NP P buffers [128 rows][64 keys] bf16, and STAGES K/V stages shared by
+// the halves — all SWIZZLE_128B, K-major (V read MN-major).
+//   MODE 1 "paired" (NH = 2, NP = 2): one CTA per SM; two row tiles of the same (entry,
+//     kv head) share every K/V tile and their softmax warps interleave on the SM (when the
+//     256-row items still fill the machine).
+//   MODE 3 "deep" (NH = 1, NP = 2): one CTA per SM, 128-row tiles, 5 K/V stages.
+//   MODE 2 "compact" (NH = 1, NP = 1): the decode CTA's footprint, so it co-resides with
+//     the decode kernel's CTAs and runs beside them.
+template <int HD, int MODE>
 struct TcCfg {
     using S = AttnSmem<HD>;
+    static constexpr int NH = MODE == 1 ? 2 : 1;
+    static constexpr int NP = MODE == 2 ? 1 : 2;
     static constexpr int STAGE = S::STAGE;
-    static constexpr int Q = kTcRows * HD * 2;
+    static constexpr int QH = kTcRows * HD * 2;           // one half's Q
     static constexpr int P_ONE = kTcRows * kKeysPerTile * 2;
-    static constexpr int BUDGET = NP == 2 ? 232448 - 1024 : 115648;  // compact: half an SM
-    static constexpr int STAGES_FIT = (BUDGET - 960 - Q - NP * P_ONE) / STAGE;
+    static constexpr int BUDGET = MODE != 2 ? 232448 - 1024 : 115648;  // compact: half an SM
+    static constexpr int STAGES_FIT = (BUDGET - 960 - NH * (QH + NP * P_ONE)) / STAGE;
     static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
-    static constexpr int STAGE0 = Q;
-    static constexpr int P = Q + STAGES * STAGE;
-    static constexpr int BAR = P + NP * P_ONE;
+    static constexpr int STAGE0 = NH * QH;
+    static constexpr int P = STAGE0 + STAGES * STAGE;     // half h's buffers at P + h * NP * P_ONE
+    static constexpr int BAR = P + NH * NP * P_ONE;
     static constexpr int TOTAL = BAR + 256 + 704;
+    static constexpr int THREADS = (4 * NH + 2) * 32;     // softmax warps, producer, MMA issuer
     static_assert(STAGES >= 2, "tensor-core attention needs two K/V stages");
 };
+
+// Per-half barriers of the tensor-core kernel: S ready [2], PV done [2], P published [2].
+struct TcBars {
+    uint64_t *sbar, *obar, *pready;
+};
+// K/V tiles half h needs: through the causal limit of its last row (>= 1 tile if it has rows).
+__device__ __forceinline__ int tc_tiles(const AttnParams& p, const AttnItem& it, int h) {
+    const int nr = min(max(it.nrows - h * kTcRows, 0), kTcRows);
+    if (nr == 0) return 0;
+    const int e = it.entry;
+    const int prefix = p.ctx_len[e] - (p.cu_q[e + 1] - p.cu_q[e]);
+    const int kneed = min(prefix + (it.row0 + h * kTcRows + nr - 1) / p.group + 1, it.key1);
+    return max(1, (kneed - it.key0 + kKeysPerTile - 1) / kKeysPerTile);
+}
 
 // Q tile: rows of HD*2 bytes, 16-byte chunks XOR-swizzled by row.
 template <int HD>
@@ -317,66 +338,86 @@ __device__ __forceinline__ uint64_t umma_desc_sw128_mn(uint32_t smem_addr, uint3
 // S(t) = Q K(t)^T into TMEM buffer t & 1 and, once the softmax warps have published
 // P(t - 1) (mbarrier, one arrival per warp), O += P(t - 1) V(t - 1); P is double
 // buffered in smem, so softmax(t) overlaps PV(t - 1) and S(t + 1).
-template <int HD, int NP>
-__device__ __forceinline__ void mma_warp_tc(const AttnItem& it, uint8_t* smem, uint64_t* full, uint64_t* empty,
-                                            uint64_t* sbar, uint64_t* obar, uint64_t* pready, uint32_t tbase) {
+template <int HD, int MODE>
+__device__ __forceinline__ void mma_warp_tc(const AttnParams& p, const AttnItem& it, uint8_t* smem, uint64_t* full,
+                                            uint64_t* empty, const TcBars (&bars)[2], uint32_t tbase) {
     using S = AttnSmem<HD>;
-    using C = TcCfg<HD, NP>;
-    constexpr int NST = C::STAGES;
-    const int nt = (it.key1 - it.key0 + kKeysPerTile - 1) / kKeysPerTile;
+    using C = TcCfg<HD, MODE>;
+    constexpr int NST = C::STAGES, NH = C::NH, NP = C::NP;
+    int nth[2] = {tc_tiles(p, it, 0), NH > 1 ? tc_tiles(p, it, 1) : 0};
+    const int nt = max(nth[0], nth[1]);
     constexpr uint32_t idS = umma_idesc_bf16(kTcRows, kKeysPerTile);
     constexpr uint32_t idO = umma_idesc_bf16(kTcRows, HD) | (1u << 16);  // B (V) MN-major
     const uint32_t qa = smem_u32(smem), sa = smem_u32(smem + C::STAGE0), pa = smem_u32(smem + C::P);
-    const uint32_t tO = tbase + 128;
-    auto issue_pv = [&](int u) {  // O += P(u) V(u)
-        mbar_wait(&pready[u & 1], uint32_t((u >> 1) & 1));
-        tc_fence_after();
-        if (elect_lane()) {
-            const uint32_t va = sa + (u % NST) * S::STAGE + S::KV_TILE;
-            const uint32_t pb = pa + (u % NP) * C::P_ONE;
+    for (int t = 0; t <= nt; ++t) {
+        if (t < nt) {  // S_h(t) = Q_h K(t)^T into half h's TMEM buffer t & 1
+            // (S buffer t & 1 was last read by softmax(t - 2): P(t - 2) was awaited before PV(t - 2))
+            const int st = t % NST;
+            mbar_wait(&full[st], uint32_t((t / NST) & 1));
+            tc_fence_after();
+            if (elect_lane()) {
+                const uint32_t ka = sa + st * S::STAGE;
 #pragma unroll
-            for (int kk = 0; kk < kKeysPerTile / 16; ++kk)
-                umma_bf16(tO, umma_desc_sw128(pb) + uint64_t(2 * kk),
-                          umma_desc_sw128_mn(va + kk * 16 * 128, kKeysPerTile * 128), idO, (u > 0 || kk > 0) ? 1u : 0u);
-            umma_commit(&obar[u & 1]);
-            umma_commit(&empty[u % NST]);  // K/V stage free once S(u) and PV(u) retire
-        }
-        __syncwarp();
-    };
-    for (int t = 0; t < nt; ++t) {
-        const int st = t % NST;
-        // (S buffer t & 1 was last read by softmax(t - 2): P(t - 2) was awaited before PV(t - 2))
-        mbar_wait(&full[st], uint32_t((t / NST) & 1));
-        tc_fence_after();
-        if (elect_lane()) {
-            const uint32_t ka = sa + st * S::STAGE;
+                for (int h = 0; h < NH; ++h) {
+                    if (t >= nth[h]) continue;
 #pragma unroll
-            for (int ks = 0; ks < HD / 16; ++ks) {
-                const int hh = ks >> 2, kk = ks & 3;
-                umma_bf16(tbase + uint32_t((t & 1) * 64), umma_desc_sw128(qa + hh * kTcRows * 128) + uint64_t(2 * kk),
-                          umma_desc_sw128(ka + hh * kKeysPerTile * 128) + uint64_t(2 * kk), idS, ks > 0 ? 1u : 0u);
+                    for (int ks = 0; ks < HD / 16; ++ks) {
+                        const int hh = ks >> 2, kk = ks & 3;
+                        umma_bf16(tbase + uint32_t(h * 256 + (t & 1) * 64),
+                                  umma_desc_sw128(qa + h * C::QH + hh * kTcRows * 128) + uint64_t(2 * kk),
+                                  umma_desc_sw128(ka + hh * kKeysPerTile * 128) + uint64_t(2 * kk), idS, ks > 0 ? 1u : 0u);
+                    }
+                    umma_commit(&bars[h].sbar[t & 1]);
+                }
             }
-            umma_commit(&sbar[t & 1]);
+            __syncwarp();
         }
-        __syncwarp();
-        if (t >= 1) issue_pv(t - 1);
+        if (t >= 1) {  // O_h += P_h(u) V(u), u = t - 1, once half h published P_h(u)
+            const int u = t - 1;
+            const uint32_t va = sa + (u % NST) * S::STAGE + S::KV_TILE;
+#pragma unroll
+            for (int h = 0; h < NH; ++h) {
+                if (u >= nth[h]) continue;
+                mbar_wait(&bars[h].pready[u & 1], uint32_t((u >> 1) & 1));
+                tc_fence_after();
+                if (elect_lane()) {
+                    const uint32_t pb = pa + (h * NP + u % NP) * C::P_ONE;
+#pragma unroll
+                    for (int kk = 0; kk < kKeysPerTile / 16; ++kk)
+                        umma_bf16(tbase + uint32_t(h * 256 + 128), umma_desc_sw128(pb) + uint64_t(2 * kk),
+                                  umma_desc_sw128_mn(va + kk * 16 * 128, kKeysPerTile * 128), idO,
+                                  (u > 0 || kk > 0) ? 1u : 0u);
+                    umma_commit(&bars[h].obar[u & 1]);
+                }
+                __syncwarp();
+            }
+            if (elect_lane()) umma_commit(&empty[u % NST]);  // K/V stage free once S(u), PV(u) retire
+            __syncwarp();
+        }
     }
-    if (nt > 0) issue_pv(nt - 1);
 }
 
-template <int HD, int NP>
+template <int HD, int MODE>
 __device__ __forceinline__ void softmax_warps_tc(const AttnParams& p, const AttnItem& it, uint8_t* smem,
-                                                 uint64_t* sbar, uint64_t* obar, uint64_t* pready, uint32_t tbase,
-                                                 int warp, int lane) {
-    using C = TcCfg<HD, NP>;
-    const int r = warp * 32 + lane;  // row of the tile == TMEM lane
+                                                 const TcBars (&bars)[2], uint32_t tbase0, int warp, int lane) {
+    using C = TcCfg<HD, MODE>;
+    constexpr int NP = C::NP;
+    const int h = warp >> 2, wq = warp & 3;  // half of the item, TMEM lane quarter
+    const int nt = tc_tiles(p, it, h);
+    if (nt == 0) return;  // this half has no rows
+    // (the halves' barriers are contiguous, 6 per half: no dynamic indexing of `bars`)
+    uint64_t* sbar = bars[0].sbar + 6 * h;
+    uint64_t* obar = bars[0].obar + 6 * h;
+    uint64_t* pready = bars[0].pready + 6 * h;
+    const uint32_t tbase = tbase0 + uint32_t(h * 256);
+    const int r = h * kTcRows + wq * 32 + lane;  // row of the item
+    const int rl = wq * 32 + lane;               // row of the half == TMEM lane
     const int e = it.entry;
     const int tok0 = p.cu_q[e];
     const int ntok = p.cu_q[e + 1] - tok0;
     const int prefix = p.ctx_len[e] - ntok;
     const int lim = r < it.nrows ? prefix + (it.row0 + r) / p.group : -1;  // last visible key
-    const int nt = (it.key1 - it.key0 + kKeysPerTile - 1) / kKeysPerTile;
-    const uint32_t lane_base = uint32_t(warp * 32) << 16;
+    const uint32_t lane_base = uint32_t(wq * 32) << 16;
     const uint32_t tO = tbase + 128;
     float m = -INFINITY, l = 0.f;
     for (int t = 0; t < nt; ++t) {
@@ -440,9 +481,9 @@ __device__ __forceinline__ void softmax_warps_tc(const AttnParams& p, const Attn
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         }
         // P row -> smem (K-major SWIZZLE_128B: 16-byte chunk j of row r at j ^ (r & 7))
-        uint4* prow = reinterpret_cast<uint4*>(smem + C::P + (t % NP) * C::P_ONE + r * 128);
+        uint4* prow = reinterpret_cast<uint4*>(smem + C::P + (h * NP + t % NP) * C::P_ONE + rl * 128);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) prow[j ^ (r & 7)] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+        for (int j = 0; j < 8; ++j) prow[j ^ (rl & 7)] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         tc_fence_before();
         __syncwarp();
@@ -482,13 +523,14 @@ __device__ __forceinline__ void softmax_warps_tc(const AttnParams& p, const Attn
 
 // MODE 0: decode / mma.sync items; 1: tensor-core prefill, deep; 2: tensor-core prefill, compact.
 template <int HD, int MODE>
-__global__ void __launch_bounds__((kWarps + 1 + (MODE > 0)) * 32) attention_kernel(const AttnParams p,
+__global__ void __launch_bounds__(MODE > 0 ? TcCfg<HD, MODE>::THREADS : (kWarps + 1) * 32) attention_kernel(const AttnParams p,
                                                                       const __grid_constant__ CUtensorMap tmK,
                                                                       const __grid_constant__ CUtensorMap tmV) {
     using S = AttnSmem<HD>;
     constexpr bool TC = MODE > 0;
-    constexpr int NP = MODE == 2 ? 1 : 2;
-    using C = TcCfg<HD, NP>;
+    using C = TcCfg<HD, MODE == 0 ? 2 : MODE>;
+    constexpr int NH = TC ? C::NH : 1;
+    constexpr int kProd = TC ? 4 * NH : kWarps;  // producer warp; the tc MMA warp follows it
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t pad = ((raw + 1023u) & ~1023u) - raw;
@@ -498,15 +540,15 @@ __global__ void __launch_bounds__((kWarps + 1 + (MODE > 0)) * 32) attention_kern
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool key_mode = !TC && it.nrows <= 16;
     constexpr bool tc = TC;  // prefill row tile on the tensor cores
-    // barrier block (256 B): full[8] empty[8] | split flag | S-ready[2] | PV-done[2] | P-ready[2] | TMEM slot
+    // barrier block (256 B): full[8] empty[8] | split flag | per half {S-ready[2] PV-done[2]
+    // P-ready[2]} | TMEM slot
     constexpr int kMaxSt = 8;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + (TC ? C::BAR : S::BAR_OFF));
     uint64_t* empty = full + kMaxSt;
     int* split_flag = reinterpret_cast<int*>(full + 2 * kMaxSt);
-    uint64_t* sbar = full + 2 * kMaxSt + 1;
-    uint64_t* obar = sbar + 2;    // [2]
-    uint64_t* pready = obar + 2;  // [2] softmax warps -> MMA warp: P(t) published (by t & 1)
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(pready + 2);
+    uint64_t* hb = full + 2 * kMaxSt + 1;
+    const TcBars bars[2] = {{hb, hb + 2, hb + 4}, {hb + 6, hb + 8, hb + 10}};
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(hb + 12);
     const int nst = tc ? C::STAGES : kStages;
     const int st0 = tc ? C::STAGE0 : S::Q_BYTES;
 
@@ -517,16 +559,14 @@ __global__ void __launch_bounds__((kWarps + 1 + (MODE > 0)) * 32) attention_kern
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], tc ? 1 : kWarps);  // tc: released by a tcgen05.commit
         }
-        mbar_init(&sbar[0], 1);
-        mbar_init(&sbar[1], 1);
-        mbar_init(&obar[0], 1);
-        mbar_init(&obar[1], 1);
-        mbar_init(&pready[0], kWarps);
-        mbar_init(&pready[1], kWarps);
+        for (int i = 0; i < 12; ++i) mbar_init(&hb[i], (i % 6) >= 4 ? 4 : 1);  // P-ready: 4 softmax warps
         mbar_fence_init();
     }
-    if constexpr (TC) {
-        if (warp == 0) tmem_alloc<256>(tslot);  // S double buffer (2 x 64 cols) + O (HD cols)
+    if constexpr (TC) {  // per half: S double buffer (2 x 64 cols) + O (HD cols)
+        if (warp == 0) {
+            if constexpr (NH == 2) tmem_alloc<512>(tslot);
+            else tmem_alloc<256>(tslot);
+        }
     }
     // Grid dependencies (see attention_launch): the first of the two attention launches
     // waits for the QKV kernel and triggers its dependent only after that wait; the second
@@ -542,11 +582,13 @@ __global__ void __launch_bounds__((kWarps + 1 + (MODE > 0)) * 32) attention_kern
     {
         constexpr int CH = HD / 8;
         const int e = it.entry, tok0 = p.cu_q[e];
-        const int nr = key_mode ? 16 : (tc ? kTcRows : kRowsPerTile);
+        const int nr = key_mode ? 16 : (tc ? NH * kTcRows : kRowsPerTile);
         for (int idx = threadIdx.x; idx < nr * CH; idx += blockDim.x) {
             const int r = idx / CH, c = idx % CH;
-            // tc: UMMA K-major SWIZZLE_128B image [c / 8][row][128 B]
-            const uint32_t so = smem_u32(smem) + (tc ? uint32_t((c >> 3) * (kTcRows * 128) + r * 128 + (((c & 7) ^ (r & 7)) << 4))
+            // tc: per half, UMMA K-major SWIZZLE_128B image [c / 8][row][128 B]
+            const int rh = r & (kTcRows - 1);
+            const uint32_t so = smem_u32(smem) + (tc ? uint32_t((r / kTcRows) * C::QH + (c >> 3) * (kTcRows * 128) + rh * 128 +
+                                                                (((c & 7) ^ (rh & 7)) << 4))
                                                    : swz_q<HD>(r, c));
             if (r < it.nrows) {
                 const int gr = it.row0 + r;
@@ -569,11 +611,12 @@ __global__ void __launch_bounds__((kWarps + 1 + (MODE > 0)) * 32) attention_kern
         }
     }
 
-    if (warp == kWarps) {  // ---- producer warp: K/V pages by TMA into the ring
+    if (warp == kProd) {  // ---- producer warp: K/V pages by TMA into the ring
         // Block ids come 32 pages (8 tiles) at a time from one coalesced warp load,
         // fetched a batch ahead, and reach the issuing lane by shuffle: no dependent
         // global load sits between two tiles' TMA issues.
-        const int ntiles = (it.key1 - it.key0 + kKeysPerTile - 1) / kKeysPerTile;
+        const int ntiles = TC ? max(tc_tiles(p, it, 0), NH > 1 ? tc_tiles(p, it, 1) : 0)
+                              : (it.key1 - it.key0 + kKeysPerTile - 1) / kKeysPerTile;
         const int32_t* bt = p.block_table + size_t(it.entry) * p.max_blocks;
         const int nvalid = (p.ctx_len[it.entry] + 15) >> 4;
         const int pg0 = it.key0 >> 4;  // key0 is a multiple of 64
@@ -609,18 +652,19 @@ __global__ void __launch_bounds__((kWarps + 1 + (MODE > 0)) * 32) attention_kern
     }
 
     if constexpr (TC) {
-        if (warp == kWarps + 1) {
-            mma_warp_tc<HD, NP>(it, smem, full, empty, sbar, obar, pready, *tslot);
+        if (warp == kProd + 1) {
+            mma_warp_tc<HD, MODE>(p, it, smem, full, empty, bars, *tslot);
             return;
         }
-        softmax_warps_tc<HD, NP>(p, it, smem, sbar, obar, pready, *tslot, warp, lane);
+        softmax_warps_tc<HD, MODE>(p, it, smem, bars, *tslot, warp, lane);
         if (p.wait_at_end) pdl_wait();
-        if (p.fused_combine) finish_split<HD>(p, it, split_flag);
+        if (NH == 1 && p.fused_combine) finish_split<HD>(p, it, split_flag);
         tc_fence_before();
-        asm volatile("bar.sync 1, %0;" ::"n"(kWarps * 32) : "memory");
+        asm volatile("bar.sync 1, %0;" ::"n"(NH * kWarps * 32) : "memory");
         if (warp == 0) {
             tc_fence_after();
-            tmem_dealloc<256>(*tslot);
+            if constexpr (NH == 2) tmem_dealloc<512>(*tslot);
+            else tmem_dealloc<256>(*tslot);
         }
         return;
     } else {
@@ -712,10 +756,13 @@ cudaError_t launch_hd(const AttnParams& p, const CUtensorMap& tk, const CUtensor
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(attention_kernel<HD, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             TcCfg<HD, 2>::TOTAL);
+                                             TcCfg<HD, 1>::TOTAL);
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(attention_kernel<HD, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     TcCfg<HD, 1>::TOTAL);
+                                     TcCfg<HD, 2>::TOTAL);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(attention_kernel<HD, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     TcCfg<HD, 3>::TOTAL);
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(attention_kernel<HD, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      AttnSmem<HD>::TOTAL);
@@ -726,19 +773,24 @@ cudaError_t launch_hd(const AttnParams& p, const CUtensorMap& tk, const CUtensor
     const int n_tc = p.tc ? p.n_tc : 0, n_rest = p.n_items - n_tc;
     AttnParams pt = p, pd = p;
     pd.items = p.items + n_tc;
-    const dim3 bt((kWarps + 2) * 32), bd((kWarps + 1) * 32);
-    if (n_tc > 0 && n_rest >= p.num_sms) {
+    const dim3 bd((kWarps + 1) * 32);
+    if (n_tc > 0 && p.tc == 2) {
         // enough HBM-streaming decode CTAs to fill the machine: they go first, and the
         // compact prefill CTAs run beside them (in the SMs' remaining shared memory)
         pd.wait_at_end = 0;
         pt.wait_at_end = 1;
         cudaError_t e = launch_pdl(attention_kernel<HD, 0>, dim3(n_rest), bd, AttnSmem<HD>::TOTAL, st, 1, pd, tk, tv);
         if (e != cudaSuccess) return e;
-        return launch_pdl(attention_kernel<HD, 2>, dim3(n_tc), bt, TcCfg<HD, 1>::TOTAL, st, 1, pt, tk, tv);
+        return launch_pdl(attention_kernel<HD, 2>, dim3(n_tc), dim3(TcCfg<HD, 2>::THREADS), TcCfg<HD, 2>::TOTAL, st, 1,
+                          pt, tk, tv);
     }
     if (n_tc > 0) {  // prefill-heavy: the deep prefill kernel first, the decodes beside / after it
         pt.wait_at_end = 0;
-        cudaError_t e = launch_pdl(attention_kernel<HD, 1>, dim3(n_tc), bt, TcCfg<HD, 2>::TOTAL, st, 1, pt, tk, tv);
+        cudaError_t e =
+            p.tc == 1 ? launch_pdl(attention_kernel<HD, 1>, dim3(n_tc), dim3(TcCfg<HD, 1>::THREADS), TcCfg<HD, 1>::TOTAL,
+                                   st, 1, pt, tk, tv)
+                      : launch_pdl(attention_kernel<HD, 3>, dim3(n_tc), dim3(TcCfg<HD, 3>::THREADS), TcCfg<HD, 3>::TOTAL,
+                                   st, 1, pt, tk, tv);
         if (e != cudaSuccess || n_rest == 0) return e;
         pd.wait_at_end = 1;
     } else {

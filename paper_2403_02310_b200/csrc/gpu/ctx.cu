@@ -110,6 +110,7 @@ struct ss_batch {
     AttnItem* items = nullptr;
     AttnCombine* combs = nullptr;
     int n_items = 0, n_combs = 0, part_rows = 0, n_tc = 0;
+    int tc_mode = 0;  // AttnParams::tc of this batch
 };
 
 // Tensor parallelism on ONE device, for validating the sharded forward where only
@@ -364,8 +365,19 @@ ss_status ensure_workspace(ss_ctx* ctx, int T, int n_out, int part_rows) {
 
 // Work list of the mixed attention launch (see attention.cu).
 void build_items(const ss_ctx* ctx, const ss_batch_desc* d, std::vector<AttnItem>& items,
-                 std::vector<AttnCombine>& combs, int& part_rows, int& n_tc) {
+                 std::vector<AttnCombine>& combs, int& part_rows, int& n_tc, int& tc_mode) {
     const int G = ctx->G;
+    // Tensor-core prefill flavour: with at least an SM's worth of HBM-streaming decode
+    // items, compact 128-row tiles that run beside them (2); else deep 256-row tiles
+    // (two 128-row halves per CTA sharing K/V, 1); 0: mma.sync 64-row tiles.
+    int dec_pairs = 0, pairs256 = 0;
+    for (int e = 0; e < d->num_entries; ++e) {
+        const int rows = (d->cu_q[e + 1] - d->cu_q[e]) * G;
+        if (rows <= 16) dec_pairs += ctx->nkv_l;
+        else pairs256 += (rows + 255) / 256 * ctx->nkv_l;
+    }
+    // deep flavours: paired 256-row items when they alone fill the SMs, else 128-row ones (3)
+    tc_mode = !ctx->attn_tc ? 0 : dec_pairs >= ctx->num_sms ? 2 : pairs256 >= ctx->num_sms ? 1 : 3;
     struct Tile {
         int e, row0, nr, extent;
     };
@@ -375,7 +387,7 @@ void build_items(const ss_ctx* ctx, const ss_batch_desc* d, std::vector<AttnItem
         const int ntok = d->cu_q[e + 1] - d->cu_q[e];
         const int prefix = d->ctx_len[e] - ntok;
         const int rows = ntok * G;
-        const int tile = rows <= 16 ? 16 : (ctx->attn_tc ? 128 : 64);
+        const int tile = rows <= 16 ? 16 : (tc_mode == 1 ? 256 : tc_mode != 0 ? 128 : 64);
         for (int row0 = 0; row0 < rows; row0 += tile) {
             const int nr = std::min(tile, rows - row0);
             tiles.push_back(Tile{e, row0, nr, prefix + (row0 + nr - 1) / G + 1});
@@ -421,7 +433,7 @@ void build_items(const ss_ctx* ctx, const ss_batch_desc* d, std::vector<AttnItem
     // longest items first so the tail of the launch is short (SS_ATTN_ORDER=1,
     // dev: prefill row tiles first)
     static const int order = getenv("SS_ATTN_ORDER") ? atoi(getenv("SS_ATTN_ORDER")) : 0;
-    const bool tc_items = ctx->attn_tc != 0;
+    const bool tc_items = tc_mode != 0;
     std::stable_sort(items.begin(), items.end(), [tc_items](const AttnItem& a, const AttnItem& b) {
         if (order == 1 && (a.nrows > 16) != (b.nrows > 16)) return a.nrows > 16;
         // per-key cost: decode streaming ~16, mma.sync row tile ~64, tcgen05 row tile ~8
@@ -476,8 +488,8 @@ ss_status upload(ss_ctx* ctx, const ss_batch_desc* d, ss_batch* b) {
     if (ss_status s = validate(ctx, d)) return s;
     std::vector<AttnItem> items;
     std::vector<AttnCombine> combs;
-    int part_rows = 0, n_tc = 0;
-    build_items(ctx, d, items, combs, part_rows, n_tc);
+    int part_rows = 0, n_tc = 0, tc_mode = 0;
+    build_items(ctx, d, items, combs, part_rows, n_tc, tc_mode);
     const int E = d->num_entries, T = d->num_tokens;
     struct Seg {
         const void* src;
@@ -528,6 +540,7 @@ ss_status upload(ss_ctx* ctx, const ss_batch_desc* d, ss_batch* b) {
     b->max_blocks = d->max_blocks;
     b->n_items = int(items.size());
     b->n_tc = n_tc;
+    b->tc_mode = tc_mode;
     b->n_combs = int(combs.size());
     b->part_rows = part_rows;
     return ensure_workspace(ctx, T, std::max(d->n_out, 1), part_rows);
@@ -552,7 +565,7 @@ AttnParams attn_params(const ss_ctx* ctx, const ss_batch* b, const bf16* q, bf16
     p.part_ml = ctx->part_ml;
     p.comb_count = ctx->comb_count;
     p.fused_combine = ctx->fused_combine;
-    p.tc = ctx->attn_tc;
+    p.tc = b->tc_mode;
     p.combines = b->combs;
     p.n_combines = b->n_combs;
     p.nq_l = ctx->nq_l;
@@ -823,6 +836,7 @@ static ss_status create_impl(const ss_model_cfg* cfg, int32_t tp_rank, int32_t t
     if (const char* f = getenv("SS_ATTN_SPLIT")) ctx->decode_split = std::max(64, atoi(f) / 64 * 64);  // dev tuning
     if (const char* f = getenv("SS_ATTN_FUSED_COMBINE")) ctx->fused_combine = atoi(f);
     if (const char* f = getenv("SS_ATTN_TC")) ctx->attn_tc = atoi(f);  // dev: 0 = mma.sync prefill tiles
+    if (ctx->fused_combine) ctx->attn_tc = 0;  // the in-kernel split merge exists on the mma.sync path only
     if (const char* f = getenv("SS_FUSE_ROPE")) ctx->fuse_rope = atoi(f);
     if (cudaMalloc(&ctx->sk_part, gemm_part_floats(ctx->num_sms) * 4) != cudaSuccess ||
         cudaMalloc(&ctx->sk_flags, gemm_flag_words(ctx->num_sms) * 4) != cudaSuccess ||

@@ -80,7 +80,7 @@ struct AttnItem {
     int32_t entry;
     int32_t kv_head;
     int32_t row0;      // first row of the tile
-    int32_t nrows;     // rows in the tile (<= 16: key-split decode mode; else <= 128 tcgen05 / 64 mma.sync)
+    int32_t nrows;     // rows in the tile (<= 16: key-split decode mode; else tcgen05 <= 256 / mma.sync <= 64)
     int32_t key0;      // key range [key0, key1)
     int32_t key1;
     int32_t part;      // -1: final output; else partial slot base (rows)
@@ -116,7 +116,8 @@ struct AttnParams {
     int64_t layer_row0;          // first row of this layer in the 2D [rows][hd] TMA view of the cache
     int32_t* comb_count;         // per split group: finished splits (zeroed, self-resetting)
     int32_t fused_combine;       // 1: last split merges in-kernel; 0: attention_combine launch
-    int32_t tc;                  // 1: prefill row tiles (128 rows) on tcgen05; 0: mma.sync (64 rows)
+    int32_t tc;                  // prefill row tiles: 0 mma.sync (64 rows); tcgen05 1 paired (256), 2 compact
+                                 // (128, beside the decodes), 3 deep (128)
     int32_t n_tc;                // items[0, n_tc) are the tcgen05 tiles (launched first)
     int32_t wait_at_end;         // set by attention_launch for the second of its two launches
     int32_t num_sms;
