@@ -350,6 +350,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     pdl_launch_dependents();
+    if constexpr (EPI == EPI_QKV) {
+        if (sk_mode == 0 && gid >= num_tiles) {  // no tile for this pair: warm L2 for attention
+            // (the cached pages are final: no kernel of this step writes them before attention)
+            const int per = ea.pf_pages * 2 * ea.nkv;  // not used; pages are walked per item below
+            (void)per;
+            const int nthreads = (G - num_tiles) * CG * kThreads;
+            const int tid = ((gid - num_tiles) * CG + int(rank)) * kThreads + int(threadIdx.x);
+            const size_t page = size_t(ea.bs) * ea.hd;  // elements of one (block, head) page
+            for (int w = tid; w < ea.pf_n * ea.pf_pages * 2; w += nthreads) {
+                const int i = w / (ea.pf_pages * 2), pg = (w >> 1) % ea.pf_pages, kv = w & 1;
+                const AttnItem itm = ea.pf_items[i];
+                const int lb = (itm.key0 >> 4) + pg;
+                if (lb * ea.bs >= itm.key1 || lb * ea.bs >= ea.pf_ctx_len[itm.entry]) continue;
+                const int32_t blk = ea.pf_bt[size_t(itm.entry) * ea.pf_max_blocks + lb];
+                const __nv_bfloat16* src = (kv ? ea.vc : ea.kc) + (size_t(blk) * ea.nkv + itm.kv_head) * page;
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(uint32_t(page * 2))
+                             : "memory");
+            }
+        }
+    }
     // Programmatic dependent launch: A (activations) and the residual come from the
     // preceding kernels, so the producer and the epilogue warps wait for them; the
     // MMA warp only consumes shared memory and needs no wait.
@@ -971,7 +991,7 @@ cudaError_t launch_t(const GemmPlan& p, cudaStream_t st) {
     if (mode == 2 && rem > 0 && long(rem) * S > resident) S = resident / rem;
     if (mode == 2 && (S < 2 || rem == 0)) mode = 0;  // nothing to split
     int groups = resident;
-    if (mode == 0 && tiles < groups) groups = tiles;
+    if (mode == 0 && tiles < groups && !(p.epi == EPI_QKV && p.ea.pf_n > 0)) groups = tiles;
     if (mode == 1 && iters < groups) groups = int(iters);
     if (mode == 2 && tiles < resident) groups = tiles * S;
     if (mode == 3) {  // whole super-groups (one member per M-tile), each with >= 1 k-block

@@ -15,6 +15,7 @@ namespace ssk {
 enum { EPI_BF16 = 0, EPI_RESADD = 1, EPI_SWIGLU = 2, EPI_F32 = 3, EPI_QKV = 4 };
 
 // Extra epilogue operands (all optional / mode specific).
+struct AttnItem;
 struct EpiArgs {
     // RMSNorm folded into the consumer GEMM: A holds the un-normalised bf16 rows;
     // each output row is scaled by rsqrt(sum(ssq_in[row][0..ssq_in_n)) * inv_dim + eps)
@@ -34,6 +35,13 @@ struct EpiArgs {
     __nv_bfloat16* kc = nullptr;
     __nv_bfloat16* vc = nullptr;
     int nq = 0, nkv = 0, hd = 0, bs = 16;
+    // EPI_QKV, whole-tile schedule: CTA pairs beyond the tile count warm L2 with the first
+    // pf_pages K/V pages of this layer's decode attention items (the cache that the
+    // attention launch after this GEMM streams first), while the GEMM runs
+    const struct AttnItem* pf_items = nullptr;
+    int pf_n = 0, pf_pages = 0, pf_max_blocks = 0;
+    const int32_t* pf_bt = nullptr;
+    const int32_t* pf_ctx_len = nullptr;
 };
 
 struct GemmPlan {
