@@ -232,7 +232,9 @@ def run_ours(args):
             continue
         ent = {"ms_per_step": ms / args.steps, "launches_per_step": n / args.steps, "share": ms / prof_total}
         pl = work["per_layer"]
-        avg = ms / n
+        # per-layer classes: time per layer (attention is one or two kernel launches per layer)
+        per_layer_cls = k in ("gemm_qkv", "gemm_o", "gemm_gate_up", "gemm_down", "attention")
+        avg = ms / args.steps / L if per_layer_cls else ms / n
         if k in ("gemm_qkv", "gemm_o", "gemm_gate_up", "gemm_down", "lm_head"):
             ent["tflops"] = pl[k] / (avg * 1e-3) / 1e12
         if k == "attention":
