@@ -279,3 +279,43 @@ def test_prefill_paired_tiles(nq, nkv, hd):
     assert err.max().item() < 2e-2, f"max abs err {err.max().item()}"
     b.free()
     f.close()
+
+
+@pytest.mark.parametrize("env", [{"SS_GEMM_SK": "3", "SS_GEMM_BN": "128"}, {"SS_GEMM_SK": "3", "SS_GEMM_BN": "256"},
+                                 {"SS_GEMM_SPLITS": "4", "SS_GEMM_BN": "128"}])
+@pytest.mark.parametrize("M", [33, 100])
+@pytest.mark.parametrize("epi", [0, 1, 2, 3])
+def test_gemm_small_m_split_schedules(small, monkeypatch, env, M, epi):
+    """Single-CTA (M <= 128) tiles through stream-K and split-K: every epilogue, values and
+    bitwise repeatability (decode-only batches take these schedules)."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    N, K = (2048 if epi == 2 else 1024), 4096
+    A = _rand((M, K), 1.0, 31)
+    B = _rand((N, K), 1.0 / math.sqrt(K), 32)
+    ref = A.float() @ B.float().T
+    outs = []
+    for _ in range(2):
+        if epi == 0:
+            D = torch.empty((M, N), dtype=torch.bfloat16, device="cuda")
+        elif epi == 1:
+            D = torch.ones((M, N), device="cuda")
+        elif epi == 2:
+            D = torch.empty((M, N // 2), dtype=torch.bfloat16, device="cuda")
+        else:
+            D = torch.empty((M, N), dtype=torch.float32, device="cuda")
+        small.k_gemm(A, B, D, M, N, K, epi)
+        torch.cuda.synchronize()
+        outs.append(D)
+    assert torch.equal(outs[0], outs[1])
+    D = outs[0]
+    if epi == 0:
+        torch.testing.assert_close(D.float(), ref, rtol=1e-2, atol=1e-2)
+    elif epi == 1:
+        torch.testing.assert_close(D, 1.0 + ref, rtol=1e-4, atol=1e-4)
+    elif epi == 2:
+        r = ref.view(M, N // 64, 2, 32)
+        want = (torch.nn.functional.silu(r[:, :, 0]) * r[:, :, 1]).reshape(M, N // 2)
+        torch.testing.assert_close(D.float(), want, rtol=2e-2, atol=2e-2)
+    else:
+        torch.testing.assert_close(D, ref, rtol=2e-4, atol=2e-4)
