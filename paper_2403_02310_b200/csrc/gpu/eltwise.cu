@@ -157,11 +157,19 @@ __global__ void argmax_kernel(const float* __restrict__ logits, int V, int ld, i
     const float* r = logits + size_t(blockIdx.x) * ld;
     float best = -INFINITY;
     int bi = 0x7fffffff;
-    for (int i = threadIdx.x; i < V; i += blockDim.x) {
-        const float v = r[i];
-        if (v > best || (v == best && i < bi)) {
-            best = v;
-            bi = i;
+    // 8 independent loads in flight per thread per step (the scan is latency-bound)
+    const int step = blockDim.x * 8;
+    for (int i0 = threadIdx.x; i0 < V; i0 += step) {
+        float v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = i0 + k * blockDim.x < V ? __ldg(r + i0 + k * blockDim.x) : -INFINITY;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int i = i0 + k * blockDim.x;
+            if (v[k] > best || (v[k] == best && i < bi)) {  // ascending i per thread: ties keep the lowest
+                best = v[k];
+                bi = i;
+            }
         }
     }
 #pragma unroll

@@ -353,8 +353,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     if constexpr (EPI == EPI_QKV) {
         if (sk_mode == 0 && gid >= num_tiles) {  // no tile for this pair: warm L2 for attention
             // (the cached pages are final: no kernel of this step writes them before attention)
-            const int per = ea.pf_pages * 2 * ea.nkv;  // not used; pages are walked per item below
-            (void)per;
             const int nthreads = (G - num_tiles) * CG * kThreads;
             const int tid = ((gid - num_tiles) * CG + int(rank)) * kThreads + int(threadIdx.x);
             const size_t page = size_t(ea.bs) * ea.hd;  // elements of one (block, head) page
