@@ -139,11 +139,18 @@ def run_ours(args):
     if args.layers:
         shape = shape.with_layers(args.layers)
     nccl_id = None
-    if world > 1:
+    if world > 1 and args.tp_comm == "nccl":
         buf = [gpu.nccl_unique_id() if rank == 0 else None]
         pg.broadcast_object_list(buf, src=0)
         nccl_id = buf[0]
     fwd = gpu.HybridForward(shape, tp_rank=rank, tp_size=world, nccl_id=nccl_id, weight_seed=1234, device=local)
+    if world > 1 and args.tp_comm == "ipc":
+        def allgather(b):
+            out = [None] * world
+            pg.all_gather_object(out, b)
+            return out
+
+        fwd.ipc_connect(allgather, max_tokens=max(8192, args.tau))
     desc = host.Descriptor.canonical(args.tau, 32, 4096, args.chunk_prefix, vocab=shape.vocab, token_seed=7)
     arrays = desc.arrays()
     fwd.kv_alloc(desc.pool_blocks)
@@ -282,7 +289,8 @@ def run_ours(args):
                    "model": f"{args.model}-shaped (L={L}, h={shape.hidden}, q={shape.num_q_heads}, "
                             f"kv={shape.num_kv_heads}, hd={shape.head_dim}, ffn={shape.ffn}, V={shape.vocab})",
                    "token_budget": args.tau, "tokens_per_step": T, "logit_rows": work["n_out"],
-                   "parallelism": f"tp{world}", "l2": "inputs larger than L2 (all weights + KV re-read every step)",
+                   "parallelism": f"tp{world}" + (f" ({args.tp_comm} all-reduce)" if world > 1 else ""),
+                   "l2": "inputs larger than L2 (all weights + KV re-read every step)",
                    "gpu_launches_per_step": launches / args.steps},
         "e2e": {"value": T / (e2e_ms * 1e-3), "unit": "tokens/s", "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "api": "ss_forward_hybrid (host descriptor arrays -> next tokens)"},
@@ -426,6 +434,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--tbt-requests", type=int, default=48, help="closed-loop P99 TBT trace size (0: skip)")
     ap.add_argument("--tbt-qps", type=float, default=4.0)
+    ap.add_argument("--tp-comm", choices=["ipc", "nccl"], default="ipc",
+                    help="tp > 1 transport: CUDA-IPC peer-memory all-reduce fused with the residual add (default) "
+                         "or NCCL all-reduce + residual-add kernel")
     ap.add_argument("--profile-step", action="store_true",
                     help="profiling only: after warm-up run one step between cudaProfilerStart/Stop and exit")
     args = ap.parse_args()

@@ -80,6 +80,17 @@ void ss_destroy(ss_ctx* ctx);
 ss_status ss_model_config(const ss_ctx* ctx, ss_model_cfg* out, int32_t* tp_rank, int32_t* tp_size);
 ss_status ss_nccl_unique_id(void* out_128_bytes);
 
+/* CUDA-IPC tensor-parallel transport, the alternative to NCCL (create the rank with
+ * nccl_id = NULL): each rank exports its exchange region (two bf16 [max_tokens][hidden]
+ * all-reduce buffers, an fp32 LM-head shard buffer, barrier flags) as a 64-byte
+ * cudaIpcMemHandle_t, the caller all-gathers the handles (any out-of-band channel),
+ * and every rank opens all of them (handles[r] = rank r's, rank order). The row-parallel
+ * O / down projections then write their partials into the exchange buffer and one fused
+ * kernel sums every rank's partial over peer memory (fixed rank order: identical on all
+ * ranks) into the residual; the vocab shards are gathered the same way. */
+ss_status ss_ipc_export(ss_ctx* ctx, int32_t max_tokens, void* handle_out_64_bytes);
+ss_status ss_ipc_open(ss_ctx* ctx, const void* handles);
+
 /* Paged KV pool: num_blocks blocks of block_size tokens for every layer and
  * this rank's KV heads. Layout per layer: [num_blocks][kv_heads_local][bs][hd]
  * bf16 for K and for V. */

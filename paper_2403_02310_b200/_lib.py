@@ -148,6 +148,8 @@ def gpu_lib():
         _sig(lib, "ss_destroy", None, [P])
         _sig(lib, "ss_model_config", I32, [P, C.POINTER(ModelCfg), C.POINTER(I32), C.POINTER(I32)])
         _sig(lib, "ss_nccl_unique_id", I32, [P])
+        _sig(lib, "ss_ipc_export", I32, [P, I32, P])
+        _sig(lib, "ss_ipc_open", I32, [P, P])
         _sig(lib, "ss_kv_alloc", I32, [P, I64, I32])
         _sig(lib, "ss_forward_hybrid", I32, [P, C.POINTER(BatchDesc), P, P, C.POINTER(F)])
         _sig(lib, "ss_create_local_group", I32, [C.POINTER(ModelCfg), I32, C.c_uint64, I32, C.POINTER(P)])
@@ -224,7 +226,7 @@ def host_check(status: int) -> None:
 
 
 GPU_EXPORTS = [
-    "ss_create", "ss_create_local_group", "ss_forward_local_group", "ss_destroy", "ss_model_config", "ss_nccl_unique_id", "ss_kv_alloc", "ss_forward_hybrid",
+    "ss_create", "ss_create_local_group", "ss_forward_local_group", "ss_destroy", "ss_model_config", "ss_nccl_unique_id", "ss_ipc_export", "ss_ipc_open", "ss_kv_alloc", "ss_forward_hybrid",
     "ss_batch_upload", "ss_forward_enqueue", "ss_read_outputs", "ss_batch_free", "ss_stream", "ss_synchronize",
     "ss_kv_fill_synthetic", "ss_set_profiling", "ss_kernel_times", "ss_kernel_class_name", "ss_launch_count",
     "ss_last_error", "ss_k_gemm", "ss_k_rmsnorm", "ss_k_rope_append", "ss_k_attention", "ss_kv_layer_ptrs",

@@ -201,6 +201,16 @@ struct ss_ctx {
     ncclComm_t comm = nullptr;
     LocalGroup* grp = nullptr;  // set instead of comm for a one-device TP group
     bf16* part_red = nullptr;   // local-group all-reduce result
+    // CUDA-IPC transport (ss_ipc_export / ss_ipc_open): this rank's exchange region and the
+    // mapped views of every rank's
+    uint8_t* ipc_region = nullptr;
+    size_t ipc_bytes = 0;
+    int ipc_tcap = 0;
+    int ipc = 0;                 // 1 once every peer is mapped
+    IpcPeers ipc_peers{};
+    void* ipc_mapped[kIpcMaxRanks] = {};
+    uint32_t ipc_epoch = 0;      // collectives so far (identical sequence on every rank)
+    uint32_t ipc_ar = 0;         // all-reduces so far (exchange buffer = ipc_ar & 1)
 
     bool prof = false;
     std::vector<Prof> pend;
@@ -657,7 +667,32 @@ ss_status allgather_logits(ss_ctx* ctx, int n_out) {
     });
 }
 
+// IPC region layout: [exchange buffer 0 | exchange buffer 1] (T_cap x h bf16 each) |
+// logits shard (T_cap x vocab_l fp32) | flags (kIpcMaxRanks u32, 256 B slot)
+size_t ipc_buf_bytes(const ss_ctx* ctx) { return (size_t(ctx->ipc_tcap) * ctx->h * 2 + 255) & ~size_t(255); }
+size_t ipc_logits_off(const ss_ctx* ctx) { return 2 * ipc_buf_bytes(ctx); }
+size_t ipc_flags_off(const ss_ctx* ctx) {
+    return ipc_logits_off(ctx) + ((size_t(ctx->ipc_tcap) * ctx->vocab_l * 4 + 255) & ~size_t(255));
+}
+
+// Row-parallel projection + all-reduce + residual add over CUDA IPC: the GEMM writes this
+// rank's bf16 partial into exchange buffer (all-reduce count & 1); one fused kernel then
+// waits for every rank, sums all partials from peer memory in rank order and adds them.
+ss_status ipc_project_allreduce(ss_ctx* ctx, int cls, const CUtensorMap& ta, WMaps& tb, int T, int K) {
+    if (T > ctx->ipc_tcap) return fail(ctx, SS_INVALID_ARG, "batch larger than the IPC exchange capacity");
+    const int slot = int(ctx->ipc_ar & 1u);
+    bf16* mine = reinterpret_cast<bf16*>(ctx->ipc_region + slot * ipc_buf_bytes(ctx));
+    if (ss_status s = gemm(ctx, cls, ta, tb, T, ctx->h, K, mine, ctx->h, EPI_BF16)) return s;
+    ++ctx->ipc_ar;
+    const uint32_t ep = ++ctx->ipc_epoch;
+    return launch(ctx, SS_K_ALLREDUCE, 1, [&] {
+        return ipc_allreduce_residual_launch(ctx->x, ctx->ipc_peers, slot, ep, ctx->xb, ctx->ssq, T, ctx->h, ctx->st);
+    });
+}
+
 ss_status enqueue_forward(ss_ctx* ctx, const ss_batch* b) {
+    if (ctx->tp > 1 && !ctx->grp && !ctx->comm && !ctx->ipc)
+        return fail(ctx, SS_INVALID_ARG, "tp > 1 needs an NCCL id at ss_create or the IPC transport (ss_ipc_open)");
     const int T = b->T, h = ctx->h;
     const int qkvN = (ctx->nq_l + 2 * ctx->nkv_l) * ctx->hd, qd = ctx->nq_l * ctx->hd;
     const float eps = ctx->cfg.rms_eps;
@@ -721,6 +756,8 @@ ss_status enqueue_forward(ss_ctx* ctx, const ss_batch* b) {
             RUN(launch(ctx, SS_K_ATTN_COMBINE, 1, [&] { return attention_combine_launch(ap, ctx->st); }));
         if (ctx->tp == 1) {
             RUN(gemm(ctx, SS_K_GEMM_O, ctx->ta_o, W.tb_o, T, h, qd, ctx->x, h, EPI_RESADD, res_out));
+        } else if (ctx->ipc) {
+            RUN(ipc_project_allreduce(ctx, SS_K_GEMM_O, ctx->ta_o, W.tb_o, T, qd));
         } else {
             RUN(gemm(ctx, SS_K_GEMM_O, ctx->ta_o, W.tb_o, T, h, qd, ctx->part, h, EPI_BF16));
             const bf16* sum = nullptr;
@@ -732,6 +769,8 @@ ss_status enqueue_forward(ss_ctx* ctx, const ss_batch* b) {
                  norm_in));
         if (ctx->tp == 1) {
             RUN(gemm(ctx, SS_K_GEMM_DOWN, ctx->ta_act, W.tb_down, T, h, ctx->ffn_l, ctx->x, h, EPI_RESADD, res_out));
+        } else if (ctx->ipc) {
+            RUN(ipc_project_allreduce(ctx, SS_K_GEMM_DOWN, ctx->ta_act, W.tb_down, T, ctx->ffn_l));
         } else {
             RUN(gemm(ctx, SS_K_GEMM_DOWN, ctx->ta_act, W.tb_down, T, h, ctx->ffn_l, ctx->part, h, EPI_BF16));
             const bf16* sum = nullptr;
@@ -744,10 +783,16 @@ ss_status enqueue_forward(ss_ctx* ctx, const ss_batch* b) {
         RUN(launch(ctx, SS_K_RMSNORM, 1, [&] {
             return rmsnorm_launch(ctx->x, ctx->final_norm, ctx->xo, b->out_rows, b->n_out, h, eps, ctx->st);
         }));
-        RUN(gemm(ctx, SS_K_LMHEAD, ctx->ta_xo, ctx->tb_lm, b->n_out, ctx->vocab_l, h, ctx->logits_l, ctx->vocab_l,
-                 EPI_F32));
+        float* lg = ctx->ipc ? reinterpret_cast<float*>(ctx->ipc_region + ipc_logits_off(ctx)) : ctx->logits_l;
+        RUN(gemm(ctx, SS_K_LMHEAD, ctx->ta_xo, ctx->tb_lm, b->n_out, ctx->vocab_l, h, lg, ctx->vocab_l, EPI_F32));
         const float* full = ctx->logits_l;
-        if (ctx->tp > 1) {
+        if (ctx->ipc) {  // every rank's vocab shard, read over peer memory after a flag barrier
+            const uint32_t ep = ++ctx->ipc_epoch;
+            RUN(launch(ctx, SS_K_ALLREDUCE, 1, [&] {
+                return ipc_gather_logits_launch(ctx->ipc_peers, ep, ctx->logits, b->n_out, ctx->vocab_l, ctx->st);
+            }));
+            full = ctx->logits;
+        } else if (ctx->tp > 1) {
             RUN(allgather_logits(ctx, b->n_out));
             RUN(launch(ctx, SS_K_ARGMAX, 1, [&] {
                 return gather_vocab_launch(ctx->logits_g, ctx->logits, ctx->tp, b->n_out, ctx->vocab_l, ctx->st);
@@ -803,6 +848,54 @@ SS_API ss_status ss_nccl_unique_id(void* out) {
     ncclUniqueId id;
     NK(g_nccl.get_id(&id));
     std::memcpy(out, &id, sizeof(id));
+    return SS_OK;
+}
+
+// ---------------------------------------------------------------- CUDA-IPC TP transport
+
+SS_API ss_status ss_ipc_export(ss_ctx* ctx, int32_t max_tokens, void* handle_out) {
+    if (!ctx || !handle_out || max_tokens < 1 || ctx->tp < 2 || ctx->grp)
+        return fail(ctx, SS_INVALID_ARG, "ss_ipc_export needs a tp > 1 rank context and max_tokens >= 1");
+    CK(cudaSetDevice(ctx->device));
+    if (!ctx->ipc_region) {
+        ctx->ipc_tcap = max_tokens;
+        ctx->ipc_bytes = ipc_flags_off(ctx) + 256;
+        CK(cudaMalloc(&ctx->ipc_region, ctx->ipc_bytes));
+        CK(cudaMemset(ctx->ipc_region + ipc_flags_off(ctx), 0, 256));
+    } else if (max_tokens != ctx->ipc_tcap) {
+        return fail(ctx, SS_INVALID_ARG, "ss_ipc_export: capacity already set");
+    }
+    cudaIpcMemHandle_t hd;
+    CK(cudaIpcGetMemHandle(&hd, ctx->ipc_region));
+    std::memcpy(handle_out, &hd, sizeof(hd));
+    return SS_OK;
+}
+
+SS_API ss_status ss_ipc_open(ss_ctx* ctx, const void* handles) {
+    if (!ctx || !handles || !ctx->ipc_region) return fail(ctx, SS_INVALID_ARG, "ss_ipc_open needs ss_ipc_export first");
+    if (ctx->tp > kIpcMaxRanks) return fail(ctx, SS_INVALID_ARG, "IPC transport supports up to 8 ranks");
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaStreamSynchronize(ctx->st));
+    IpcPeers pe{};
+    pe.n = ctx->tp;
+    pe.rank = ctx->rank;
+    for (int r = 0; r < ctx->tp; ++r) {
+        uint8_t* base = ctx->ipc_region;
+        if (r != ctx->rank) {
+            cudaIpcMemHandle_t hd;
+            std::memcpy(&hd, static_cast<const uint8_t*>(handles) + size_t(r) * sizeof(hd), sizeof(hd));
+            void* p = nullptr;
+            CK(cudaIpcOpenMemHandle(&p, hd, cudaIpcMemLazyEnablePeerAccess));
+            ctx->ipc_mapped[r] = p;
+            base = static_cast<uint8_t*>(p);
+        }
+        pe.buf[r][0] = reinterpret_cast<const bf16*>(base);
+        pe.buf[r][1] = reinterpret_cast<const bf16*>(base + ipc_buf_bytes(ctx));
+        pe.logits[r] = reinterpret_cast<const float*>(base + ipc_logits_off(ctx));
+        pe.flags[r] = reinterpret_cast<uint32_t*>(base + ipc_flags_off(ctx));
+    }
+    ctx->ipc_peers = pe;
+    ctx->ipc = 1;
     return SS_OK;
 }
 
@@ -935,9 +1028,9 @@ static ss_status create_impl(const ss_model_cfg* cfg, int32_t tp_rank, int32_t t
             return bail(fail(ctx, SS_OUT_OF_MEMORY, "rope table"));
         cudaMemcpy(ctx->rope, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice);
     }
-    if (tp_size > 1 && !grp) {
+    // without an NCCL id a tp rank runs on the CUDA-IPC transport (ss_ipc_export / ss_ipc_open)
+    if (tp_size > 1 && !grp && nccl_id) {
         std::string why;
-        if (!nccl_id) return bail(fail(ctx, SS_INVALID_ARG, "tp_size > 1 needs an NCCL unique id"));
         if (!g_nccl.load(why)) return bail(fail(ctx, SS_NCCL_ERROR, why));
         ncclUniqueId id;
         std::memcpy(&id, nccl_id, sizeof(id));
@@ -1023,6 +1116,9 @@ SS_API void ss_destroy(ss_ctx* ctx) {
     if (!ctx) return;
     if (ctx->st) cudaStreamSynchronize(ctx->st);
     if (ctx->comm) g_nccl.destroy(ctx->comm);
+    for (int r = 0; r < kIpcMaxRanks; ++r)
+        if (ctx->ipc_mapped[r]) cudaIpcCloseMemHandle(ctx->ipc_mapped[r]);
+    if (ctx->ipc_region) cudaFree(ctx->ipc_region);
     cudaFree(ctx->wmem);
     cudaFree(ctx->rope);
     cudaFree(ctx->sk_part);

@@ -2,6 +2,8 @@
 // synthetic initialisers. All are HBM-bound: 16-byte vector accesses along the
 // contiguous hidden / head dimension, warp-shuffle reductions.
 #include "../../../include/ss_synth.h"
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -145,6 +147,82 @@ __global__ void residual_add_kernel(float* __restrict__ x, const __nv_bfloat16* 
             const int64_t row = i / (h / 8), g = i % (h / 8);
             ssq[row * (h / 32) + g / 4] = ss;
         }
+    }
+}
+
+// ---- CUDA-IPC tensor parallelism: one-shot all-reduce fused with the residual add.
+// Every rank's row-parallel GEMM wrote its bf16 partial into its own exchange buffer;
+// after a flag barrier over peer memory each rank reads all ranks' partials (NVLink
+// P2P loads, fixed rank order: the sum is bitwise identical on every rank), adds them in
+// fp32 to the residual and emits the bf16 copy and per-chunk sums of squares.
+__device__ __forceinline__ void ipc_barrier(const IpcPeers& pe, uint32_t epoch) {
+    // one thread per CTA: CTA 0 signals every rank (its own flag slot in each rank's
+    // array), then every CTA waits for all ranks' flags of this epoch
+    if (threadIdx.x == 0) {
+        if (blockIdx.x == 0) {
+            __threadfence_system();
+            for (int r = 0; r < pe.n; ++r)
+                asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(pe.flags[r] + pe.rank), "r"(epoch) : "memory");
+        }
+        for (int r = 0; r < pe.n; ++r) {
+            uint32_t v, spins = 0;
+            do {
+                asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(pe.flags[pe.rank] + r) : "memory");
+                if (++spins == (1u << 30)) __trap();
+            } while (int32_t(v - epoch) < 0);
+        }
+    }
+    __syncthreads();
+}
+
+__global__ void ipc_allreduce_residual_kernel(float* __restrict__ x, const IpcPeers pe, int slot, uint32_t epoch,
+                                              __nv_bfloat16* __restrict__ xb, float* __restrict__ ssq, int64_t n8,
+                                              int h) {
+    pdl_launch_dependents();
+    pdl_wait();  // this rank's partial is complete
+    ipc_barrier(pe, epoch);
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;  // multiple of 32
+    for (int64_t base = blockIdx.x * int64_t(blockDim.x); base < n8; base += stride) {
+        const int64_t i = base + threadIdx.x;
+        const bool act = i < n8;
+        float ss = 0.f;
+        if (act) {
+            float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+            for (int r = 0; r < pe.n; ++r) {
+                const uint4 v = __ldcv(reinterpret_cast<const uint4*>(pe.buf[r][slot]) + i);
+                a.x += bf16_lo(v.x); a.y += bf16_hi(v.x); a.z += bf16_lo(v.y); a.w += bf16_hi(v.y);
+                b.x += bf16_lo(v.z); b.y += bf16_hi(v.z); b.z += bf16_lo(v.w); b.w += bf16_hi(v.w);
+            }
+            float4* d = reinterpret_cast<float4*>(x) + 2 * i;
+            float4 xa = d[0], xc = d[1];
+            xa.x += a.x; xa.y += a.y; xa.z += a.z; xa.w += a.w;
+            xc.x += b.x; xc.y += b.y; xc.z += b.z; xc.w += b.w;
+            d[0] = xa;
+            d[1] = xc;
+            reinterpret_cast<uint4*>(xb)[i] =
+                make_uint4(pack_bf16(xa.x, xa.y), pack_bf16(xa.z, xa.w), pack_bf16(xc.x, xc.y), pack_bf16(xc.z, xc.w));
+            ss = xa.x * xa.x + xa.y * xa.y + xa.z * xa.z + xa.w * xa.w + xc.x * xc.x + xc.y * xc.y + xc.z * xc.z +
+                 xc.w * xc.w;
+        }
+        ss += __shfl_xor_sync(0xffffffffu, ss, 1);
+        ss += __shfl_xor_sync(0xffffffffu, ss, 2);
+        if (act && (i & 3) == 0) {  // 4 threads = one 32-column chunk of one row
+            const int64_t row = i / (h / 8), g = i % (h / 8);
+            ssq[row * (h / 32) + g / 4] = ss;
+        }
+    }
+}
+
+// Vocab all-gather of the LM-head shards: logits[row][r * vl + c] = rank r's shard.
+__global__ void ipc_gather_logits_kernel(const IpcPeers pe, uint32_t epoch, float* __restrict__ out, int rows,
+                                         int vl) {
+    pdl_launch_dependents();
+    pdl_wait();
+    ipc_barrier(pe, epoch);
+    const int64_t n = int64_t(pe.n) * rows * vl;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t r = i / (int64_t(rows) * vl), rem = i % (int64_t(rows) * vl), row = rem / vl, c = rem % vl;
+        out[row * int64_t(pe.n) * vl + r * vl + c] = __ldcv(pe.logits[r] + rem);
     }
 }
 
@@ -342,6 +420,24 @@ cudaError_t residual_add_launch(float* x, const __nv_bfloat16* part, __nv_bfloat
     return n8 > 0 ? launch_pdl(residual_add_kernel, dim3(grid_for(n8, 256)), dim3(256), 0, st, 1, x, part, xb, ssq, n8,
                                h)
                   : cudaSuccess;
+}
+
+cudaError_t ipc_allreduce_residual_launch(float* x, const IpcPeers& pe, int slot, uint32_t epoch,
+                                          __nv_bfloat16* xb, float* ssq, int T, int h, cudaStream_t st) {
+    const int64_t n8 = int64_t(T) * h / 8;
+    // few CTAs: each spins once on the barrier, then strides over the rows
+    const int grid = int(std::min<int64_t>(grid_for(n8, 256), 4 * 148));
+    return n8 > 0 ? launch_pdl(ipc_allreduce_residual_kernel, dim3(grid), dim3(256), 0, st, 1, x, pe, slot, epoch, xb,
+                               ssq, n8, h)
+                  : cudaSuccess;
+}
+
+cudaError_t ipc_gather_logits_launch(const IpcPeers& pe, uint32_t epoch, float* out, int rows, int vl,
+                                     cudaStream_t st) {
+    const int64_t n = int64_t(pe.n) * rows * vl;
+    const int grid = int(std::min<int64_t>(grid_for(n, 256), 4 * 148));
+    return n > 0 ? launch_pdl(ipc_gather_logits_kernel, dim3(grid), dim3(256), 0, st, 1, pe, epoch, out, rows, vl)
+                 : cudaSuccess;
 }
 
 cudaError_t argmax_launch(const float* logits, int rows, int V, int ld, int32_t* out, cudaStream_t st) {

@@ -146,6 +146,21 @@ cudaError_t rmsnorm_launch(const float* x, const __nv_bfloat16* w, __nv_bfloat16
 cudaError_t rope_append_launch(const __nv_bfloat16* qkv, __nv_bfloat16* q_out, const int32_t* pos,
                                const int64_t* slot, const float2* rope_cs, int T, int nq_l, int nkv_l, int hd,
                                int bs, __nv_bfloat16* kc, __nv_bfloat16* vc, cudaStream_t st);
+// CUDA-IPC tensor-parallel transport (one process per GPU, buffers mapped from every
+// rank): per rank two bf16 exchange buffers [T_cap][h] (alternating per all-reduce, so a
+// rank never overwrites a buffer a peer may still read), an fp32 logits shard buffer and
+// a flag array [8] (flag r = last collective epoch rank r reached).
+constexpr int kIpcMaxRanks = 8;
+struct IpcPeers {
+    const __nv_bfloat16* buf[kIpcMaxRanks][2];
+    const float* logits[kIpcMaxRanks];
+    uint32_t* flags[kIpcMaxRanks];
+    int n, rank;
+};
+cudaError_t ipc_allreduce_residual_launch(float* x, const IpcPeers& pe, int slot, uint32_t epoch,
+                                          __nv_bfloat16* xb, float* ssq, int T, int h, cudaStream_t st);
+cudaError_t ipc_gather_logits_launch(const IpcPeers& pe, uint32_t epoch, float* out, int rows, int vl,
+                                     cudaStream_t st);
 // x += part (TP all-reduce result), also refreshing xb / ssq for the next norm-folded GEMM.
 cudaError_t residual_add_launch(float* x, const __nv_bfloat16* part, __nv_bfloat16* xb, float* ssq, int T, int h,
                                 cudaStream_t st);
