@@ -128,6 +128,8 @@ def run_ours(args):
     rank, world, local = dist_env()
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}; launch N>1 under torch.distributed.run")
+    if os.environ.get("SS_BENCH_ONE_DEVICE"):  # dev: every rank on cuda:0 (checks the N>1 path on one GPU)
+        local = 0
     torch.cuda.set_device(local)
     pg = None
     if world > 1:
@@ -247,7 +249,8 @@ def run_ours(args):
         if k == "attention":
             ent["gbs"] = pl["attention_bytes"] / (avg * 1e-3) / 1e9
         kernels[k] = ent
-    dom = max(kernels, key=lambda k: kernels[k]["share"])
+    # dominant compute kernel (the TP collective class has no roofline of its own here)
+    dom = max((k for k in kernels if "tflops" in kernels[k] or "gbs" in kernels[k]), key=lambda k: kernels[k]["share"])
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tfile):
