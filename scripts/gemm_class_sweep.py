@@ -15,7 +15,15 @@ code = r'''
 import sys, os, json
 sys.path.insert(0, os.environ["ROOT"])
 from paper_2403_02310_b200 import gpu, host
-shape = gpu.MODELS[sys.argv[1]].with_layers(int(sys.argv[3]))
+name = sys.argv[1]
+if ":" in name:  # model:tp -> one tensor-parallel rank's shard as a TP1 model
+    mname, tp = name.split(":")
+    tp = int(tp)
+    m = gpu.MODELS[mname]
+    shape = gpu.ModelShape(f"{mname}_tp{tp}", int(sys.argv[3]), m.hidden, m.num_q_heads // tp, m.num_kv_heads // tp,
+                           m.head_dim, m.ffn // tp, m.vocab // tp, rope_theta=m.rope_theta)
+else:
+    shape = gpu.MODELS[name].with_layers(int(sys.argv[3]))
 f = gpu.HybridForward(shape, weight_seed=1234)
 if int(sys.argv[2]) == 0:  # decode-only: 32 decodes at 4096
     d = host.Descriptor.build([host.BatchEntry(i, "decode", 1, 4096) for i in range(32)], vocab=shape.vocab)
