@@ -382,14 +382,29 @@ void build_items(const ss_ctx* ctx, const ss_batch_desc* d, std::vector<AttnItem
     // Tensor-core prefill flavour: with at least an SM's worth of HBM-streaming decode
     // items, compact 128-row tiles that run beside them (2); else deep 256-row tiles
     // (two 128-row halves per CTA sharing K/V, 1); 0: mma.sync 64-row tiles.
+    // work estimates in 64-key tile iterations: decode (HBM streaming) vs tensor-core tiles
     int dec_pairs = 0, pairs256 = 0;
+    long dec_iters = 0, tc_iters = 0;
     for (int e = 0; e < d->num_entries; ++e) {
-        const int rows = (d->cu_q[e + 1] - d->cu_q[e]) * G;
-        if (rows <= 16) dec_pairs += ctx->nkv_l;
-        else pairs256 += (rows + 255) / 256 * ctx->nkv_l;
+        const int ntok = d->cu_q[e + 1] - d->cu_q[e], rows = ntok * G, prefix = d->ctx_len[e] - ntok;
+        if (rows <= 16) {
+            dec_pairs += ctx->nkv_l;
+            dec_iters += long(ctx->nkv_l) * ((d->ctx_len[e] + 63) / 64);
+        } else {
+            pairs256 += (rows + 255) / 256 * ctx->nkv_l;
+            for (int r0 = 0; r0 < rows; r0 += 128)
+                tc_iters += long(ctx->nkv_l) * ((prefix + std::min(rows, r0 + 128) / G + 63) / 64);
+        }
     }
-    // deep flavours: paired 256-row items when they alone fill the SMs, else 128-row ones (3)
-    tc_mode = !ctx->attn_tc ? 0 : dec_pairs >= ctx->num_sms ? 2 : pairs256 >= ctx->num_sms ? 1 : 3;
+    // compact prefill tiles beside the decode kernel when the decodes fill the SMs and the
+    // prefill work is small next to them (measured: chunk 480 @ 0 with 32 x 4k decodes);
+    // else a deep flavour first: paired 256-row items when they alone fill the SMs, else
+    // 128-row ones (chunk 480 @ 2048: deep 11.27 vs compact 11.85 ms/step; tau = 2048: paired
+    // 26.37 vs compact 26.93)
+    tc_mode = !ctx->attn_tc                                          ? 0
+              : (dec_pairs >= ctx->num_sms && 4 * tc_iters < dec_iters) ? 2
+              : pairs256 >= ctx->num_sms                             ? 1
+                                                                     : 3;
     static const int force = getenv("SS_ATTN_TC_MODE") ? atoi(getenv("SS_ATTN_TC_MODE")) : -1;  // dev
     if (ctx->attn_tc && force >= 1 && force <= 3) tc_mode = force;
     struct Tile {
