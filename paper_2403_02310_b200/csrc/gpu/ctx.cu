@@ -189,6 +189,7 @@ struct ss_ctx {
     uint32_t* sk_flags = nullptr;   // stream-K ready flags
     uint32_t sk_epoch = 0;
     CUtensorMap ta_xn, ta_o, ta_act, ta_xo, ta_xb;
+    CUtensorMap ta32_xn, ta32_o, ta32_act, ta32_xo, ta32_xb;  // 32-row boxes (GemmPlan::ar == 32)
     bf16* xb = nullptr;   // bf16 copy of the residual stream (A of the norm-folded GEMMs)
     float* ssq = nullptr;  // per (row, 32-column chunk) sums of squares of the residual
     CUtensorMap tm_k, tm_v;  // 2D TMA views of the paged K/V pools
@@ -340,7 +341,11 @@ ss_status ensure_workspace(ss_ctx* ctx, int T, int n_out, int part_rows) {
         if (!make_tmap_2d(&ctx->ta_xn, ctx->xn, cap, h, 128, 64) ||
             !make_tmap_2d(&ctx->ta_o, ctx->o, cap, qd, 128, 64) ||
             !make_tmap_2d(&ctx->ta_act, ctx->act, cap, ctx->ffn_l, 128, 64) ||
-            !make_tmap_2d(&ctx->ta_xb, ctx->xb, cap, h, 128, 64))
+            !make_tmap_2d(&ctx->ta_xb, ctx->xb, cap, h, 128, 64) ||
+            !make_tmap_2d(&ctx->ta32_xn, ctx->xn, cap, h, 32, 64) ||
+            !make_tmap_2d(&ctx->ta32_o, ctx->o, cap, qd, 32, 64) ||
+            !make_tmap_2d(&ctx->ta32_act, ctx->act, cap, ctx->ffn_l, 32, 64) ||
+            !make_tmap_2d(&ctx->ta32_xb, ctx->xb, cap, h, 32, 64))
             return fail(ctx, SS_CUDA_ERROR, "cuTensorMapEncodeTiled failed (activation maps)");
     }
     if (n_out > ctx->O_cap) {
@@ -358,7 +363,8 @@ ss_status ensure_workspace(ss_ctx* ctx, int T, int n_out, int part_rows) {
         }
         CK(cudaMalloc(&ctx->next_tok, size_t(cap) * 4));
         ctx->O_cap = cap;
-        if (!make_tmap_2d(&ctx->ta_xo, ctx->xo, cap, ctx->h, 128, 64))
+        if (!make_tmap_2d(&ctx->ta_xo, ctx->xo, cap, ctx->h, 128, 64) ||
+            !make_tmap_2d(&ctx->ta32_xo, ctx->xo, cap, ctx->h, 32, 64))
             return fail(ctx, SS_CUDA_ERROR, "cuTensorMapEncodeTiled failed (logit rows)");
     }
     if (part_rows > ctx->P_cap) {
@@ -632,7 +638,18 @@ ss_status gemm(ss_ctx* ctx, int cls, const CUtensorMap& ta, WMaps& tb, int M, in
     p.bn = s.bn;
     p.splits = s.splits;
     p.sk_mode = s.mode;
+    p.ar = s.cg == 1 ? s.ar : 128;
     p.tmA = ta;
+    if (p.ar == 32) {  // the same activation buffer through its 32-row-box map
+        const CUtensorMap* twin = &ta == &ctx->ta_xn    ? &ctx->ta32_xn
+                                  : &ta == &ctx->ta_o   ? &ctx->ta32_o
+                                  : &ta == &ctx->ta_act ? &ctx->ta32_act
+                                  : &ta == &ctx->ta_xo  ? &ctx->ta32_xo
+                                  : &ta == &ctx->ta_xb  ? &ctx->ta32_xb
+                                                        : nullptr;
+        if (twin) p.tmA = *twin;
+        else p.ar = 128;
+    }
     const CUtensorMap* mb = tb.get(p.bn / p.cg);
     if (!mb) return fail(ctx, SS_CUDA_ERROR, "cuTensorMapEncodeTiled failed (weight tile map)");
     p.tmB = *mb;

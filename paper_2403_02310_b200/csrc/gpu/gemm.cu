@@ -38,9 +38,13 @@ constexpr int kThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue
 constexpr int kSmemMax = 232448;                         // 227 KB opt-in per CTA
 constexpr int kSmemBudget = kSmemMax - 1024 - 1024 - 8 * 4096;  // operand ring
 
-template <int CG, int BN>
+// AR < 128 (single-CTA tiles, M <= AR): only AR rows of A are loaded per stage; the MMA
+// still reads 128 rows from the stage, the rest being whatever follows in smem, which only
+// lands in accumulator rows >= M that are never stored. The freed smem buys more stages
+// of weight tiles in flight (decode-only batches are weight-streaming bound per SM).
+template <int CG, int BN, int AR = 128>
 struct GemmCfg {
-    static constexpr int A_BYTES = 128 * BK * 2;       // this CTA's 128 rows of A
+    static constexpr int A_BYTES = AR * BK * 2;        // this CTA's rows of A
     static constexpr int B_ROWS = BN / CG;             // this CTA's rows of B
     static constexpr int B_BYTES = B_ROWS * BK * 2;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -297,13 +301,13 @@ __device__ __forceinline__ void add_rows(uint32_t (&v)[32], const uint4* ep, int
     }
 }
 
-template <int CG, int BN, int EPI>
+template <int CG, int BN, int EPI, int AR>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
                         int N, int K, void* __restrict__ out, int ldo, int num_mt, int num_tiles,
                         float* __restrict__ part, uint32_t* __restrict__ flags, uint32_t epoch, int sk_mode,
                         int sk_slices, const EpiArgs ea) {
-    using Cfg = GemmCfg<CG, BN>;
+    using Cfg = GemmCfg<CG, BN, AR>;
     constexpr int STAGES = Cfg::STAGES;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
@@ -943,11 +947,11 @@ EncodeFn encode_fn() {
     return fn;
 }
 
-template <int CG, int BN, int EPI>
+template <int CG, int BN, int EPI, int AR = 128>
 cudaError_t launch_t(const GemmPlan& p, cudaStream_t st) {
-    using Cfg = GemmCfg<CG, BN>;
+    using Cfg = GemmCfg<CG, BN, AR>;
     static bool attr_set = false;
-    auto kern = gemm_tcgen05_kernel<CG, BN, EPI>;
+    auto kern = gemm_tcgen05_kernel<CG, BN, EPI, AR>;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
         if (e != cudaSuccess) return e;
@@ -1084,6 +1088,7 @@ GemmShape gemm_pick(int M, int N, int K, int epi, int num_sms) {
         consider(1, 256);
         consider(1, 128);
     }
+    best.ar = (best.cg == 1 && M <= 32 && !getenv("SS_GEMM_AR128")) ? 32 : 128;
     if (M > 128 && force_cg != 1)
         for (int bn : kBn2) consider(2, bn);
     return best;
@@ -1104,7 +1109,8 @@ bool gemm_prepare(GemmPlan& p, const void* A, uint64_t a_rows, const void* B, in
     p.bn = bn ? bn : s.bn;
     p.splits = s.splits;
     p.sk_mode = s.mode;
-    if (!make_tmap_2d(&p.tmA, A, a_rows, uint64_t(K), 128, BK)) return false;
+    p.ar = (p.cg == 1 && p.bn == s.bn) ? s.ar : 128;
+    if (!make_tmap_2d(&p.tmA, A, a_rows, uint64_t(K), uint32_t(p.ar), BK)) return false;
     if (!make_tmap_2d(&p.tmB, B, uint64_t(N), uint64_t(K), uint32_t(p.bn / p.cg), BK)) return false;
     return true;
 }
@@ -1117,6 +1123,20 @@ cudaError_t gemm_launch(const GemmPlan& p, cudaStream_t st) {
         if (p.epi == EPI_F32) return launch_t<CGv, BNv, EPI_F32>(p, st);            \
         if (p.epi == EPI_SWIGLU && BNv % 64 == 0) return launch_t<CGv, (BNv % 64 == 0 ? BNv : 64), EPI_SWIGLU>(p, st); \
         if (p.epi == EPI_QKV && BNv % 128 == 0) return launch_t<CGv, (BNv % 128 == 0 ? BNv : 128), EPI_QKV>(p, st); \
+    }
+    if (p.cg == 1 && p.ar == 32) {
+#define SS_GEMM_CASE32(BNv)                                                              \
+    if (p.bn == BNv) {                                                                   \
+        if (p.epi == EPI_BF16) return launch_t<1, BNv, EPI_BF16, 32>(p, st);             \
+        if (p.epi == EPI_RESADD) return launch_t<1, BNv, EPI_RESADD, 32>(p, st);         \
+        if (p.epi == EPI_F32) return launch_t<1, BNv, EPI_F32, 32>(p, st);               \
+        if (p.epi == EPI_SWIGLU) return launch_t<1, BNv, EPI_SWIGLU, 32>(p, st);         \
+        if (p.epi == EPI_QKV) return launch_t<1, BNv, EPI_QKV, 32>(p, st);               \
+    }
+        SS_GEMM_CASE32(128)
+        SS_GEMM_CASE32(256)
+#undef SS_GEMM_CASE32
+        return cudaErrorInvalidValue;
     }
     SS_GEMM_CASE(1, 128)
     SS_GEMM_CASE(1, 256)

@@ -51,6 +51,7 @@ struct GemmPlan {
     int ldo = 0;
     int epi = 0;
     int cg = 1;    // CTAs per MMA group (2: cta_group::2 pairs, 256-row tiles)
+    int ar = 128;  // rows of A per stage (32: M <= 32 single-CTA tiles; tmA's box must match)
     int bn = 256;  // tile N; each CTA stages bn / cg rows of B (the B map's box rows)
     int num_sms = 148;
     // stream-K workspace: partial accumulators [groups][128 * cg][bn] fp32 and one
@@ -70,6 +71,7 @@ inline size_t gemm_flag_words(int num_sms) { return size_t(num_sms) * 16; }
 
 struct GemmShape {
     int cg, bn, splits, mode;  // mode: GemmPlan::sk_mode
+    int ar = 128;              // GemmPlan::ar
 };
 
 bool make_tmap_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,

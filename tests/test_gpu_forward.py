@@ -130,3 +130,21 @@ def test_closed_loop_engine_on_gpu():
                 covered[e.request_id] = e.prefix_tokens + e.chunk_tokens
     assert all(covered[i] == r.prompt_tokens for i, r in enumerate(trace))
     f.close()
+
+
+@pytest.mark.parametrize("model,n_dec", [("tiny", 32), ("tiny", 7), ("mistral7b", 24)])
+def test_decode_only_batch(model, n_dec):
+    """Decode-only iterations (the bulk of a replayed trace): M <= 32 projections run on
+    single-CTA tiles that stage only 32 rows of A per stage; parity with the oracle."""
+    s = gpu.MODELS[model] if model == "tiny" else gpu.MODELS[model].with_layers(2)
+    ents = [host.BatchEntry(i, "decode", 1, 100 + 37 * i) for i in range(n_dec)]
+    d = host.Descriptor.build(ents, vocab=s.vocab, token_seed=3)
+    f = gpu.HybridForward(s, weight_seed=1234)
+    f.kv_alloc(d.pool_blocks)
+    f.fill_descriptor_prefixes(d, seed=5)
+    lg, nt, _ = f.forward(d)
+    f.close()
+    o = orc_mod.Oracle(s, weight_seed=1234, num_blocks=d.pool_blocks)
+    o.fill_descriptor_prefixes(d, seed=5)
+    compare(lg, o.forward(d), f"{model} decode-only x{n_dec}")
+    assert (nt == lg.argmax(1)).all()
