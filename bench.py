@@ -327,7 +327,9 @@ def closed_loop_tbt(fwd, model, tau, n_requests, qps, seed=42):
 
     trace = host.make_trace("openchat", qps, n_requests, seed)
     params = host.model_preset(model if model != "tiny" else "tiny")
-    pool = 40000 if model != "tiny" else 65536
+    shape = fwd.shape
+    per_block = shape.num_layers * 2 * (shape.num_kv_heads // fwd.tp_size) * 16 * shape.head_dim * 2
+    pool = 65536 if model == "tiny" else int(min(40000, 90e9 // per_block))  # <= 90 GB of KV pool
     fwd.kv_alloc(pool)
     cfg = host.ReplicaConfig(token_budget=tau, kv_blocks=pool)
     t0 = time.perf_counter()
