@@ -625,6 +625,9 @@ __global__ void __launch_bounds__(MODE > 0 ? TcCfg<HD, MODE>::THREADS : (kWarps 
             return __ldg(bt + (lb < nvalid ? lb : 0));  // pages past the context: a valid page, masked
         };
         int32_t cur = batch(0), nxt = ntiles > 8 ? batch(1) : 0;
+        // a decode's K/V streams through once: first out of L2, so the chunk's freshly
+        // appended K/V and the next projection's operands stay resident
+        const uint64_t pol = (p.kv_hint && it.nrows <= 16) ? l2_policy_evict_first() : l2_policy_evict_normal();
         for (int t = 0; t < ntiles; ++t) {
             if (t > 0 && (t & 7) == 0) {
                 cur = nxt;
@@ -643,7 +646,7 @@ __global__ void __launch_bounds__(MODE > 0 ? TcCfg<HD, MODE>::THREADS : (kWarps 
                 const int kv = lane & 1, hh = (lane >> 1) % (HD / 64), pg = lane / (2 * (HD / 64));
                 const int32_t row = int32_t(p.layer_row0 + (int64_t(blk[pg]) * p.nkv_l + it.kv_head) * 16);
                 uint8_t* dst = smem + st0 + st * S::STAGE + kv * S::KV_TILE + hh * (kKeysPerTile * 128) + pg * 16 * 128;
-                tma_load_2d(dst, kv ? &tmV : &tmK, hh * 64, row, &full[st]);
+                tma_load_2d_hint(dst, kv ? &tmV : &tmK, hh * 64, row, &full[st], pol);
             }
             __syncwarp();
         }
@@ -774,6 +777,18 @@ cudaError_t launch_hd(const AttnParams& p, const CUtensorMap& tk, const CUtensor
     AttnParams pt = p, pd = p;
     pd.items = p.items + n_tc;
     const dim3 bd((kWarps + 1) * 32);
+    static const bool tc2_first = [] {
+        const char* v = getenv("SS_ATTN_TC2_FIRST");
+        return v && atoi(v) > 0;
+    }();
+    if (n_tc > 0 && p.tc == 2 && tc2_first) {  // dev: compact prefill CTAs first, decodes beside them
+        pt.wait_at_end = 0;
+        pd.wait_at_end = 1;
+        cudaError_t e = launch_pdl(attention_kernel<HD, 2>, dim3(n_tc), dim3(TcCfg<HD, 2>::THREADS), TcCfg<HD, 2>::TOTAL,
+                                   st, 1, pt, tk, tv);
+        if (e != cudaSuccess || n_rest == 0) return e;
+        return launch_pdl(attention_kernel<HD, 0>, dim3(n_rest), bd, AttnSmem<HD>::TOTAL, st, 1, pd, tk, tv);
+    }
     if (n_tc > 0 && p.tc == 2) {
         // enough HBM-streaming decode CTAs to fill the machine: they go first, and the
         // compact prefill CTAs run beside them (in the SMs' remaining shared memory)

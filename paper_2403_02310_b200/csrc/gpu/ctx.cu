@@ -596,6 +596,8 @@ AttnParams attn_params(const ss_ctx* ctx, const ss_batch* b, const bf16* q, bf16
     p.n_tc = b->n_tc;
     p.wait_at_end = 0;
     p.num_sms = ctx->num_sms;
+    static const int kv_hint = getenv("SS_ATTN_L2HINT") ? atoi(getenv("SS_ATTN_L2HINT")) : 1;  // dev A/B
+    p.kv_hint = kv_hint;
     p.part_o = ctx->part_o;
     p.part_ml = ctx->part_ml;
     p.comb_count = ctx->comb_count;
@@ -657,6 +659,8 @@ ss_status gemm(ss_ctx* ctx, int cls, const CUtensorMap& ta, WMaps& tb, int M, in
     p.flags = ctx->sk_flags;
     p.epoch = ++ctx->sk_epoch;
     p.ea = ea;
+    static const int l2hint = getenv("SS_GEMM_L2HINT") ? atoi(getenv("SS_GEMM_L2HINT")) : 3;  // dev A/B
+    p.ea.l2hint = l2hint;
     return launch(ctx, cls, 1, [&] { return gemm_launch(p, ctx->st); });
 }
 

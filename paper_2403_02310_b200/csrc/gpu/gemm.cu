@@ -92,6 +92,15 @@ __device__ __forceinline__ void tma_load_2d_cg2(void* smem_dst, const CUtensorMa
         : "memory");
 }
 
+__device__ __forceinline__ void tma_load_2d_cg2_hint(void* smem_dst, const CUtensorMap* m, int32_t c0, int32_t c1,
+                                                     uint32_t bar_cluster, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
+        "[%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(bar_cluster), "l"(policy)
+        : "memory");
+}
+
 template <int CG>
 __device__ __forceinline__ void tmem_alloc_cg(uint32_t* slot, uint32_t cols_pow2);
 template <>
@@ -379,6 +388,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0) {
         if (lane == 0) {  // ---------------- TMA producer (both CTAs)
             const uint32_t full_leader = CG == 2 ? peer_addr(full, 0) : 0;
+            const uint64_t polA = (ea.l2hint & 1) ? l2_policy_evict_last() : l2_policy_evict_normal();
+            const uint64_t polB = (ea.l2hint & 2) ? l2_policy_evict_first() : l2_policy_evict_normal();
             // The weights (B) do not depend on the preceding kernels: the first
             // stages' B tiles are requested before the grid-dependency wait, so
             // their HBM latency overlaps the previous kernel's tail.
@@ -393,10 +404,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const int kb = sg.kb0 + j;
                         if constexpr (CG == 1) {
                             mbar_arrive_expect_tx(&full[j], Cfg::STAGE_BYTES);
-                            tma_load_2d(sB + j * Cfg::B_BYTES, &tmB, kb * BK, n0, &full[j]);
+                            tma_load_2d_hint(sB + j * Cfg::B_BYTES, &tmB, kb * BK, n0, &full[j], polB);
                         } else {
                             if (leader) mbar_arrive_expect_tx(&full[j], 2 * Cfg::STAGE_BYTES);
-                            tma_load_2d_cg2(sB + j * Cfg::B_BYTES, &tmB, kb * BK, n0, full_leader + uint32_t(j * 8));
+                            tma_load_2d_cg2_hint(sB + j * Cfg::B_BYTES, &tmB, kb * BK, n0, full_leader + uint32_t(j * 8), polB);
                         }
                     }
                 }
@@ -420,16 +431,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if constexpr (CG == 1) {
                         if (!pre) {
                             mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
-                            tma_load_2d(sB + s * Cfg::B_BYTES, &tmB, kb * BK, n0, &full[s]);
+                            tma_load_2d_hint(sB + s * Cfg::B_BYTES, &tmB, kb * BK, n0, &full[s], polB);
                         }
-                        tma_load_2d(sA + s * Cfg::A_BYTES, &tmA, kb * BK, m0, &full[s]);
+                        tma_load_2d_hint(sA + s * Cfg::A_BYTES, &tmA, kb * BK, m0, &full[s], polA);
                     } else {
                         const uint32_t fb = full_leader + uint32_t(s * 8);
                         if (!pre) {
                             if (leader) mbar_arrive_expect_tx(&full[s], 2 * Cfg::STAGE_BYTES);
-                            tma_load_2d_cg2(sB + s * Cfg::B_BYTES, &tmB, kb * BK, n0, fb);
+                            tma_load_2d_cg2_hint(sB + s * Cfg::B_BYTES, &tmB, kb * BK, n0, fb, polB);
                         }
-                        tma_load_2d_cg2(sA + s * Cfg::A_BYTES, &tmA, kb * BK, m0, fb);
+                        tma_load_2d_cg2_hint(sA + s * Cfg::A_BYTES, &tmA, kb * BK, m0, fb, polA);
                     }
                     if (++s == STAGES) {
                         s = 0;

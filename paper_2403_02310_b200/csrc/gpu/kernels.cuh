@@ -42,6 +42,7 @@ struct EpiArgs {
     int pf_n = 0, pf_pages = 0, pf_max_blocks = 0;
     const int32_t* pf_bt = nullptr;
     const int32_t* pf_ctx_len = nullptr;
+    int l2hint = 0;  // operand L2 priority bits: 1 A evict-last, 2 B evict-first
 };
 
 struct GemmPlan {
@@ -131,6 +132,7 @@ struct AttnParams {
     int32_t n_tc;                // items[0, n_tc) are the tcgen05 tiles (launched first)
     int32_t wait_at_end;         // set by attention_launch for the second of its two launches
     int32_t num_sms;
+    int32_t kv_hint;             // decode K/V loads marked L2 evict-first
 };
 // 2D TMA views [L * nblocks * nkv * 16][hd] of the K and V pools (box 16 x 64, SWIZZLE_128B).
 bool attention_tmaps(CUtensorMap* tk, CUtensorMap* tv, const void* kc, const void* vc, int64_t total_rows, int hd);
