@@ -627,7 +627,8 @@ __global__ void __launch_bounds__(MODE > 0 ? TcCfg<HD, MODE>::THREADS : (kWarps 
         int32_t cur = batch(0), nxt = ntiles > 8 ? batch(1) : 0;
         // a decode's K/V streams through once: first out of L2, so the chunk's freshly
         // appended K/V and the next projection's operands stay resident
-        const uint64_t pol = (p.kv_hint && it.nrows <= 16) ? l2_policy_evict_first() : l2_policy_evict_normal();
+        const uint64_t pol = it.nrows <= 16 ? ((p.kv_hint & 1) ? l2_policy_evict_first() : l2_policy_evict_normal())
+                                            : ((p.kv_hint & 2) ? l2_policy_evict_last() : l2_policy_evict_normal());
         for (int t = 0; t < ntiles; ++t) {
             if (t > 0 && (t & 7) == 0) {
                 cur = nxt;

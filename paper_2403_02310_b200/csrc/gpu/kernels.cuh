@@ -132,7 +132,7 @@ struct AttnParams {
     int32_t n_tc;                // items[0, n_tc) are the tcgen05 tiles (launched first)
     int32_t wait_at_end;         // set by attention_launch for the second of its two launches
     int32_t num_sms;
-    int32_t kv_hint;             // decode K/V loads marked L2 evict-first
+    int32_t kv_hint;             // L2 priority bits: 1 decode K/V evict-first, 2 prefill K/V evict-last
 };
 // 2D TMA views [L * nblocks * nkv * 16][hd] of the K and V pools (box 16 x 64, SWIZZLE_128B).
 bool attention_tmaps(CUtensorMap* tk, CUtensorMap* tv, const void* kc, const void* vc, int64_t total_rows, int hd);
