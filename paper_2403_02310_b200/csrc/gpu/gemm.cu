@@ -1087,7 +1087,10 @@ GemmShape gemm_pick(int M, int N, int K, int epi, int num_sms) {
         for (int S = 1; S <= 4; ++S) {
             if (force_s && S != force_s) continue;
             if (S > 1 && (rem == 0 || rem * S > slots)) break;
-            const double last = rem == 0 ? 0.0 : t1 / S + (S > 1 ? 8.0 + 2.0 * S : 0.0);
+            // split partials of 32-row single-CTA tiles are 4x smaller (decode-only sweep:
+            // 2.5 + 2.7 S fits the measured S = 2..4 overheads)
+            const double ovh = cg == 1 && M <= 32 ? 2.5 + 2.7 * S : 8.0 + 2.0 * S;
+            const double last = rem == 0 ? 0.0 : t1 / S + (S > 1 ? ovh : 0.0);
             const double cost = double(full) * t1 + last + epi_us;
             if (cost < best_cost - 1e-9) {
                 best_cost = cost;
