@@ -27,6 +27,9 @@ enum { SS_T_Q = 0, SS_T_K = 1, SS_T_V = 2, SS_T_O = 3, SS_T_GATE = 4, SS_T_UP = 
 #define SS_TAG_LMHEAD 0xE0001u
 #define SS_TAG_TOKEN 0xA0000u
 #define SS_TAG_KV(l, which) (0xC0000u + (uint32_t)(l) * 2u + (uint32_t)(which))
+/* RMSNorm gains: which = 0 attn_norm (input_layernorm), 1 mlp_norm (post-attention), 2 final */
+enum { SS_NORM_ATTN = 0, SS_NORM_MLP = 1, SS_NORM_FINAL = 2 };
+#define SS_TAG_NORM(l, which) (0xD0000u + (uint32_t)(l) * 4u + (uint32_t)(which))
 
 SS_HD uint64_t ss_mix64(uint64_t x) {
     x += 0x9E3779B97F4A7C15ull;
@@ -69,6 +72,13 @@ SS_HD float ss_bf16_bits_to_f32(uint16_t h) {
 /* bf16 bits of element (row, col) of a tensor with per-tensor scale. */
 SS_HD uint16_t ss_synth_bf16(uint64_t seed, uint32_t tag, uint64_t row, uint64_t col, float scale) {
     return ss_f32_to_bf16_bits(ss_unit(ss_key(seed, tag, row, col)) * scale);
+}
+
+/* RMSNorm gain element i (bf16 bits): 1 + u/4, u uniform in [-1, 1), so gains lie in
+ * [0.75, 1.25) — non-unit, so a dropped or misapplied gain changes every logit. The
+ * product u/4 is exact; the sum is one correctly-rounded fp32 add (FMA-safe). */
+SS_HD uint16_t ss_norm_gain_bf16(uint64_t seed, int layer, int which, int64_t i) {
+    return ss_f32_to_bf16_bits(1.0f + 0.25f * ss_unit(ss_key(seed, SS_TAG_NORM(layer, which), 0u, (uint64_t)i)));
 }
 
 /* Synthetic token id of request rid at absolute position pos. */

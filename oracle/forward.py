@@ -1,6 +1,9 @@
 """TEST INFRASTRUCTURE ONLY: ctypes driver of liboracle.so, the fp32 CPU
 restatement of the hybrid-batch forward (see oracle/oracle.h). Only tests/,
-__graft_entry__.smoke() and bench.py's CPU legs may import this module."""
+__graft_entry__.smoke() and bench.py's CPU legs may import this module.
+
+Self-contained: it loads no product library (the struct layouts below mirror
+include/ss_gpu.h), so bench.py's CPU reference arm maps only liboracle.so."""
 from __future__ import annotations
 
 import ctypes as C
@@ -8,13 +11,25 @@ import os
 
 import numpy as np
 
-from paper_2403_02310_b200 import _lib
-
 HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_SO = os.path.join(HERE, "liboracle.so")
 AR_FN = C.CFUNCTYPE(None, C.POINTER(C.c_float), C.c_int64, C.c_void_p)
 
 _L = None
+
+
+class ModelCfgC(C.Structure):
+    """Layout of ss_model_cfg (include/ss_gpu.h)."""
+    _fields_ = [
+        ("num_layers", C.c_int32), ("hidden", C.c_int32), ("num_q_heads", C.c_int32),
+        ("num_kv_heads", C.c_int32), ("head_dim", C.c_int32), ("ffn", C.c_int32), ("vocab", C.c_int32),
+        ("rope_theta", C.c_float), ("rms_eps", C.c_float), ("max_positions", C.c_int32),
+    ]
+
+
+def model_cfg(shape) -> ModelCfgC:
+    return ModelCfgC(shape.num_layers, shape.hidden, shape.num_q_heads, shape.num_kv_heads, shape.head_dim,
+                     shape.ffn, shape.vocab, shape.rope_theta, shape.rms_eps, shape.max_positions)
 
 
 def lib():
@@ -24,7 +39,7 @@ def lib():
             raise ImportError(f"{ORACLE_SO} missing: run `make -C oracle`")
         L = C.CDLL(ORACLE_SO)
         P = C.c_void_p
-        L.orc_create.argtypes = [C.POINTER(_lib.ModelCfg), C.c_int32, C.c_int32, C.c_uint64, C.c_int64, C.c_int32,
+        L.orc_create.argtypes = [C.POINTER(ModelCfgC), C.c_int32, C.c_int32, C.c_uint64, C.c_int64, C.c_int32,
                                  C.c_int32]
         L.orc_create.restype = P
         L.orc_destroy.argtypes = [P]
@@ -32,7 +47,7 @@ def lib():
         L.orc_threads.restype = C.c_int32
         L.orc_kv_fill_synthetic.argtypes = [P, P, C.c_int32, C.c_int32, C.c_int32, C.c_uint64]
         L.orc_kv_fill_synthetic.restype = C.c_int32
-        L.orc_forward.argtypes = [P, C.POINTER(_lib.BatchDesc), P, P]
+        L.orc_forward.argtypes = [P, P, P, P]  # ss_batch_desc* (any ctypes struct of that layout)
         L.orc_forward.restype = C.c_int32
         L.orc_weight.argtypes = [P, C.c_char_p, C.c_int32, P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
         L.orc_weight.restype = C.c_int32
@@ -45,7 +60,8 @@ class Oracle:
     def __init__(self, shape, tp_rank=0, tp_size=1, weight_seed=1234, num_blocks=1024, layers=None, with_head=True):
         self.shape, self.tp_rank, self.tp_size = shape, tp_rank, tp_size
         n = shape.num_layers if layers is None else layers
-        self._h = lib().orc_create(C.byref(shape.c()), tp_rank, tp_size, weight_seed, num_blocks, n, int(with_head))
+        self._h = lib().orc_create(C.byref(model_cfg(shape)), tp_rank, tp_size, weight_seed, num_blocks, n,
+                                   int(with_head))
         if not self._h:
             raise RuntimeError(lib().orc_last_error().decode())
         self._ar = None
@@ -85,7 +101,7 @@ class Oracle:
         vl = self.shape.vocab // self.tp_size
         lg = np.zeros((v.n_out, vl), np.float32)
         hid = np.zeros((v.num_tokens, self.shape.hidden), np.float32) if want_hidden else None
-        st = lib().orc_forward(self._h, C.byref(v), lg.ctypes.data, hid.ctypes.data if want_hidden else None)
+        st = lib().orc_forward(self._h, C.addressof(v), lg.ctypes.data, hid.ctypes.data if want_hidden else None)
         if st:
             raise RuntimeError(lib().orc_last_error().decode())
         return (lg, hid) if want_hidden else lg

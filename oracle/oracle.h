@@ -44,7 +44,8 @@ int32_t orc_kv_fill_synthetic(orc* o, const int32_t* block_table, int32_t n_bloc
  * nullable. hidden: [T][hidden] final residual stream (pre final norm), nullable. */
 int32_t orc_forward(orc* o, const ss_batch_desc* d, float* logits, float* hidden);
 /* Copies a materialised weight ([rows][cols], fp32) for tests: names as in
- * ss_weight_ptr but unfused: "wq","wk","wv","wo","wg","wu","wd","embed","lm_head". */
+ * ss_weight_ptr but unfused: "wq","wk","wv","wo","wg","wu","wd","embed","lm_head", and the
+ * RMSNorm gains "attn_norm","mlp_norm" (per layer), "final_norm" ([1][hidden]). */
 int32_t orc_weight(orc* o, const char* name, int32_t layer, float* out, int64_t* rows, int64_t* cols);
 const char* orc_last_error(void);
 

@@ -78,6 +78,7 @@ void sgemm_nt(const float* A, const float* B, float* C, int64_t M, int64_t N, in
 
 struct Layer {
     std::vector<float> wq, wk, wv, wo, wg, wu, wd;  // unfused, natural layouts
+    std::vector<float> g_attn, g_mlp;               // RMSNorm gains, applied explicitly
 };
 
 }  // namespace
@@ -88,7 +89,7 @@ struct orc {
     bool head;
     uint64_t seed;
     std::vector<Layer> layers;
-    std::vector<float> embed, lm_head;
+    std::vector<float> embed, lm_head, g_final;
     std::vector<float> kc, vc;  // [L][nblocks][nkv][16][hd]
     int64_t nblocks, lstride;
     std::vector<float> cosv, sinv;  // [max_pos][hd/2]
@@ -108,14 +109,20 @@ void gen(std::vector<float>& w, int64_t rows, int64_t cols, uint64_t seed, uint3
                 ss_synth_bf16(seed, tag, uint64_t(row_off + i), uint64_t(col_off + j), scale));
 }
 
-void rmsnorm_rows(const float* x, float* out, int64_t M, int64_t h, float eps) {
+// HF LlamaRMSNorm: out = g * (x * rsqrt(mean(x^2) + eps))
+void rmsnorm_rows(const float* x, const float* g, float* out, int64_t M, int64_t h, float eps) {
 #pragma omp parallel for schedule(static)
     for (int64_t r = 0; r < M; ++r) {
         double ss = 0;
         for (int64_t i = 0; i < h; ++i) ss += double(x[r * h + i]) * x[r * h + i];
         const float inv = float(1.0 / std::sqrt(ss / double(h) + double(eps)));
-        for (int64_t i = 0; i < h; ++i) out[r * h + i] = x[r * h + i] * inv;  // gains are 1
+        for (int64_t i = 0; i < h; ++i) out[r * h + i] = g[i] * (x[r * h + i] * inv);
     }
+}
+
+void gen_gain(std::vector<float>& g, int64_t h, uint64_t seed, int layer, int which) {
+    g.resize(size_t(h));
+    for (int64_t i = 0; i < h; ++i) g[size_t(i)] = ss_bf16_bits_to_f32(ss_norm_gain_bf16(seed, layer, which, i));
 }
 
 void allreduce(orc* o, float* buf, int64_t n) {
@@ -165,7 +172,10 @@ orc* orc_create(const ss_model_cfg* cfg, int32_t tp_rank, int32_t tp_size, uint6
         gen(W.wg, o->ffn, h, seed, SS_TAG_LAYER(l, SS_T_GATE), int64_t(tp_rank) * o->ffn, 0, sq);
         gen(W.wu, o->ffn, h, seed, SS_TAG_LAYER(l, SS_T_UP), int64_t(tp_rank) * o->ffn, 0, sq);
         gen(W.wd, h, o->ffn, seed, SS_TAG_LAYER(l, SS_T_DOWN), 0, int64_t(tp_rank) * o->ffn, sd);
+        gen_gain(W.g_attn, h, seed, l, SS_NORM_ATTN);
+        gen_gain(W.g_mlp, h, seed, l, SS_NORM_MLP);
     }
+    gen_gain(o->g_final, h, seed, 0, SS_NORM_FINAL);
     gen(o->embed, cfg->vocab, h, seed, SS_TAG_EMBED, 0, 0, ss_embed_scale());
     if (o->head) gen(o->lm_head, o->vl, h, seed, SS_TAG_LMHEAD, int64_t(tp_rank) * o->vl, 0, sq);
     o->nblocks = num_blocks;
@@ -230,7 +240,7 @@ int32_t orc_forward(orc* o, const ss_batch_desc* d, float* logits, float* hidden
         const Layer& W = o->layers[size_t(l)];
         float* KC = &o->kc[size_t(l * o->lstride)];
         float* VC = &o->vc[size_t(l * o->lstride)];
-        rmsnorm_rows(x.data(), xn.data(), T, h, eps);
+        rmsnorm_rows(x.data(), W.g_attn.data(), xn.data(), T, h, eps);
         sgemm_nt(xn.data(), W.wq.data(), q.data(), T, qr, h, false);
         sgemm_nt(xn.data(), W.wk.data(), k.data(), T, kr, h, false);
         sgemm_nt(xn.data(), W.wv.data(), v.data(), T, kr, h, false);
@@ -292,7 +302,7 @@ int32_t orc_forward(orc* o, const ss_batch_desc* d, float* logits, float* hidden
         sgemm_nt(att.data(), W.wo.data(), part.data(), T, h, qr, false);
         allreduce(o, part.data(), T * h);
         for (int64_t i = 0; i < T * h; ++i) x[size_t(i)] += part[size_t(i)];
-        rmsnorm_rows(x.data(), xn.data(), T, h, eps);
+        rmsnorm_rows(x.data(), W.g_mlp.data(), xn.data(), T, h, eps);
         sgemm_nt(xn.data(), W.wg.data(), g.data(), T, o->ffn, h, false);
         sgemm_nt(xn.data(), W.wu.data(), u.data(), T, o->ffn, h, false);
 #pragma omp parallel for schedule(static)
@@ -309,7 +319,7 @@ int32_t orc_forward(orc* o, const ss_batch_desc* d, float* logits, float* hidden
         std::vector<float> xo(size_t(d->n_out * h)), xr(size_t(d->n_out * h));
         for (int i = 0; i < d->n_out; ++i)
             std::memcpy(&xr[size_t(i * h)], &x[size_t(int64_t(d->out_rows[i]) * h)], size_t(h) * 4);
-        rmsnorm_rows(xr.data(), xo.data(), d->n_out, h, eps);
+        rmsnorm_rows(xr.data(), o->g_final.data(), xo.data(), d->n_out, h, eps);
         sgemm_nt(xo.data(), o->lm_head.data(), logits, d->n_out, o->vl, h, false);
     }
     return 0;
@@ -321,6 +331,7 @@ int32_t orc_weight(orc* o, const char* name, int32_t layer, float* out, int64_t*
     int64_t r = 0, c = 0;
     const int64_t h = o->h, qr = int64_t(o->nq) * o->hd, kr = int64_t(o->nkv) * o->hd;
     if (n == "embed") { w = &o->embed; r = o->cfg.vocab; c = h; }
+    else if (n == "final_norm") { w = &o->g_final; r = 1; c = h; }
     else if (n == "lm_head") { w = &o->lm_head; r = o->vl; c = h; }
     else if (layer >= 0 && layer < o->L) {
         const Layer& W = o->layers[size_t(layer)];
@@ -331,6 +342,8 @@ int32_t orc_weight(orc* o, const char* name, int32_t layer, float* out, int64_t*
         else if (n == "wg") { w = &W.wg; r = o->ffn; c = h; }
         else if (n == "wu") { w = &W.wu; r = o->ffn; c = h; }
         else if (n == "wd") { w = &W.wd; r = h; c = o->ffn; }
+        else if (n == "attn_norm") { w = &W.g_attn; r = 1; c = h; }
+        else if (n == "mlp_norm") { w = &W.g_mlp; r = 1; c = h; }
     }
     if (!w || w->empty()) return 1;
     if (rows) *rows = r;

@@ -757,8 +757,10 @@ __global__ void attention_combine_kernel(const AttnParams p) {
 
 template <int HD>
 cudaError_t launch_hd(const AttnParams& p, const CUtensorMap& tk, const CUtensorMap& tv, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
+    static bool attr[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    if (!attr[dev]) {
         cudaError_t e = cudaFuncSetAttribute(attention_kernel<HD, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              TcCfg<HD, 1>::TOTAL);
         if (e == cudaSuccess)
@@ -771,18 +773,14 @@ cudaError_t launch_hd(const AttnParams& p, const CUtensorMap& tk, const CUtensor
             e = cudaFuncSetAttribute(attention_kernel<HD, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      AttnSmem<HD>::TOTAL);
         if (e != cudaSuccess) return e;
-        attr = true;
+        attr[dev] = true;
     }
     // items[0, n_tc): tensor-core prefill tiles; the rest: decode / mma.sync items
     const int n_tc = p.tc ? p.n_tc : 0, n_rest = p.n_items - n_tc;
     AttnParams pt = p, pd = p;
     pd.items = p.items + n_tc;
     const dim3 bd((kWarps + 1) * 32);
-    static const bool tc2_first = [] {
-        const char* v = getenv("SS_ATTN_TC2_FIRST");
-        return v && atoi(v) > 0;
-    }();
-    if (n_tc > 0 && p.tc == 2 && tc2_first) {  // dev: compact prefill CTAs first, decodes beside them
+    if (n_tc > 0 && p.tc == 2 && p.tc2_first > 0 && n_rest > 0) {  // dev: compact prefill CTAs first, decodes beside them
         pt.wait_at_end = 0;
         pd.wait_at_end = 1;
         cudaError_t e = launch_pdl(attention_kernel<HD, 2>, dim3(n_tc), dim3(TcCfg<HD, 2>::THREADS), TcCfg<HD, 2>::TOTAL,
@@ -790,7 +788,7 @@ cudaError_t launch_hd(const AttnParams& p, const CUtensorMap& tk, const CUtensor
         if (e != cudaSuccess || n_rest == 0) return e;
         return launch_pdl(attention_kernel<HD, 0>, dim3(n_rest), bd, AttnSmem<HD>::TOTAL, st, 1, pd, tk, tv);
     }
-    if (n_tc > 0 && p.tc == 2) {
+    if (n_tc > 0 && p.tc == 2 && n_rest > 0) {
         // enough HBM-streaming decode CTAs to fill the machine: they go first, and the
         // compact prefill CTAs run beside them (in the SMs' remaining shared memory)
         pd.wait_at_end = 0;

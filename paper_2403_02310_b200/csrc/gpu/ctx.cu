@@ -211,8 +211,11 @@ struct ss_ctx {
     IpcPeers ipc_peers{};
     void* ipc_mapped[kIpcMaxRanks] = {};
     uint32_t ipc_epoch = 0;      // collectives so far (identical sequence on every rank)
+    uint32_t* dev_err = nullptr;   // device error word (IpcPeers::err), checked after each forward
+    uint32_t* host_err = nullptr;  // pinned copy of it
     uint32_t ipc_ar = 0;         // all-reduces so far (exchange buffer = ipc_ar & 1)
 
+    Tuning tu;  // dev overrides, read once at ss_create (tuning_from_env)
     bool prof = false;
     std::vector<Prof> pend;
     std::vector<cudaEvent_t> free_ev;
@@ -229,6 +232,19 @@ ss_status fail(ss_ctx* c, ss_status s, const std::string& msg) {
     else g_create_err = msg;
     return s;
 }
+
+// Makes ctx's device current for the duration of a C-ABI call (the caller's thread may
+// have another current device) and restores the caller's.
+struct DevGuard {
+    int prev = -1;
+    explicit DevGuard(int d) {
+        if (cudaGetDevice(&prev) == cudaSuccess && prev != d) cudaSetDevice(d);
+        else prev = -1;
+    }
+    ~DevGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
 
 #define CK(call)                                                                                    \
     do {                                                                                            \
@@ -285,8 +301,9 @@ T* carve(uint8_t*& p, size_t n) {
 }
 
 ss_status init_weight(ss_ctx* ctx, bf16* w, int kind, int layer, int64_t rows, int64_t cols, float sa, float sb,
-                      float sc) {
+                      float sc, int norm = 0) {
     WeightInit wi{};
+    wi.norm = norm;
     wi.kind = kind;
     wi.layer = layer;
     wi.rank = ctx->rank;
@@ -411,8 +428,9 @@ void build_items(const ss_ctx* ctx, const ss_batch_desc* d, std::vector<AttnItem
               : (dec_pairs >= ctx->num_sms && 4 * tc_iters < dec_iters) ? 2
               : pairs256 >= ctx->num_sms                             ? 1
                                                                      : 3;
-    static const int force = getenv("SS_ATTN_TC_MODE") ? atoi(getenv("SS_ATTN_TC_MODE")) : -1;  // dev
+    const int force = ctx->tu.attn_tc_mode;  // dev
     if (ctx->attn_tc && force >= 1 && force <= 3) tc_mode = force;
+    if (tc_mode == 2 && dec_pairs == 0) tc_mode = 3;  // the compact flavour runs beside decode CTAs only
     struct Tile {
         int e, row0, nr, extent;
     };
@@ -467,9 +485,9 @@ void build_items(const ss_ctx* ctx, const ss_batch_desc* d, std::vector<AttnItem
     }
     // longest items first so the tail of the launch is short (SS_ATTN_ORDER=1,
     // dev: prefill row tiles first)
-    static const int order = getenv("SS_ATTN_ORDER") ? atoi(getenv("SS_ATTN_ORDER")) : 0;
+    const int order = ctx->tu.attn_order;
     const bool tc_items = tc_mode != 0;
-    std::stable_sort(items.begin(), items.end(), [tc_items](const AttnItem& a, const AttnItem& b) {
+    std::stable_sort(items.begin(), items.end(), [tc_items, order](const AttnItem& a, const AttnItem& b) {
         if (order == 1 && (a.nrows > 16) != (b.nrows > 16)) return a.nrows > 16;
         // per-key cost: decode streaming ~16, mma.sync row tile ~64, tcgen05 row tile ~8
         auto wt = [tc_items](const AttnItem& x) { return x.nrows <= 16 ? 16 : (tc_items ? 8 : 64); };
@@ -519,7 +537,10 @@ ss_status validate(ss_ctx* ctx, const ss_batch_desc* d) {
     return SS_OK;
 }
 
-ss_status upload(ss_ctx* ctx, const ss_batch_desc* d, ss_batch* b) {
+// ev_start (nullable) is recorded on the stream just before the descriptor's H2D copy, so a
+// step's measured time covers copy + forward but not the host-side validation / work-list
+// build / staging above it.
+ss_status upload(ss_ctx* ctx, const ss_batch_desc* d, ss_batch* b, cudaEvent_t ev_start = nullptr) {
     if (ss_status s = validate(ctx, d)) return s;
     std::vector<AttnItem> items;
     std::vector<AttnCombine> combs;
@@ -559,6 +580,7 @@ ss_status upload(ss_ctx* ctx, const ss_batch_desc* d, ss_batch* b) {
         dptrs[i] = b->dev + off;
         off += (segs[i].bytes + 255) & ~size_t(255);
     }
+    if (ev_start) CK(cudaEventRecord(ev_start, ctx->st));
     CK(cudaMemcpyAsync(b->dev, ctx->pinned, total, cudaMemcpyHostToDevice, ctx->st));
     b->cu_q = reinterpret_cast<int32_t*>(dptrs[0]);
     b->ctx_len = reinterpret_cast<int32_t*>(dptrs[1]);
@@ -596,8 +618,8 @@ AttnParams attn_params(const ss_ctx* ctx, const ss_batch* b, const bf16* q, bf16
     p.n_tc = b->n_tc;
     p.wait_at_end = 0;
     p.num_sms = ctx->num_sms;
-    static const int kv_hint = getenv("SS_ATTN_L2HINT") ? atoi(getenv("SS_ATTN_L2HINT")) : 1;  // dev A/B
-    p.kv_hint = kv_hint;
+    p.kv_hint = ctx->tu.attn_l2hint;
+    p.tc2_first = ctx->tu.attn_tc2_first;
     p.part_o = ctx->part_o;
     p.part_ml = ctx->part_ml;
     p.comb_count = ctx->comb_count;
@@ -625,16 +647,12 @@ ss_status gemm(ss_ctx* ctx, int cls, const CUtensorMap& ta, WMaps& tb, int M, in
     p.ldo = ldo;
     p.epi = epi;
     p.num_sms = ctx->num_sms;
-    GemmShape s = gemm_pick(M, N, K, epi, ctx->num_sms);
+    GemmShape s = gemm_pick(M, N, K, epi, ctx->num_sms, ctx->tu);
     {  // dev tuning: SS_GEMM_<class>=mode,bn[,splits] overrides the pick for one projection
-        static const char* names[] = {"QKV", "O", "GATEUP", "DOWN", "LMHEAD"};
         const int idx = cls == SS_K_GEMM_QKV ? 0 : cls == SS_K_GEMM_O ? 1 : cls == SS_K_GEMM_GATEUP ? 2
                       : cls == SS_K_GEMM_DOWN ? 3 : 4;
-        const std::string var = std::string("SS_GEMM_") + names[idx];
-        if (const char* f = getenv(var.c_str())) {
-            int md = s.mode, bn = s.bn, sp = 1;
-            if (sscanf(f, "%d,%d,%d", &md, &bn, &sp) >= 2) s = GemmShape{M > 128 ? 2 : 1, bn, sp, md};
-        }
+        const int* f = ctx->tu.gemm_force[idx];
+        if (f[0] >= 0) s = GemmShape{M > 128 ? 2 : 1, f[1], f[2], f[0]};
     }
     p.cg = s.cg;
     p.bn = s.bn;
@@ -658,9 +676,11 @@ ss_status gemm(ss_ctx* ctx, int cls, const CUtensorMap& ta, WMaps& tb, int M, in
     p.part = ctx->sk_part;
     p.flags = ctx->sk_flags;
     p.epoch = ++ctx->sk_epoch;
+    p.force_sk = ctx->tu.gemm_sk;
+    p.force_splits = ctx->tu.gemm_splits;
+    p.debug = ctx->tu.gemm_debug;
     p.ea = ea;
-    static const int l2hint = getenv("SS_GEMM_L2HINT") ? atoi(getenv("SS_GEMM_L2HINT")) : 3;  // dev A/B
-    p.ea.l2hint = l2hint;
+    p.ea.l2hint = ctx->tu.gemm_l2hint;
     return launch(ctx, cls, 1, [&] { return gemm_launch(p, ctx->st); });
 }
 
@@ -741,7 +761,7 @@ ss_status enqueue_forward(ss_ctx* ctx, const ss_batch* b) {
     // RMSNorm is folded into the QKV / gate-up GEMMs: they consume the bf16 copy of
     // the residual (xb) and scale rows by rsqrt(mean(x^2) + eps) from the
     // per-chunk sums of squares (ssq) that embed / the residual-add epilogues
-    // produce (norm gains are unit in the synthetic model, i.e. folded into W).
+    // produce; the norm gains were folded into Wqkv / Wgu at ss_create.
     EpiArgs norm_in;
     norm_in.ssq_in = ctx->ssq;
     norm_in.ssq_in_n = h / 32;
@@ -844,14 +864,29 @@ ss_status enqueue_forward(ss_ctx* ctx, const ss_batch* b) {
     return SS_OK;
 }
 
-ss_status read_outputs(ss_ctx* ctx, const ss_batch* b, float* logits, int32_t* next) {
-    if (b->n_out == 0) return SS_OK;
-    const float* full = ctx->tp > 1 ? ctx->logits : ctx->logits_l;
-    if (logits)
-        CK(cudaMemcpyAsync(logits, full, size_t(b->n_out) * ctx->cfg.vocab * 4, cudaMemcpyDeviceToHost, ctx->st));
-    if (next) CK(cudaMemcpyAsync(next, ctx->next_tok, size_t(b->n_out) * 4, cudaMemcpyDeviceToHost, ctx->st));
+// After a synchronize: a collective that timed out on a missing peer left a code in the
+// device error word (see IpcPeers); report it once and clear it.
+ss_status check_dev_err(ss_ctx* ctx) {
+    if (!ctx->ipc || *ctx->host_err == 0) return SS_OK;
+    const uint32_t e = *ctx->host_err;
+    *ctx->host_err = 0;
+    CK(cudaMemsetAsync(ctx->dev_err, 0, 4, ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
-    return SS_OK;
+    return fail(ctx, SS_NCCL_ERROR,
+                "TP peer rank " + std::to_string(e >> 8) + " did not reach a collective within the timeout; the "
+                "forward's outputs are invalid");
+}
+
+ss_status read_outputs(ss_ctx* ctx, const ss_batch* b, float* logits, int32_t* next) {
+    if (b->n_out > 0) {
+        const float* full = ctx->tp > 1 ? ctx->logits : ctx->logits_l;
+        if (logits)
+            CK(cudaMemcpyAsync(logits, full, size_t(b->n_out) * ctx->cfg.vocab * 4, cudaMemcpyDeviceToHost, ctx->st));
+        if (next) CK(cudaMemcpyAsync(next, ctx->next_tok, size_t(b->n_out) * 4, cudaMemcpyDeviceToHost, ctx->st));
+    }
+    if (ctx->ipc) CK(cudaMemcpyAsync(ctx->host_err, ctx->dev_err, 4, cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    return check_dev_err(ctx);
 }
 
 void collect_prof(ss_ctx* ctx) {
@@ -930,6 +965,14 @@ SS_API ss_status ss_ipc_open(ss_ctx* ctx, const void* handles) {
         pe.logits[r] = reinterpret_cast<const float*>(base + ipc_logits_off(ctx));
         pe.flags[r] = reinterpret_cast<uint32_t*>(base + ipc_flags_off(ctx));
     }
+    if (!ctx->dev_err) {
+        CK(cudaMalloc(&ctx->dev_err, 4));
+        CK(cudaMallocHost(&ctx->host_err, 4));
+    }
+    CK(cudaMemset(ctx->dev_err, 0, 4));
+    *ctx->host_err = 0;
+    pe.err = ctx->dev_err;
+    pe.timeout_ns = 10ull * 1000 * 1000 * 1000;  // a peer missing for 10 s is a failed rank
     ctx->ipc_peers = pe;
     ctx->ipc = 1;
     return SS_OK;
@@ -978,12 +1021,18 @@ static ss_status create_impl(const ss_model_cfg* cfg, int32_t tp_rank, int32_t t
     ctx->vocab_l = c.vocab / tp_size;
     ctx->seed = weight_seed;
     ctx->grp = grp;
+    ctx->tu = tuning_from_env();
     if (const char* f = getenv("SS_ATTN_SPLIT")) ctx->decode_split = std::max(64, atoi(f) / 64 * 64);  // dev tuning
     if (const char* f = getenv("SS_ATTN_FUSED_COMBINE")) ctx->fused_combine = atoi(f);
     if (const char* f = getenv("SS_ATTN_TC")) ctx->attn_tc = atoi(f);  // dev: 0 = mma.sync prefill tiles
     if (ctx->fused_combine) ctx->attn_tc = 0;  // the in-kernel split merge exists on the mma.sync path only
     if (const char* f = getenv("SS_KV_PF_MB")) ctx->kv_pf_mb = atoi(f);  // dev tuning
     if (const char* f = getenv("SS_FUSE_ROPE")) ctx->fuse_rope = atoi(f);
+    // every allocation below lands on `device`, whatever the calling thread's current device
+    if (cudaSetDevice(device) != cudaSuccess) {
+        delete ctx;
+        return fail(nullptr, SS_CUDA_ERROR, "cudaSetDevice");
+    }
     if (cudaMalloc(&ctx->sk_part, gemm_part_floats(ctx->num_sms) * 4) != cudaSuccess ||
         cudaMalloc(&ctx->sk_flags, gemm_flag_words(ctx->num_sms) * 4) != cudaSuccess ||
         cudaMemset(ctx->sk_flags, 0, gemm_flag_words(ctx->num_sms) * 4) != cudaSuccess) {
@@ -997,7 +1046,6 @@ static ss_status create_impl(const ss_model_cfg* cfg, int32_t tp_rank, int32_t t
         g_create_err = m;
         return s;
     };
-    if (cudaSetDevice(device) != cudaSuccess) return bail(fail(ctx, SS_CUDA_ERROR, "cudaSetDevice"));
     if (grp) ctx->st = grp->st;
     else if (cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking) != cudaSuccess)
         return bail(fail(ctx, SS_CUDA_ERROR, "stream create"));
@@ -1030,9 +1078,14 @@ static ss_status create_impl(const ss_model_cfg* cfg, int32_t tp_rank, int32_t t
             (s = init_weight(ctx, W.wo, W_O, l, h, qd, s_o, s_o, s_o)) ||
             (s = init_weight(ctx, W.wgu, W_GU, l, 2 * ctx->ffn_l, h, s_gu, s_gu, s_gu)) ||
             (s = init_weight(ctx, W.wdown, W_DOWN, l, h, ctx->ffn_l, s_dn, s_dn, s_dn)) ||
-            (s = init_weight(ctx, W.attn_norm, W_ONES, l, 1, h, 1, 1, 1)) ||
-            (s = init_weight(ctx, W.mlp_norm, W_ONES, l, 1, h, 1, 1, 1)))
+            (s = init_weight(ctx, W.attn_norm, W_NORM, l, 1, h, 1, 1, 1, SS_NORM_ATTN)) ||
+            (s = init_weight(ctx, W.mlp_norm, W_NORM, l, 1, h, 1, 1, 1, SS_NORM_MLP)))
             return bail(s);
+        // the pre-attention / pre-MLP RMSNorm gains are folded into the consuming
+        // projections' K columns (the norm itself is folded into their epilogues)
+        if (fold_gain_launch(W.wqkv, W.attn_norm, qkv_rows, h, ctx->st) != cudaSuccess ||
+            fold_gain_launch(W.wgu, W.mlp_norm, 2 * ctx->ffn_l, h, ctx->st) != cudaSuccess)
+            return bail(fail(ctx, SS_CUDA_ERROR, "norm-gain fold launch"));
         if (!bmaps(W.tb_qkv, W.wqkv, qkv_rows, h) || !bmaps(W.tb_o, W.wo, h, qd) ||
             !bmaps(W.tb_gu, W.wgu, 2 * ctx->ffn_l, h) || !bmaps(W.tb_down, W.wdown, h, ctx->ffn_l))
             return bail(fail(ctx, SS_CUDA_ERROR, "cuTensorMapEncodeTiled failed (weights)"));
@@ -1045,7 +1098,7 @@ static ss_status create_impl(const ss_model_cfg* cfg, int32_t tp_rank, int32_t t
         if ((s = init_weight(ctx, ctx->embed, W_EMBED, 0, c.vocab, h, ss_embed_scale(), 0, 0)) ||
             (s = init_weight(ctx, ctx->lm_head, W_LMHEAD, 0, ctx->vocab_l, h, ss_weight_scale(-1, h, c.num_layers), 0,
                              0)) ||
-            (s = init_weight(ctx, ctx->final_norm, W_ONES, 0, 1, h, 1, 1, 1)))
+            (s = init_weight(ctx, ctx->final_norm, W_NORM, 0, 1, h, 1, 1, 1, SS_NORM_FINAL)))
             return bail(s);
         if (!bmaps(ctx->tb_lm, ctx->lm_head, ctx->vocab_l, h))
             return bail(fail(ctx, SS_CUDA_ERROR, "cuTensorMapEncodeTiled failed (lm head)"));
@@ -1150,11 +1203,14 @@ SS_API ss_status ss_forward_local_group(ss_ctx* const* ranks, int32_t n, const s
 
 SS_API void ss_destroy(ss_ctx* ctx) {
     if (!ctx) return;
+    DevGuard dg(ctx->device);
     if (ctx->st) cudaStreamSynchronize(ctx->st);
     if (ctx->comm) g_nccl.destroy(ctx->comm);
     for (int r = 0; r < kIpcMaxRanks; ++r)
         if (ctx->ipc_mapped[r]) cudaIpcCloseMemHandle(ctx->ipc_mapped[r]);
     if (ctx->ipc_region) cudaFree(ctx->ipc_region);
+    cudaFree(ctx->dev_err);
+    cudaFreeHost(ctx->host_err);
     cudaFree(ctx->wmem);
     cudaFree(ctx->rope);
     cudaFree(ctx->sk_part);
@@ -1195,6 +1251,7 @@ SS_API ss_status ss_model_config(const ss_ctx* ctx, ss_model_cfg* out, int32_t* 
 SS_API ss_status ss_kv_alloc(ss_ctx* ctx, int64_t num_blocks, int32_t block_size) {
     if (!ctx || num_blocks < 1 || block_size != 16)
         return fail(ctx, SS_INVALID_ARG, "KV pool needs num_blocks >= 1 and block_size 16 (reference default)");
+    DevGuard dg(ctx->device);
     cudaFree(ctx->kc);
     cudaFree(ctx->vc);
     ctx->kc = ctx->vc = nullptr;
@@ -1215,6 +1272,7 @@ SS_API ss_status ss_kv_alloc(ss_ctx* ctx, int64_t num_blocks, int32_t block_size
 
 SS_API ss_status ss_batch_upload(ss_ctx* ctx, const ss_batch_desc* desc, ss_batch** out) {
     if (!ctx || !out) return SS_INVALID_ARG;
+    DevGuard dg(ctx->device);
     ss_batch* b = new ss_batch();
     if (ss_status s = upload(ctx, desc, b)) {
         cudaFree(b->dev);
@@ -1229,6 +1287,7 @@ SS_API ss_status ss_batch_upload(ss_ctx* ctx, const ss_batch_desc* desc, ss_batc
 SS_API void ss_batch_free(ss_ctx* ctx, ss_batch* b) {
     if (!b) return;
     if (ctx) {
+        DevGuard dg(ctx->device);
         cudaStreamSynchronize(ctx->st);
         if (ctx->last == b) ctx->last = nullptr;
     }
@@ -1238,20 +1297,22 @@ SS_API void ss_batch_free(ss_ctx* ctx, ss_batch* b) {
 
 SS_API ss_status ss_forward_enqueue(ss_ctx* ctx, const ss_batch* b) {
     if (!ctx || !b) return SS_INVALID_ARG;
+    DevGuard dg(ctx->device);
     if (ss_status s = ensure_workspace(ctx, b->T, std::max(b->n_out, 1), b->part_rows)) return s;
     return enqueue_forward(ctx, b);
 }
 
 SS_API ss_status ss_read_outputs(ss_ctx* ctx, const ss_batch* b, float* logits, int32_t* next) {
     if (!ctx || !b) return SS_INVALID_ARG;
+    DevGuard dg(ctx->device);
     return read_outputs(ctx, b, logits, next);
 }
 
 SS_API ss_status ss_forward_hybrid(ss_ctx* ctx, const ss_batch_desc* desc, float* logits, int32_t* next,
                                    float* elapsed_ms) {
     if (!ctx) return SS_INVALID_ARG;
-    CK(cudaEventRecord(ctx->ev0, ctx->st));
-    if (ss_status s = upload(ctx, desc, &ctx->scratch)) return s;
+    DevGuard dg(ctx->device);
+    if (ss_status s = upload(ctx, desc, &ctx->scratch, ctx->ev0)) return s;
     if (ss_status s = enqueue_forward(ctx, &ctx->scratch)) return s;
     CK(cudaEventRecord(ctx->ev1, ctx->st));
     if (ss_status s = read_outputs(ctx, &ctx->scratch, logits, next)) return s;
@@ -1264,14 +1325,17 @@ SS_API void* ss_stream(ss_ctx* ctx) { return ctx ? static_cast<void*>(ctx->st) :
 
 SS_API ss_status ss_synchronize(ss_ctx* ctx) {
     if (!ctx) return SS_INVALID_ARG;
+    DevGuard dg(ctx->device);
+    if (ctx->ipc) CK(cudaMemcpyAsync(ctx->host_err, ctx->dev_err, 4, cudaMemcpyDeviceToHost, ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
-    return SS_OK;
+    return check_dev_err(ctx);
 }
 
 SS_API ss_status ss_kv_fill_synthetic(ss_ctx* ctx, const int32_t* block_table, int32_t n_blocks, int32_t rid,
                                       int32_t n_tokens, uint64_t seed) {
     if (!ctx || !block_table || n_tokens < 0 || int64_t(n_blocks) * ctx->bs < n_tokens)
         return fail(ctx, SS_INVALID_ARG, "bad synthetic fill arguments");
+    DevGuard dg(ctx->device);
     for (int b = 0; b < n_blocks; ++b)
         if (block_table[b] < 0 || block_table[b] >= ctx->nblocks) return fail(ctx, SS_OUT_OF_KV, "block outside pool");
     int32_t* d = nullptr;
@@ -1293,6 +1357,7 @@ SS_API ss_status ss_set_profiling(ss_ctx* ctx, int32_t enabled) {
 
 SS_API ss_status ss_kernel_times(ss_ctx* ctx, double* ms_out, int64_t* launches_out, int32_t reset) {
     if (!ctx) return SS_INVALID_ARG;
+    DevGuard dg(ctx->device);
     CK(cudaStreamSynchronize(ctx->st));
     collect_prof(ctx);
     for (int k = 0; k < SS_K_NUM_CLASSES; ++k) {
@@ -1313,10 +1378,10 @@ SS_API int64_t ss_launch_count(ss_ctx* ctx) { return ctx ? ctx->total_launches :
 SS_API ss_status ss_k_gemm(ss_ctx* ctx, const void* A, const void* B, void* D, int32_t M, int32_t N, int32_t K,
                            int32_t epi) {
     if (!ctx || epi < 0 || epi > 3) return fail(ctx, SS_INVALID_ARG, "bad gemm arguments");
+    DevGuard dg(ctx->device);
     GemmPlan p;
-    int ldo = epi == EPI_SWIGLU ? N / 2 : N;
-    if (const char* f = getenv("SS_GEMM_LDO_PAD")) ldo += atoi(f);  // dev: padded output rows
-    if (!gemm_prepare(p, A, uint64_t(M), B, M, N, K, D, ldo, epi, ctx->num_sms))
+    const int ldo = (epi == EPI_SWIGLU ? N / 2 : N) + ctx->tu.ldo_pad;  // dev: padded output rows
+    if (!gemm_prepare(p, A, uint64_t(M), B, M, N, K, D, ldo, epi, ctx->num_sms, ctx->tu))
         return fail(ctx, SS_INVALID_ARG, "gemm shape unsupported (N%32, K%8, SwiGLU N%64) or tensor map failed");
     p.part = ctx->sk_part;
     p.flags = ctx->sk_flags;
@@ -1327,6 +1392,7 @@ SS_API ss_status ss_k_gemm(ss_ctx* ctx, const void* A, const void* B, void* D, i
 SS_API ss_status ss_k_rmsnorm(ss_ctx* ctx, const float* x, const void* w, void* out, const int32_t* rows, int32_t M,
                               int32_t h, float eps) {
     if (!ctx || h % 8) return fail(ctx, SS_INVALID_ARG, "rmsnorm needs h % 8 == 0");
+    DevGuard dg(ctx->device);
     return launch(ctx, SS_K_RMSNORM, 1, [&] {
         return rmsnorm_launch(x, static_cast<const bf16*>(w), static_cast<bf16*>(out), rows, M, h, eps, ctx->st);
     });
@@ -1335,6 +1401,7 @@ SS_API ss_status ss_k_rmsnorm(ss_ctx* ctx, const float* x, const void* w, void* 
 SS_API ss_status ss_k_rope_append(ss_ctx* ctx, const void* qkv, void* q_out, const int32_t* pos, const int64_t* slot,
                                   int32_t T, int32_t layer) {
     if (!ctx || layer < 0 || layer >= ctx->L || !ctx->kc) return fail(ctx, SS_INVALID_ARG, "bad rope/append args");
+    DevGuard dg(ctx->device);
     return launch(ctx, SS_K_ROPE_APPEND, 1, [&] {
         return rope_append_launch(static_cast<const bf16*>(qkv), static_cast<bf16*>(q_out), pos, slot, ctx->rope, T,
                                   ctx->nq_l, ctx->nkv_l, ctx->hd, ctx->bs, ctx->kc + size_t(layer) * ctx->layer_stride,
@@ -1344,6 +1411,7 @@ SS_API ss_status ss_k_rope_append(ss_ctx* ctx, const void* qkv, void* q_out, con
 
 SS_API ss_status ss_k_attention(ss_ctx* ctx, const ss_batch* b, const void* q, void* o, int32_t layer) {
     if (!ctx || !b || layer < 0 || layer >= ctx->L) return fail(ctx, SS_INVALID_ARG, "bad attention args");
+    DevGuard dg(ctx->device);
     if (ss_status s = ensure_workspace(ctx, b->T, std::max(b->n_out, 1), b->part_rows)) return s;
     const AttnParams ap = attn_params(ctx, b, static_cast<const bf16*>(q), static_cast<bf16*>(o), layer);
     if (ss_status s = launch(ctx, SS_K_ATTN, 1, [&] { return attention_launch(ap, ctx->tm_k, ctx->tm_v, ctx->st); })) return s;

@@ -155,24 +155,41 @@ __global__ void residual_add_kernel(float* __restrict__ x, const __nv_bfloat16* 
 // after a flag barrier over peer memory each rank reads all ranks' partials (NVLink
 // P2P loads, fixed rank order: the sum is bitwise identical on every rank), adds them in
 // fp32 to the residual and emits the bf16 copy and per-chunk sums of squares.
-__device__ __forceinline__ void ipc_barrier(const IpcPeers& pe, uint32_t epoch) {
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Returns false (CTA-uniform) when a peer missed the collective: the error word is set
+// and the caller skips its work, so a stalled rank surfaces as a status, not a trap.
+__device__ __forceinline__ bool ipc_barrier(const IpcPeers& pe, uint32_t epoch) {
+    __shared__ int ok;
     // one thread per CTA: CTA 0 signals every rank (its own flag slot in each rank's
     // array), then every CTA waits for all ranks' flags of this epoch
     if (threadIdx.x == 0) {
+        ok = 1;
         if (blockIdx.x == 0) {
             __threadfence_system();
             for (int r = 0; r < pe.n; ++r)
                 asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(pe.flags[r] + pe.rank), "r"(epoch) : "memory");
         }
-        for (int r = 0; r < pe.n; ++r) {
-            uint32_t v, spins = 0;
-            do {
+        const uint64_t t0 = globaltimer_ns();
+        for (int r = 0; r < pe.n && ok; ++r) {
+            uint32_t v;
+            for (int spin = 0;; ++spin) {
                 asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(pe.flags[pe.rank] + r) : "memory");
-                if (++spins == (1u << 30)) __trap();
-            } while (int32_t(v - epoch) < 0);
+                if (int32_t(v - epoch) >= 0) break;
+                if ((spin & 255) == 255 && globaltimer_ns() - t0 > pe.timeout_ns) {
+                    atomicCAS(pe.err, 0u, kDevErrPeerTimeout | (uint32_t(r) << 8));
+                    ok = 0;
+                    break;
+                }
+            }
         }
     }
     __syncthreads();
+    return ok != 0;
 }
 
 __global__ void ipc_allreduce_residual_kernel(float* __restrict__ x, const IpcPeers pe, int slot, uint32_t epoch,
@@ -180,7 +197,7 @@ __global__ void ipc_allreduce_residual_kernel(float* __restrict__ x, const IpcPe
                                               int h) {
     pdl_launch_dependents();
     pdl_wait();  // this rank's partial is complete
-    ipc_barrier(pe, epoch);
+    if (!ipc_barrier(pe, epoch)) return;
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;  // multiple of 32
     for (int64_t base = blockIdx.x * int64_t(blockDim.x); base < n8; base += stride) {
         const int64_t i = base + threadIdx.x;
@@ -218,7 +235,7 @@ __global__ void ipc_gather_logits_kernel(const IpcPeers pe, uint32_t epoch, floa
                                          int vl) {
     pdl_launch_dependents();
     pdl_wait();
-    ipc_barrier(pe, epoch);
+    if (!ipc_barrier(pe, epoch)) return;
     const int64_t n = int64_t(pe.n) * rows * vl;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
         const int64_t r = i / (int64_t(rows) * vl), rem = i % (int64_t(rows) * vl), row = rem / vl, c = rem % vl;
@@ -359,13 +376,20 @@ __global__ void init_weight_kernel(__nv_bfloat16* __restrict__ w, const WeightIn
                 tag = SS_TAG_LMHEAD;
                 gr = uint64_t(int64_t(wi.rank) * wi.vocab_l + i);
                 break;
-            default: {
-                w[idx] = __ushort_as_bfloat16(uint16_t(0x3F80));  // 1.0
+            default: {  // W_NORM: one gain vector [1][cols]
+                w[idx] = __ushort_as_bfloat16(ss_norm_gain_bf16(wi.seed, wi.layer, wi.norm, j));
                 continue;
             }
         }
         w[idx] = __ushort_as_bfloat16(ss_synth_bf16(wi.seed, tag, gr, gc, sc));
     }
+}
+
+__global__ void fold_gain_kernel(__nv_bfloat16* __restrict__ w, const __nv_bfloat16* __restrict__ g, int64_t rows,
+                                 int64_t cols) {
+    const int64_t n = rows * cols;
+    for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < n; idx += int64_t(gridDim.x) * blockDim.x)
+        w[idx] = __float2bfloat16_rn(__bfloat162float(w[idx]) * __bfloat162float(g[idx % cols]));
 }
 
 __global__ void kv_fill_kernel(__nv_bfloat16* __restrict__ kb, __nv_bfloat16* __restrict__ vb, int64_t lstride,
@@ -458,6 +482,11 @@ cudaError_t peer_sum_launch(__nv_bfloat16* out, const PeerBufs& src, int n_src, 
 
 cudaError_t init_weight_launch(__nv_bfloat16* w, const WeightInit& wi, cudaStream_t st) {
     init_weight_kernel<<<grid_for(wi.rows * wi.cols, 256), 256, 0, st>>>(w, wi);
+    return cudaGetLastError();
+}
+
+cudaError_t fold_gain_launch(__nv_bfloat16* w, const __nv_bfloat16* gain, int64_t rows, int64_t cols, cudaStream_t st) {
+    fold_gain_kernel<<<grid_for(rows * cols, 256), 256, 0, st>>>(w, gain, rows, cols);
     return cudaGetLastError();
 }
 

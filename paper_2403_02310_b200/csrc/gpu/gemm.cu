@@ -312,12 +312,14 @@ __device__ __forceinline__ void add_rows(uint32_t (&v)[32], const uint4* ep, int
 
 template <int CG, int BN, int EPI, int AR>
 __global__ void __launch_bounds__(kThreads, 1)
-    gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
-                        int N, int K, void* __restrict__ out, int ldo, int num_mt, int num_tiles,
+    gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M_rows,
+                        int row0, int N, int K, void* __restrict__ out, int ldo, int num_mt, int num_tiles,
                         float* __restrict__ part, uint32_t* __restrict__ flags, uint32_t epoch, int sk_mode,
                         int sk_slices, const EpiArgs ea) {
     using Cfg = GemmCfg<CG, BN, AR>;
     constexpr int STAGES = Cfg::STAGES;
+    // rows [row0, row0 + M_rows) of A / the output / every row-indexed epilogue operand
+    const int M = row0 + M_rows;  // exclusive row end
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
@@ -419,7 +421,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             SegIter sit(sk_mode, gid, G, num_kb, num_tiles, rg, sk_slices, P);
             for (Seg sg; sit.next(sg);) {
                 const int t = sg.t, kb0 = sg.kb0, kb1 = sg.kb1;
-                const int m0 = (t % num_mt) * Cfg::TILE_M + 128 * int(rank);
+                const int m0 = row0 + (t % num_mt) * Cfg::TILE_M + 128 * int(rank);
                 const int n0 = (t / num_mt) * BN + Cfg::B_ROWS * int(rank);
                 for (int kb = kb0; kb < kb1; ++kb, ++it) {
                     const bool pre = it < npre;  // B already in flight, slot fresh
@@ -528,7 +530,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         SegIter sit(sk_mode, gid, G, num_kb, num_tiles, rg, sk_slices, P);
         for (Seg sg; sit.next(sg);) {
             const int t = sg.t, kb0 = sg.kb0, kb1 = sg.kb1;
-            const int m0 = (t % num_mt) * Cfg::TILE_M, n0 = (t / num_mt) * BN;
+            const int m0 = row0 + (t % num_mt) * Cfg::TILE_M, n0 = (t / num_mt) * BN;
             const int row = m0 + rloc;
             const int rbase = row - lane;  // first row of this warp
             // RMSNorm of the A row, folded in: scale = rsqrt(mean(x^2) + eps). The
@@ -958,15 +960,25 @@ EncodeFn encode_fn() {
     return fn;
 }
 
+// Per-device launch state of one kernel instantiation: the smem attribute is set and the
+// co-resident cluster count measured once per device.
+constexpr int kMaxDevices = 64;
+struct DevOnce {
+    bool attr[kMaxDevices] = {};
+    int resident[kMaxDevices] = {};
+};
+
 template <int CG, int BN, int EPI, int AR = 128>
 cudaError_t launch_t(const GemmPlan& p, cudaStream_t st) {
     using Cfg = GemmCfg<CG, BN, AR>;
-    static bool attr_set = false;
+    static DevOnce once;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
     auto kern = gemm_tcgen05_kernel<CG, BN, EPI, AR>;
-    if (!attr_set) {
+    if (!once.attr[dev]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
         if (e != cudaSuccess) return e;
-        attr_set = true;
+        once.attr[dev] = true;
     }
     const int num_mt = (p.M + Cfg::TILE_M - 1) / Cfg::TILE_M;
     const int num_n = (p.N + BN - 1) / BN;
@@ -982,23 +994,24 @@ cudaError_t launch_t(const GemmPlan& p, cudaStream_t st) {
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[1].val.programmaticStreamSerializationAllowed = pdl_allowed();
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
     // Groups that can be co-resident: stream-K heads spin on other groups, so the
     // grid must never exceed one resident wave.
-    static int resident = 0;
-    if (resident == 0) {
+    if (once.resident[dev] == 0) {
         cfg.gridDim = dim3(CG * (p.num_sms / CG));
-        int n = 0;
-        if (CG > 1 && cudaOccupancyMaxActiveClusters(&n, kern, &cfg) == cudaSuccess && n > 0) resident = n;
-        else resident = p.num_sms / CG;
-        if (resident > p.num_sms / CG) resident = p.num_sms / CG;
+        int n = 0, r;
+        if (CG > 1 && cudaOccupancyMaxActiveClusters(&n, kern, &cfg) == cudaSuccess && n > 0) r = n;
+        else r = p.num_sms / CG;
+        once.resident[dev] = r > p.num_sms / CG ? p.num_sms / CG : r;
     }
+    int resident = once.resident[dev];
+    if (p.max_groups > 0 && p.max_groups < resident) resident = p.max_groups;
     int mode = p.sk_mode, S = p.splits < 1 ? 1 : p.splits;
     if (mode < 0) mode = S > 1 ? 2 : 0;
-    if (const char* f = getenv("SS_GEMM_SK")) mode = atoi(f);
-    if (const char* f = getenv("SS_GEMM_SPLITS")) S = atoi(f);
+    if (p.force_sk >= 0) mode = p.force_sk;
+    if (p.force_splits > 0) S = p.force_splits;
     if (mode == 3 && num_mt > resident) mode = 0;
     const int rem = tiles % resident;  // tiles of the ragged last wave
     if (mode == 2 && rem > 0 && long(rem) * S > resident) S = resident / rem;
@@ -1013,10 +1026,10 @@ cudaError_t launch_t(const GemmPlan& p, cudaStream_t st) {
         groups = int(gs) * num_mt;
     }
     cfg.gridDim = dim3(CG * groups);
-    if (getenv("SS_GEMM_DEBUG"))
+    if (p.debug)
         fprintf(stderr, "gemm cg=%d bn=%d epi=%d M=%d N=%d K=%d tiles=%d resident=%d mode=%d groups=%d\n", CG, BN,
                 EPI, p.M, p.N, p.K, tiles, resident, mode, groups);
-    return cudaLaunchKernelEx(&cfg, kern, p.tmA, p.tmB, p.M, p.N, p.K, p.out, p.ldo, num_mt, tiles, p.part,
+    return cudaLaunchKernelEx(&cfg, kern, p.tmA, p.tmB, p.M, p.row0, p.N, p.K, p.out, p.ldo, num_mt, tiles, p.part,
                               p.flags, p.epoch, mode, S, p.ea);
 }
 
@@ -1024,6 +1037,36 @@ cudaError_t launch_t(const GemmPlan& p, cudaStream_t st) {
 constexpr int kBn2[] = {64, 96, 128, 160, 192, 224, 256};
 
 }  // namespace
+
+Tuning tuning_from_env() {
+    Tuning t;
+    auto geti = [](const char* name, int& v) {
+        if (const char* f = getenv(name)) v = atoi(f);
+    };
+    geti("SS_ATTN_TC_MODE", t.attn_tc_mode);
+    geti("SS_ATTN_ORDER", t.attn_order);
+    geti("SS_ATTN_L2HINT", t.attn_l2hint);
+    geti("SS_ATTN_TC2_FIRST", t.attn_tc2_first);
+    geti("SS_GEMM_L2HINT", t.gemm_l2hint);
+    geti("SS_GEMM_SK", t.gemm_sk);
+    geti("SS_GEMM_SPLITS", t.gemm_splits);
+    geti("SS_GEMM_BN", t.gemm_bn);
+    geti("SS_GEMM_CG", t.gemm_cg);
+    if (getenv("SS_GEMM_AR128")) t.gemm_ar128 = 1;
+    if (getenv("SS_GEMM_DEBUG")) t.gemm_debug = 1;
+    geti("SS_GEMM_LDO_PAD", t.ldo_pad);
+    static const char* names[5] = {"SS_GEMM_QKV", "SS_GEMM_O", "SS_GEMM_GATEUP", "SS_GEMM_DOWN", "SS_GEMM_LMHEAD"};
+    for (int i = 0; i < 5; ++i)
+        if (const char* f = getenv(names[i])) {
+            int md = -1, bn = 0, sp = 1;
+            if (sscanf(f, "%d,%d,%d", &md, &bn, &sp) >= 2) {
+                t.gemm_force[i][0] = md;
+                t.gemm_force[i][1] = bn;
+                t.gemm_force[i][2] = sp;
+            }
+        }
+    return t;
+}
 
 bool make_tmap_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
                   uint32_t box_cols) {
@@ -1038,13 +1081,8 @@ bool make_tmap_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-GemmShape gemm_pick(int M, int N, int K, int epi, int num_sms) {
-    int force_bn = 0, force_cg = 0, force_s = 0;
-    if (const char* f = getenv("SS_GEMM_BN")) force_bn = atoi(f);  // tuning overrides (dev only)
-    if (const char* f = getenv("SS_GEMM_CG")) force_cg = atoi(f);
-    if (const char* f = getenv("SS_GEMM_SPLITS")) force_s = atoi(f);
-    int force_mode = -1;
-    if (const char* f = getenv("SS_GEMM_SK")) force_mode = atoi(f);
+GemmShape gemm_pick(int M, int N, int K, int epi, int num_sms, const Tuning& tu) {
+    const int force_bn = tu.gemm_bn, force_cg = tu.gemm_cg, force_s = tu.gemm_splits, force_mode = tu.gemm_sk;
     const bool swiglu = epi == EPI_SWIGLU;
     GemmShape best{M > 128 ? 2 : 1, swiglu ? 256 : 128, 1, -1};
     double best_cost = 1e30;
@@ -1102,14 +1140,14 @@ GemmShape gemm_pick(int M, int N, int K, int epi, int num_sms) {
         consider(1, 256);
         consider(1, 128);
     }
-    best.ar = (best.cg == 1 && M <= 32 && !getenv("SS_GEMM_AR128")) ? 32 : 128;
+    best.ar = (best.cg == 1 && M <= 32 && !tu.gemm_ar128) ? 32 : 128;
     if (M > 128 && force_cg != 1)
         for (int bn : kBn2) consider(2, bn);
     return best;
 }
 
 bool gemm_prepare(GemmPlan& p, const void* A, uint64_t a_rows, const void* B, int M, int N, int K, void* out,
-                  int ldo, int epi, int num_sms, int bn) {
+                  int ldo, int epi, int num_sms, const Tuning& tu, int bn) {
     if (M < 1 || N < 32 || K < 16 || N % 32 || K % 8 || (epi == EPI_SWIGLU && N % 64) || epi == EPI_QKV) return false;
     p.M = M;
     p.N = N;
@@ -1118,7 +1156,10 @@ bool gemm_prepare(GemmPlan& p, const void* A, uint64_t a_rows, const void* B, in
     p.ldo = ldo;
     p.epi = epi;
     p.num_sms = num_sms;
-    const GemmShape s = gemm_pick(M, N, K, epi, num_sms);
+    const GemmShape s = gemm_pick(M, N, K, epi, num_sms, tu);
+    p.force_sk = tu.gemm_sk;
+    p.force_splits = tu.gemm_splits;
+    p.debug = tu.gemm_debug;
     p.cg = s.cg;
     p.bn = bn ? bn : s.bn;
     p.splits = s.splits;

@@ -45,9 +45,30 @@ struct EpiArgs {
     int l2hint = 0;  // operand L2 priority bits: 1 A evict-last, 2 B evict-first
 };
 
+// Developer tuning overrides (the SS_* environment variables the scripts/ A/B sweeps set),
+// read once per context at ss_create by tuning_from_env() and carried explicitly to the
+// launchers; nothing on the launch path reads the environment. Defaults = production.
+struct Tuning {
+    int attn_tc_mode = -1;    // SS_ATTN_TC_MODE: force the tensor-core prefill flavour (1..3)
+    int attn_order = 0;       // SS_ATTN_ORDER=1: prefill row tiles first in the work list
+    int attn_l2hint = 1;      // SS_ATTN_L2HINT: K/V L2 priority bits (AttnParams::kv_hint)
+    int attn_tc2_first = 0;   // SS_ATTN_TC2_FIRST: compact prefill launch before the decodes
+    int gemm_l2hint = 3;      // SS_GEMM_L2HINT: operand L2 priority bits (EpiArgs::l2hint)
+    int gemm_sk = -1;         // SS_GEMM_SK: force the schedule mode
+    int gemm_splits = 0;      // SS_GEMM_SPLITS: force the split count
+    int gemm_bn = 0;          // SS_GEMM_BN
+    int gemm_cg = 0;          // SS_GEMM_CG
+    int gemm_ar128 = 0;       // SS_GEMM_AR128: no 32-row A stages for M <= 32
+    int gemm_debug = 0;       // SS_GEMM_DEBUG: print each launch's schedule
+    int gemm_force[5][3] = {{-1, 0, 1}, {-1, 0, 1}, {-1, 0, 1}, {-1, 0, 1}, {-1, 0, 1}};  // SS_GEMM_<QKV|O|GATEUP|DOWN|LMHEAD>=mode,bn[,splits]
+    int ldo_pad = 0;          // SS_GEMM_LDO_PAD (ss_k_gemm only)
+};
+Tuning tuning_from_env();
+
 struct GemmPlan {
     CUtensorMap tmA, tmB;  // 64-byte aligned members of a 64-aligned struct
     int M = 0, N = 0, K = 0;
+    int row0 = 0;  // the GEMM covers rows [row0, row0 + M) of A, out and the epilogue operands
     void* out = nullptr;
     int ldo = 0;
     int epi = 0;
@@ -63,6 +84,8 @@ struct GemmPlan {
     int sk_mode = -1;  // -1 auto, 0 whole tiles round-robin, 1 stream-K, 2 lockstep split-K,
                        // 3 M-lockstep stream-K (super-groups of num_mt CTA pairs)
     int splits = 1;    // K slices per tile for mode 2 (tiles * splits must fit one resident wave)
+    int force_sk = -1, force_splits = 0, debug = 0;  // Tuning overrides applied at launch
+    int max_groups = 0;  // > 0: at most this many CTA groups (SM budget of a concurrent launch)
     EpiArgs ea;
 } __attribute__((aligned(64)));
 
@@ -78,10 +101,10 @@ struct GemmShape {
 bool make_tmap_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
                   uint32_t box_cols);
 // Tile shape for an M x N GEMM: minimises wave-quantised time over the compiled shapes.
-GemmShape gemm_pick(int M, int N, int K, int epi, int num_sms);
+GemmShape gemm_pick(int M, int N, int K, int epi, int num_sms, const Tuning& tu);
 // A is [a_rows >= M][K] bf16; B is [N][K] bf16; out row stride ldo elements.
 bool gemm_prepare(GemmPlan& p, const void* A, uint64_t a_rows, const void* B, int M, int N, int K, void* out,
-                  int ldo, int epi, int num_sms, int bn = 0);
+                  int ldo, int epi, int num_sms, const Tuning& tu, int bn = 0);
 cudaError_t gemm_launch(const GemmPlan& p, cudaStream_t st);
 
 // ------------------------------------------------------------------ K1 attention
@@ -133,6 +156,7 @@ struct AttnParams {
     int32_t wait_at_end;         // set by attention_launch for the second of its two launches
     int32_t num_sms;
     int32_t kv_hint;             // L2 priority bits: 1 decode K/V evict-first, 2 prefill K/V evict-last
+    int32_t tc2_first;           // Tuning::attn_tc2_first
 };
 // 2D TMA views [L * nblocks * nkv * 16][hd] of the K and V pools (box 16 x 64, SWIZZLE_128B).
 bool attention_tmaps(CUtensorMap* tk, CUtensorMap* tv, const void* kc, const void* vc, int64_t total_rows, int hd);
@@ -160,7 +184,13 @@ struct IpcPeers {
     const float* logits[kIpcMaxRanks];
     uint32_t* flags[kIpcMaxRanks];
     int n, rank;
+    // A peer that does not reach a collective within timeout_ns is reported, not trapped:
+    // the waiting CTAs store kDevErrPeerTimeout | peer << 8 into *err (this rank's device
+    // error word, read by the host after the forward) and skip the collective's work.
+    uint32_t* err;
+    uint64_t timeout_ns;
 };
+constexpr uint32_t kDevErrPeerTimeout = 1;
 cudaError_t ipc_allreduce_residual_launch(float* x, const IpcPeers& pe, int slot, uint32_t epoch,
                                           __nv_bfloat16* xb, float* ssq, int T, int h, cudaStream_t st);
 cudaError_t ipc_gather_logits_launch(const IpcPeers& pe, uint32_t epoch, float* out, int rows, int vl,
@@ -178,15 +208,19 @@ cudaError_t peer_sum_launch(__nv_bfloat16* out, const PeerBufs& src, int n_src, 
 cudaError_t gather_vocab_launch(const float* in, float* out, int tp, int rows, int vl, cudaStream_t st);
 
 // Synthetic initialisers (ss_synth.h).
-enum WeightKind { W_QKV = 0, W_O = 1, W_GU = 2, W_DOWN = 3, W_EMBED = 4, W_LMHEAD = 5, W_ONES = 6 };
+enum WeightKind { W_QKV = 0, W_O = 1, W_GU = 2, W_DOWN = 3, W_EMBED = 4, W_LMHEAD = 5, W_NORM = 6 };
 struct WeightInit {
     int kind, layer, rank;
     int64_t rows, cols;
     int nq_l, nkv_l, hd, ffn_l, vocab_l;
     uint64_t seed;
     float scale_a, scale_b, scale_c;  // per-tag scales (q/k/v or gate/up)
+    int norm;                         // W_NORM: which gain (SS_NORM_*)
 };
 cudaError_t init_weight_launch(__nv_bfloat16* w, const WeightInit& wi, cudaStream_t st);
+// w[r][c] = bf16(w[r][c] * gain[c]): an RMSNorm gain folded into the consuming projection
+// (x_hat * g) . W^T = x_hat . (W diag(g))^T.
+cudaError_t fold_gain_launch(__nv_bfloat16* w, const __nv_bfloat16* gain, int64_t rows, int64_t cols, cudaStream_t st);
 cudaError_t kv_fill_launch(__nv_bfloat16* kbase, __nv_bfloat16* vbase, int64_t layer_stride, int L,
                            const int32_t* bt_dev, int n_tokens, int rid, int nkv_l, int kv_off, int nkv_g, int hd,
                            int bs, uint64_t seed, cudaStream_t st);
@@ -194,11 +228,6 @@ cudaError_t kv_fill_launch(__nv_bfloat16* kbase, __nv_bfloat16* vbase, int64_t l
 }  // namespace ssk
 
 namespace ssk {
-// SS_NO_PDL=1 (dev): launch without programmatic dependent launch.
-inline int pdl_allowed() {
-    static const int v = getenv("SS_NO_PDL") ? 0 : 1;
-    return v;
-}
 // Launch with the programmatic-stream-serialization attribute (PDL) and an
 // optional cluster shape. Every kernel in this library calls pdl_wait() before
 // its first global access, so PDL launches are always safe.
@@ -213,7 +242,7 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
     cudaLaunchAttribute attr[2];
     int n = 0;
     attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[n].val.programmaticStreamSerializationAllowed = pdl_allowed();
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
     ++n;
     if (cluster_x > 1) {
         attr[n].id = cudaLaunchAttributeClusterDimension;

@@ -111,10 +111,19 @@ ss::Batch to_batch(const ssh_entry* e, int32_t n) {
 // engine.cpp:227). Time is the library's CUDA-event measurement.
 class GpuExecutor final : public ss::StepExecutor {
 public:
-    GpuExecutor(ss_ctx* ctx, std::uint64_t seed) : ctx_(ctx), seed_(seed) {
+    // The GPU step is one whole-model forward on this rank's TP shard: the replica must be
+    // un-pipelined (the reference divides iteration_time by pp, costmodel.cpp:55; a GPU
+    // pipeline is not built) and its tp degree must be the context's (every rank runs the
+    // same replicated schedule).
+    GpuExecutor(ss_ctx* ctx, std::uint64_t seed, const ss::ReplicaConfig& rc) : ctx_(ctx), seed_(seed) {
         ss_model_cfg mc;
         int32_t r, t;
         if (ss_model_config(ctx, &mc, &r, &t) != SS_OK) throw ss::ContractViolation("invalid GPU context");
+        if (rc.pp != 1)
+            throw ss::ContractViolation("GPU model step: pp_degree must be 1 (the forward covers all layers)");
+        if (rc.tp != t)
+            throw ss::ContractViolation("GPU model step: tp_degree " + std::to_string(rc.tp) +
+                                        " differs from the GPU context's tp_size " + std::to_string(t));
         vocab_ = mc.vocab;
     }
     double step_ms(const ss::Batch& b, const ss::KvLedger& kv, const std::vector<ss::Request>& reqs) override {
@@ -230,7 +239,7 @@ ss_status ssh_simulate(const ssh_replica_cfg* cfg, const ssh_cost_params* params
         const ss::ReplicaConfig rc = to_cfg(*cfg);
         const ss::CostParams cp = to_params(*params);
         std::unique_ptr<ss::StepExecutor> exec;
-        if (gpu) exec = std::make_unique<GpuExecutor>(gpu, token_seed);
+        if (gpu) exec = std::make_unique<GpuExecutor>(gpu, token_seed, rc);
         else exec = std::make_unique<ss::CostModelExecutor>(cp, rc.tp, rc.pp);
         auto r = std::make_unique<ssh_report>();
         r->rep = ss::simulate(rc, cp, reqs, *exec, so);
@@ -352,7 +361,7 @@ ss_status ssh_capacity_search(const ssh_replica_cfg* cfg, const ssh_cost_params*
             ss::SimOptions so;
             so.keep_events = false;  // probe_sim_options, cli.cpp:373-379
             std::unique_ptr<ss::StepExecutor> exec;
-            if (gpu) exec = std::make_unique<GpuExecutor>(gpu, token_seed);
+            if (gpu) exec = std::make_unique<GpuExecutor>(gpu, token_seed, rc);
             else exec = std::make_unique<ss::CostModelExecutor>(cp, rc.tp, rc.pp);
             return ss::summarize(ss::simulate(rc, cp, trace, *exec, so));
         };

@@ -83,17 +83,6 @@ class Batch:
     def handle(self):
         return self._h
 
-    def ipc_connect(self, allgather, max_tokens: int = 8192):
-        """CUDA-IPC TP transport (a rank created without an NCCL id): exports this rank's
-        exchange region, all-gathers the 64-byte handles with `allgather(bytes) -> list`
-        (rank order, e.g. torch.distributed.all_gather_object) and maps every peer's."""
-        buf = (C.c_char * 64)()
-        self._check(gpu_lib().ss_ipc_export(self._h, max_tokens, buf))
-        handles = allgather(bytes(buf))
-        assert len(handles) == self.tp_size and all(len(x) == 64 for x in handles)
-        allh = (C.c_char * (64 * self.tp_size)).from_buffer_copy(b"".join(handles))
-        self._check(gpu_lib().ss_ipc_open(self._h, allh))
-
     def free(self):
         if self._h is not None and self._h.value:
             gpu_lib().ss_batch_free(self._fwd._h, self._h)

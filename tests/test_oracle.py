@@ -1,8 +1,11 @@
 """The fp32 CPU oracle (oracle/liboracle.so) — pinned before it is trusted.
 
 1. HF pin: chunked prefill + decodes over paged KV through the oracle must
-   reproduce HF transformers' full-sequence fp32 logits (tests/golden/
-   hf_tiny_logits.npz, made by tests/golden/make_hf_golden.py).
+   reproduce HF transformers' full-sequence fp32 logits, non-unit RMSNorm gains
+   included, at two shapes: the tiny model (hd 64, GQA 2, theta 1e4;
+   tests/golden/hf_tiny_logits.npz) and the production head geometry (hd 128,
+   GQA 4, theta 5e6, positions past 2048; hf_hd128_gqa4_logits.npz), both made
+   by tests/golden/make_hf_golden.py.
 2. Tensor parallelism: the Megatron shard math with an explicit all-reduce
    (torch.distributed gloo, world_size 2) equals the unsharded forward.
 3. Paged KV: block tables from the host session are honoured (results do
@@ -19,12 +22,20 @@ from paper_2403_02310_b200 import gpu, host
 orc_mod = pytest.importorskip("oracle.forward")
 Oracle = orc_mod.Oracle
 
-GOLD = os.path.join(os.path.dirname(__file__), "golden", "hf_tiny_logits.npz")
+GOLDEN_DIR = os.path.join(os.path.dirname(__file__), "golden")
+GOLD = os.path.join(GOLDEN_DIR, "hf_tiny_logits.npz")
+HF_GOLDENS = ["hf_tiny_logits.npz", "hf_hd128_gqa4_logits.npz"]
 
 
-def _replay(orc, g, schedule, seed):
+def golden_shape(g):
+    f = lambda k: g["shape_" + k].item()
+    return gpu.ModelShape("hf_golden", int(f("num_layers")), int(f("hidden")), int(f("num_q_heads")),
+                          int(f("num_kv_heads")), int(f("head_dim")), int(f("ffn")), int(f("vocab")),
+                          rope_theta=float(f("rope_theta")), rms_eps=float(f("rms_eps")))
+
+
+def _replay(orc, g, schedule, seed, s):
     """schedule: list of steps, each a list of (rid, kind, tokens, prefix); returns {(rid,pos): logits}."""
-    s = gpu.MODELS["tiny"]
     sess = host.Session(4096, vocab=s.vocab, token_seed=seed)
     prompts = {}
     for step in schedule:
@@ -44,8 +55,8 @@ def _replay(orc, g, schedule, seed):
     return got
 
 
-def _schedule(seq_lens, prompts):
-    # stall-free style: decodes first, then chunks of <= 48 tokens per request per step
+def _schedule(seq_lens, prompts, chunk=48):
+    # stall-free style: decodes first, then chunks of <= `chunk` tokens per request per step
     steps, done = [], {i: 0 for i in range(len(seq_lens))}
     while any(done[i] < seq_lens[i] for i in done):
         step = []
@@ -55,20 +66,21 @@ def _schedule(seq_lens, prompts):
                 done[i] += 1
         for i, L in enumerate(seq_lens):
             if done[i] < prompts[i]:
-                c = min(48 - 7 * i, prompts[i] - done[i])
+                c = min(chunk - 7 * i, prompts[i] - done[i])
                 step.append((i, "prefill", c, done[i]))
                 done[i] += c
         steps.append(step)
     return steps
 
 
-def test_oracle_matches_hf_transformers():
-    g = np.load(GOLD)
-    s = gpu.MODELS["tiny"]
+@pytest.mark.parametrize("golden", HF_GOLDENS)
+def test_oracle_matches_hf_transformers(golden):
+    g = np.load(os.path.join(GOLDEN_DIR, golden))
+    s = golden_shape(g)
     seq = [int(x) for x in g["seq_lens"]]
     prompts = [seq[0] - 9, seq[1] - 40, seq[2] - 61]
     orc = Oracle(s, weight_seed=int(g["weight_seed"]), num_blocks=4096)
-    got = _replay(orc, g, _schedule(seq, prompts), int(g["token_seed"]))
+    got = _replay(orc, g, _schedule(seq, prompts, chunk=48 if seq[2] < 1000 else 400), int(g["token_seed"]), s)
     checked = 0
     for i in range(len(seq)):
         # the host token generator must reproduce the HF input ids exactly
@@ -153,3 +165,18 @@ def test_oracle_tensor_parallel_gloo():
     o.fill_descriptor_prefixes(d, 4)
     ref = o.forward(d)
     np.testing.assert_allclose(tp_logits, ref, rtol=1e-4, atol=1e-4)
+
+
+@pytest.mark.parametrize("tau,n_dec,kv,prefix,vocab", [(512, 32, 4096, 0, 32000), (2048, 32, 4096, 2048, 64000),
+                                                       (160, 8, 300, 40, 512)])
+def test_canonical_restatement_matches_host(tau, n_dec, kv, prefix, vocab):
+    """oracle/canonical.py (the CPU reference arm's input, no product library) builds the
+    same descriptor as the C++ host (ssh_desc_canonical), array for array."""
+    from oracle.canonical import CanonicalDesc
+
+    a = CanonicalDesc(tau, n_dec, kv, prefix, vocab=vocab, token_seed=7)
+    b = host.Descriptor.canonical(tau, n_dec, kv, prefix, vocab=vocab, token_seed=7)
+    assert a.pool_blocks == b.pool_blocks
+    ea, eb = a.arrays(), b.arrays()
+    for k in ("cu_q", "ctx_len", "pos", "token_ids", "slot", "block_table", "out_rows"):
+        assert np.array_equal(ea[k], eb[k]), k
