@@ -225,14 +225,20 @@ def run_ours(args):
     view = desc.view
     h2d = sum(a.nbytes for k, a in arrays.items())
     d2h = 4 * work["n_out"]
-    for _ in range(2):
-        fwd.forward(desc, logits=False)
-    barrier()
-    t0 = time.perf_counter()
-    for _ in range(args.e2e_steps):
-        _, nt, _ = fwd.forward(view, logits=False)
-    barrier()
-    e2e_ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / args.e2e_steps)
+    def e2e_time():
+        for _ in range(3):  # the shape's graph is captured on its second forward
+            fwd.forward(desc, logits=False)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            fwd.forward(view, logits=False)
+        barrier()
+        return max_over_ranks((time.perf_counter() - t0) * 1e3 / args.e2e_steps)
+
+    e2e_ms = e2e_time()  # CUDA graph replays (default)
+    fwd.set_graphs(False)
+    e2e_eager_ms = e2e_time()  # the same calls with eager launches, for the graph effect
+    fwd.set_graphs(True)
 
     peaks, peak_src = load_peaks()
     T = work["T"]
@@ -296,6 +302,12 @@ def run_ours(args):
     if world == 1 and args.tbt_requests > 0:
         batch.free()
         tbt = closed_loop_tbt(fwd, args.model, args.tau, args.tbt_requests, args.tbt_qps)
+        # the same closed loop with eager launches (graphs off): P99 TBT / wall beside it
+        fwd.set_graphs(False)
+        t_eager = closed_loop_tbt(fwd, args.model, args.tau, args.tbt_requests, args.tbt_qps, cost_clock=False)
+        fwd.set_graphs(True)
+        tbt["graphs_off"] = {k: t_eager[k] for k in ("p99_ms", "median_ms", "iter_ms_median", "wall_s")}
+        tbt["graphs"] = dict(zip(("captures", "replays"), fwd.graph_stats()))
 
     out = {
         "metric": METRIC, "value": T / (ms_step * 1e-3), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
@@ -311,7 +323,11 @@ def run_ours(args):
                    "l2": "inputs larger than L2 (all weights + KV re-read every step)",
                    "gpu_launches_per_step": launches / args.steps},
         "e2e": {"value": T / (e2e_ms * 1e-3), "unit": "tokens/s", "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "api": "ss_forward_hybrid (host descriptor arrays -> next tokens)"},
+                "d2h_bytes_per_step": d2h, "api": "ss_forward_hybrid (host descriptor arrays -> next tokens)",
+                "graphs": "CUDA graph replay of the batch shape (ss_set_graphs, default on)",
+                "gap_vs_device_ms": e2e_ms - ms_step,
+                "graphs_off": {"value": T / (e2e_eager_ms * 1e-3), "ms_per_step": e2e_eager_ms,
+                               "gap_vs_device_ms": e2e_eager_ms - ms_step}},
         "gpu_launches": launches,
         "roofline": roof,
         "whole_step_roofline": {"ms": whole_roof_ms, "frac": whole_roof_ms / ms_step, "alg_bytes": work["bytes"],
@@ -362,7 +378,7 @@ def time_canonical(fwd, shape, tau, prefix, steps, warmup, peaks, world, sync, m
             "whole_step_roofline": {"ms": roof, "frac": roof / ms}}
 
 
-def closed_loop_tbt(fwd, model, tau, n_requests, qps, seed=42):
+def closed_loop_tbt(fwd, model, tau, n_requests, qps, seed=42, cost_clock=True):
     """P99 TBT from a replayed synthetic trace: the restated engine (byte-identical
     to the reference's, tests/test_host_parity.py) runs the stall-free schedule
     with the real B200 forward as its model step (engine.cpp:227 seam); every
@@ -382,15 +398,17 @@ def closed_loop_tbt(fwd, model, tau, n_requests, qps, seed=42):
     rep = host.simulate(cfg, params, trace, gpu=fwd, token_seed=seed, keep_events=False)
     wall = time.perf_counter() - t0
     s = rep.summarize()
-    ref = host.simulate(cfg, params, trace, keep_events=False).summarize()
     iters = [mb.iteration_ms for mb in rep.microbatches()]
-    return {"p99_ms": s["tbt_p99_ms"], "median_ms": s["tbt_median_ms"], "ttft_median_ms": s["ttft_median_ms"],
+    out = {"p99_ms": s["tbt_p99_ms"], "median_ms": s["tbt_median_ms"], "ttft_median_ms": s["ttft_median_ms"],
             "throughput_tps": s["throughput_tps"], "iterations": len(iters),
             "iter_ms_median": sorted(iters)[len(iters) // 2], "iter_ms_max": max(iters), "wall_s": wall,
             "trace": f"openchat (median prompt 1730 / P90 5696, output 415 / 834), n={n_requests}, qps={qps}, "
-                     f"seed={seed}, stall_free tau={tau}",
-            "cost_model_clock": {"p99_ms": ref["tbt_p99_ms"], "ttft_median_ms": ref["ttft_median_ms"],
-                                 "throughput_tps": ref["throughput_tps"]}}
+                     f"seed={seed}, stall_free tau={tau}"}
+    if cost_clock:
+        ref = host.simulate(cfg, params, trace, keep_events=False).summarize()
+        out["cost_model_clock"] = {"p99_ms": ref["tbt_p99_ms"], "ttft_median_ms": ref["ttft_median_ms"],
+                                   "throughput_tps": ref["throughput_tps"]}
+    return out
 
 
 def reference_cost_model_ms(model, tau, chunk_prefix, tp):

@@ -127,6 +127,23 @@ void ss_batch_free(ss_ctx* ctx, ss_batch* batch);
 void* ss_stream(ss_ctx* ctx);
 ss_status ss_synchronize(ss_ctx* ctx);
 
+/* CUDA graphs of the forward (default on). ss_forward_hybrid / ss_forward_enqueue capture
+ * one graph per batch shape (token / entry / logit-row counts, attention work-list
+ * counts, block-table width) the second time that shape is seen and replay it afterwards,
+ * so a step costs one graph launch of host work instead of ~6 launches per layer. Off
+ * while per-kernel profiling is on, for the one-device local group and on the NCCL
+ * transport. Outputs are bitwise identical with and without graphs. */
+ss_status ss_set_graphs(ss_ctx* ctx, int32_t enabled);
+/* All-reduce algorithm of the CUDA-IPC TP transport (after O and down): SS_AR_ONESHOT pulls
+ * every rank's partial (one barrier; (tp-1) messages of NVLink ingress per rank),
+ * SS_AR_TWOSHOT reduce-scatters then all-gathers over peer memory (two barriers;
+ * 2(tp-1)/tp messages per rank, the ring's byte count). SS_AR_AUTO (default): two-shot
+ * from tp >= 4 and a 1 MB message. Both are deterministic and identical on every rank. */
+enum { SS_AR_AUTO = 0, SS_AR_ONESHOT = 1, SS_AR_TWOSHOT = 2 };
+ss_status ss_set_tp_allreduce(ss_ctx* ctx, int32_t algo);
+/* Graphs captured and replayed since creation (either pointer may be NULL). */
+ss_status ss_graph_stats(ss_ctx* ctx, int64_t* captures, int64_t* replays);
+
 /* Fills KV positions [0, n_tokens) of one request (given its block table)
  * with the synthetic cache values of ss_synth.h, for every layer. Used to
  * stand up canonical batches whose decodes sit at a 4k context. */

@@ -162,6 +162,9 @@ def gpu_lib():
         _sig(lib, "ss_synchronize", I32, [P])
         _sig(lib, "ss_kv_fill_synthetic", I32, [P, P, I32, I32, I32, C.c_uint64])
         _sig(lib, "ss_set_profiling", I32, [P, I32])
+        _sig(lib, "ss_set_graphs", I32, [P, I32])
+        _sig(lib, "ss_set_tp_allreduce", I32, [P, I32])
+        _sig(lib, "ss_graph_stats", I32, [P, C.POINTER(I64), C.POINTER(I64)])
         _sig(lib, "ss_kernel_times", I32, [P, P, P, I32])
         _sig(lib, "ss_kernel_class_name", C.c_char_p, [I32])
         _sig(lib, "ss_launch_count", I64, [P])
@@ -228,6 +231,7 @@ def host_check(status: int) -> None:
 GPU_EXPORTS = [
     "ss_create", "ss_create_local_group", "ss_forward_local_group", "ss_destroy", "ss_model_config", "ss_nccl_unique_id", "ss_ipc_export", "ss_ipc_open", "ss_kv_alloc", "ss_forward_hybrid",
     "ss_batch_upload", "ss_forward_enqueue", "ss_read_outputs", "ss_batch_free", "ss_stream", "ss_synchronize",
+    "ss_set_graphs", "ss_graph_stats", "ss_set_tp_allreduce",
     "ss_kv_fill_synthetic", "ss_set_profiling", "ss_kernel_times", "ss_kernel_class_name", "ss_launch_count",
     "ss_last_error", "ss_k_gemm", "ss_k_rmsnorm", "ss_k_rope_append", "ss_k_attention", "ss_kv_layer_ptrs",
     "ss_weight_ptr",

@@ -20,6 +20,7 @@
 #include <cmath>
 #include <condition_variable>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -91,6 +92,16 @@ struct WMaps {
 struct Layer {
     bf16 *wqkv, *wo, *wgu, *wdown, *attn_norm, *mlp_norm;
     WMaps tb_qkv, tb_o, tb_gu, tb_down;
+};
+
+// Epoch space of one forward (EpiArgs::epoch_base): more than its GEMM + collective launches.
+constexpr uint32_t kEpochStride = 1u << 14;
+
+struct GraphEnt {
+    cudaGraphExec_t exec = nullptr;
+    int64_t launches[SS_K_NUM_CLASSES] = {};
+    int64_t total = 0;
+    uint64_t last_use = 0;
 };
 
 struct Prof {
@@ -186,8 +197,22 @@ struct ss_ctx {
     int decode_split = 0;           // dev override (SS_ATTN_SPLIT): fixed keys per decode split; 0 = adaptive
     int fuse_rope = 1;              // RoPE + KV append in the QKV GEMM epilogue (else the K2 kernel)
     float* sk_part = nullptr;       // stream-K GEMM partial accumulators
-    uint32_t* sk_flags = nullptr;   // stream-K ready flags
-    uint32_t sk_epoch = 0;
+    uint32_t* sk_flags = nullptr;   // stream-K ready flags: [forward GEMMs | single ss_k_gemm calls]
+    uint32_t sk_epoch = 0;          // GEMM launches so far in this forward (flag epoch offset)
+    uint32_t sk_single_epoch = 0;   // ss_k_gemm launches (immediate epochs, second flag half)
+    // Device epoch base of the forward (EpiArgs::epoch_base, IpcPeers::epoch_base): embed adds
+    // kEpochStride once per forward, every GEMM / collective launch adds its offset within the
+    // forward. Graph replays therefore use fresh epochs like eager forwards do.
+    uint32_t* d_epoch = nullptr;
+    // CUDA graphs of the forward, one per batch shape (graph_key): captured the second time
+    // a shape is seen, replayed afterwards. Invalidated when a workspace is reallocated.
+    int graphs = 1;             // ss_set_graphs / SS_GRAPHS
+    uint64_t ws_gen = 0;        // bumped by every workspace / batch-buffer / KV pool reallocation
+    uint64_t graphs_gen = 0;
+    uint64_t graph_clock = 0;
+    std::map<std::vector<int64_t>, struct GraphEnt> graph_cache;
+    std::map<std::vector<int64_t>, int> graph_seen;
+    int64_t graph_captures = 0, graph_replays = 0;
     CUtensorMap ta_xn, ta_o, ta_act, ta_xo, ta_xb;
     CUtensorMap ta32_xn, ta32_o, ta32_act, ta32_xo, ta32_xb;  // 32-row boxes (GemmPlan::ar == 32)
     bf16* xb = nullptr;   // bf16 copy of the residual stream (A of the norm-folded GEMMs)
@@ -214,6 +239,7 @@ struct ss_ctx {
     uint32_t* dev_err = nullptr;   // device error word (IpcPeers::err), checked after each forward
     uint32_t* host_err = nullptr;  // pinned copy of it
     uint32_t ipc_ar = 0;         // all-reduces so far (exchange buffer = ipc_ar & 1)
+    int ipc_algo = SS_AR_AUTO;   // ss_set_tp_allreduce / SS_TP_ALLREDUCE
 
     Tuning tu;  // dev overrides, read once at ss_create (tuning_from_env)
     bool prof = false;
@@ -355,6 +381,7 @@ ss_status ensure_workspace(ss_ctx* ctx, int T, int n_out, int part_rows) {
         CK(cudaMalloc(&ctx->ssq, size_t(cap) * (h / 32) * 4));
         if (ctx->grp) CK(cudaMalloc(&ctx->part_red, size_t(cap) * h * 2));
         ctx->T_cap = cap;
+        ++ctx->ws_gen;
         if (!make_tmap_2d(&ctx->ta_xn, ctx->xn, cap, h, 128, 64) ||
             !make_tmap_2d(&ctx->ta_o, ctx->o, cap, qd, 128, 64) ||
             !make_tmap_2d(&ctx->ta_act, ctx->act, cap, ctx->ffn_l, 128, 64) ||
@@ -380,6 +407,7 @@ ss_status ensure_workspace(ss_ctx* ctx, int T, int n_out, int part_rows) {
         }
         CK(cudaMalloc(&ctx->next_tok, size_t(cap) * 4));
         ctx->O_cap = cap;
+        ++ctx->ws_gen;
         if (!make_tmap_2d(&ctx->ta_xo, ctx->xo, cap, ctx->h, 128, 64) ||
             !make_tmap_2d(&ctx->ta32_xo, ctx->xo, cap, ctx->h, 32, 64))
             return fail(ctx, SS_CUDA_ERROR, "cuTensorMapEncodeTiled failed (logit rows)");
@@ -394,6 +422,7 @@ ss_status ensure_workspace(ss_ctx* ctx, int T, int n_out, int part_rows) {
         CK(cudaMalloc(&ctx->comb_count, size_t(cap) * 4));
         CK(cudaMemsetAsync(ctx->comb_count, 0, size_t(cap) * 4, ctx->st));
         ctx->P_cap = cap;
+        ++ctx->ws_gen;
     }
     return SS_OK;
 }
@@ -570,6 +599,7 @@ ss_status upload(ss_ctx* ctx, const ss_batch_desc* d, ss_batch* b, cudaEvent_t e
         b->dev = nullptr;
         CK(cudaMalloc(&b->dev, total * 2));
         b->dev_cap = total * 2;
+        ++ctx->ws_gen;
     }
     // previous users of the pinned staging buffer must be done before overwrite
     CK(cudaStreamSynchronize(ctx->st));
@@ -675,12 +705,13 @@ ss_status gemm(ss_ctx* ctx, int cls, const CUtensorMap& ta, WMaps& tb, int M, in
     p.tmB = *mb;
     p.part = ctx->sk_part;
     p.flags = ctx->sk_flags;
-    p.epoch = ++ctx->sk_epoch;
+    p.epoch = ++ctx->sk_epoch;  // offset within the forward; + the device base (embed)
     p.force_sk = ctx->tu.gemm_sk;
     p.force_splits = ctx->tu.gemm_splits;
     p.debug = ctx->tu.gemm_debug;
     p.ea = ea;
     p.ea.l2hint = ctx->tu.gemm_l2hint;
+    p.ea.epoch_base = ctx->d_epoch;
     return launch(ctx, cls, 1, [&] { return gemm_launch(p, ctx->st); });
 }
 
@@ -723,12 +754,22 @@ ss_status allgather_logits(ss_ctx* ctx, int n_out) {
     });
 }
 
-// IPC region layout: [exchange buffer 0 | exchange buffer 1] (T_cap x h bf16 each) |
+// IPC region layout: [exchange buffer 0 | exchange buffer 1 | two-shot share] (T_cap x h bf16 each) |
 // logits shard (T_cap x vocab_l fp32) | flags (kIpcMaxRanks u32, 256 B slot)
 size_t ipc_buf_bytes(const ss_ctx* ctx) { return (size_t(ctx->ipc_tcap) * ctx->h * 2 + 255) & ~size_t(255); }
-size_t ipc_logits_off(const ss_ctx* ctx) { return 2 * ipc_buf_bytes(ctx); }
+size_t ipc_red_off(const ss_ctx* ctx) { return 2 * ipc_buf_bytes(ctx); }
+size_t ipc_logits_off(const ss_ctx* ctx) { return 3 * ipc_buf_bytes(ctx); }
 size_t ipc_flags_off(const ss_ctx* ctx) {
     return ipc_logits_off(ctx) + ((size_t(ctx->ipc_tcap) * ctx->vocab_l * 4 + 255) & ~size_t(255));
+}
+
+// All-reduce algorithm of the IPC transport: one-shot (every rank pulls every partial:
+// (tp - 1) messages of ingress per rank, one barrier) or two-shot (reduce-scatter +
+// all-gather: 2 (tp - 1) / tp messages, two barriers). Auto: two-shot from tp = 4 and 1 MB.
+bool ipc_two_shot(const ss_ctx* ctx, int T) {
+    if (ctx->ipc_algo == SS_AR_ONESHOT) return false;
+    if (ctx->ipc_algo == SS_AR_TWOSHOT) return true;
+    return ctx->tp >= 4 && size_t(T) * ctx->h * 2 >= (size_t(1) << 20);
 }
 
 // Row-parallel projection + all-reduce + residual add over CUDA IPC: the GEMM writes this
@@ -740,6 +781,16 @@ ss_status ipc_project_allreduce(ss_ctx* ctx, int cls, const CUtensorMap& ta, WMa
     bf16* mine = reinterpret_cast<bf16*>(ctx->ipc_region + slot * ipc_buf_bytes(ctx));
     if (ss_status s = gemm(ctx, cls, ta, tb, T, ctx->h, K, mine, ctx->h, EPI_BF16)) return s;
     ++ctx->ipc_ar;
+    if (ipc_two_shot(ctx, T)) {
+        const uint32_t ep1 = ++ctx->ipc_epoch, ep2 = ++ctx->ipc_epoch;
+        if (ss_status s = launch(ctx, SS_K_ALLREDUCE, 1, [&] {
+                return ipc_reduce_scatter_launch(ctx->ipc_peers, slot, ep1, T, ctx->h, ctx->st);
+            }))
+            return s;
+        return launch(ctx, SS_K_ALLREDUCE, 1, [&] {
+            return ipc_gather_residual_launch(ctx->x, ctx->ipc_peers, ep2, ctx->xb, ctx->ssq, T, ctx->h, ctx->st);
+        });
+    }
     const uint32_t ep = ++ctx->ipc_epoch;
     return launch(ctx, SS_K_ALLREDUCE, 1, [&] {
         return ipc_allreduce_residual_launch(ctx->x, ctx->ipc_peers, slot, ep, ctx->xb, ctx->ssq, T, ctx->h, ctx->st);
@@ -756,8 +807,13 @@ ss_status enqueue_forward(ss_ctx* ctx, const ss_batch* b) {
 #define RUN(x)                 \
     if ((s = (x)) != SS_OK) \
         return s;
-    RUN(launch(ctx, SS_K_EMBED, 1,
-               [&] { return embed_launch(b->tokens, ctx->embed, ctx->x, ctx->xb, ctx->ssq, T, h, ctx->st); }));
+    // epoch offsets restart every forward; embed advances the device base (d_epoch)
+    ctx->sk_epoch = 0;
+    ctx->ipc_epoch = 0;
+    RUN(launch(ctx, SS_K_EMBED, 1, [&] {
+        return embed_launch(b->tokens, ctx->embed, ctx->x, ctx->xb, ctx->ssq, T, h, ctx->d_epoch, kEpochStride,
+                            ctx->st);
+    }));
     // RMSNorm is folded into the QKV / gate-up GEMMs: they consume the bf16 copy of
     // the residual (xb) and scale rows by rsqrt(mean(x^2) + eps) from the
     // per-chunk sums of squares (ssq) that embed / the residual-add epilogues
@@ -864,6 +920,78 @@ ss_status enqueue_forward(ss_ctx* ctx, const ss_batch* b) {
     return SS_OK;
 }
 
+void graphs_clear(ss_ctx* ctx) {
+    for (auto& kv : ctx->graph_cache) cudaGraphExecDestroy(kv.second.exec);
+    ctx->graph_cache.clear();
+    ctx->graph_seen.clear();
+}
+
+// Everything a captured forward bakes into its launches besides the (stable) workspace
+// pointers: the batch's sizes, work-list counts and buffers, and the IPC buffer parity.
+std::vector<int64_t> graph_key(const ss_ctx* ctx, const ss_batch* b) {
+    return {b->T,      b->E,         b->n_out,     b->n_items,     b->n_tc, b->tc_mode, b->n_combs, b->part_rows,
+            b->max_blocks, int64_t(reinterpret_cast<intptr_t>(b->dev)), int64_t(ctx->ipc_ar & 1u)};
+}
+
+// Enqueues one forward of b: a CUDA graph replay when this batch shape was captured, else
+// eager launches (capturing the shape's graph the second time it is seen). Graphs are off
+// for per-kernel profiling (events between launches) and for the one-device local group
+// (host barriers between ranks), and on NCCL (dlopen'ed library; not captured).
+ss_status run_forward(ss_ctx* ctx, const ss_batch* b) {
+    if (!ctx->graphs || ctx->prof || ctx->grp || ctx->comm) return enqueue_forward(ctx, b);
+    if (ctx->graphs_gen != ctx->ws_gen) {
+        graphs_clear(ctx);
+        ctx->graphs_gen = ctx->ws_gen;
+    }
+    const std::vector<int64_t> key = graph_key(ctx, b);
+    ++ctx->graph_clock;
+    auto it = ctx->graph_cache.find(key);
+    if (it != ctx->graph_cache.end()) {
+        GraphEnt& g = it->second;
+        CK(cudaGraphLaunch(g.exec, ctx->st));
+        g.last_use = ctx->graph_clock;
+        for (int k = 0; k < SS_K_NUM_CLASSES; ++k) ctx->launches[k] += g.launches[k];
+        ctx->total_launches += g.total;
+        ctx->sk_epoch = 0;
+        ctx->ipc_ar += uint32_t(2 * ctx->L * (ctx->ipc ? 1 : 0));  // the replayed all-reduces
+        ctx->last = b;
+        ++ctx->graph_replays;
+        return SS_OK;
+    }
+    if (ctx->graph_seen.size() > 4096) ctx->graph_seen.clear();
+    if (++ctx->graph_seen[key] < 2) return enqueue_forward(ctx, b);
+    if (ctx->graph_cache.size() >= 64) {  // least recently used out
+        auto lru = ctx->graph_cache.begin();
+        for (auto i = ctx->graph_cache.begin(); i != ctx->graph_cache.end(); ++i)
+            if (i->second.last_use < lru->second.last_use) lru = i;
+        cudaGraphExecDestroy(lru->second.exec);
+        ctx->graph_cache.erase(lru);
+    }
+    int64_t before[SS_K_NUM_CLASSES];
+    std::memcpy(before, ctx->launches, sizeof(before));
+    const int64_t total0 = ctx->total_launches;
+    CK(cudaStreamBeginCapture(ctx->st, cudaStreamCaptureModeThreadLocal));
+    const ss_status s = enqueue_forward(ctx, b);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ec = cudaStreamEndCapture(ctx->st, &graph);
+    if (s != SS_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return s;
+    }
+    if (ec != cudaSuccess) return fail(ctx, SS_CUDA_ERROR, std::string("graph capture: ") + cudaGetErrorString(ec));
+    GraphEnt g;
+    const cudaError_t ei = cudaGraphInstantiate(&g.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ei != cudaSuccess) return fail(ctx, SS_CUDA_ERROR, std::string("graph instantiate: ") + cudaGetErrorString(ei));
+    for (int k = 0; k < SS_K_NUM_CLASSES; ++k) g.launches[k] = ctx->launches[k] - before[k];
+    g.total = ctx->total_launches - total0;
+    g.last_use = ctx->graph_clock;
+    CK(cudaGraphLaunch(g.exec, ctx->st));  // the captured launches did not run
+    ctx->graph_cache.emplace(key, g);
+    ++ctx->graph_captures;
+    return SS_OK;
+}
+
 // After a synchronize: a collective that timed out on a missing peer left a code in the
 // device error word (see IpcPeers); report it once and clear it.
 ss_status check_dev_err(ss_ctx* ctx) {
@@ -962,6 +1090,7 @@ SS_API ss_status ss_ipc_open(ss_ctx* ctx, const void* handles) {
         }
         pe.buf[r][0] = reinterpret_cast<const bf16*>(base);
         pe.buf[r][1] = reinterpret_cast<const bf16*>(base + ipc_buf_bytes(ctx));
+        pe.red[r] = reinterpret_cast<bf16*>(base + ipc_red_off(ctx));
         pe.logits[r] = reinterpret_cast<const float*>(base + ipc_logits_off(ctx));
         pe.flags[r] = reinterpret_cast<uint32_t*>(base + ipc_flags_off(ctx));
     }
@@ -973,7 +1102,9 @@ SS_API ss_status ss_ipc_open(ss_ctx* ctx, const void* handles) {
     *ctx->host_err = 0;
     pe.err = ctx->dev_err;
     pe.timeout_ns = 10ull * 1000 * 1000 * 1000;  // a peer missing for 10 s is a failed rank
+    pe.epoch_base = ctx->d_epoch;
     ctx->ipc_peers = pe;
+    ++ctx->ws_gen;  // captured graphs predate the transport
     ctx->ipc = 1;
     return SS_OK;
 }
@@ -1028,14 +1159,17 @@ static ss_status create_impl(const ss_model_cfg* cfg, int32_t tp_rank, int32_t t
     if (ctx->fused_combine) ctx->attn_tc = 0;  // the in-kernel split merge exists on the mma.sync path only
     if (const char* f = getenv("SS_KV_PF_MB")) ctx->kv_pf_mb = atoi(f);  // dev tuning
     if (const char* f = getenv("SS_FUSE_ROPE")) ctx->fuse_rope = atoi(f);
+    if (const char* f = getenv("SS_GRAPHS")) ctx->graphs = atoi(f);  // dev A/B
+    if (const char* f = getenv("SS_TP_ALLREDUCE")) ctx->ipc_algo = atoi(f);
     // every allocation below lands on `device`, whatever the calling thread's current device
     if (cudaSetDevice(device) != cudaSuccess) {
         delete ctx;
         return fail(nullptr, SS_CUDA_ERROR, "cudaSetDevice");
     }
     if (cudaMalloc(&ctx->sk_part, gemm_part_floats(ctx->num_sms) * 4) != cudaSuccess ||
-        cudaMalloc(&ctx->sk_flags, gemm_flag_words(ctx->num_sms) * 4) != cudaSuccess ||
-        cudaMemset(ctx->sk_flags, 0, gemm_flag_words(ctx->num_sms) * 4) != cudaSuccess) {
+        cudaMalloc(&ctx->sk_flags, 2 * gemm_flag_words(ctx->num_sms) * 4) != cudaSuccess ||
+        cudaMemset(ctx->sk_flags, 0, 2 * gemm_flag_words(ctx->num_sms) * 4) != cudaSuccess ||
+        cudaMalloc(&ctx->d_epoch, 4) != cudaSuccess || cudaMemset(ctx->d_epoch, 0, 4) != cudaSuccess) {
         std::string m = "stream-K workspace allocation";
         ss_destroy(ctx);
         return fail(nullptr, SS_OUT_OF_MEMORY, m);
@@ -1215,6 +1349,8 @@ SS_API void ss_destroy(ss_ctx* ctx) {
     cudaFree(ctx->rope);
     cudaFree(ctx->sk_part);
     cudaFree(ctx->sk_flags);
+    cudaFree(ctx->d_epoch);
+    graphs_clear(ctx);
     cudaFree(ctx->kc);
     cudaFree(ctx->vc);
     for (void* q : {(void*)ctx->x, (void*)ctx->xn, (void*)ctx->qkv, (void*)ctx->q, (void*)ctx->o, (void*)ctx->act,
@@ -1267,6 +1403,7 @@ SS_API ss_status ss_kv_alloc(ss_ctx* ctx, int64_t num_blocks, int32_t block_size
     if (!attention_tmaps(&ctx->tm_k, &ctx->tm_v, ctx->kc, ctx->vc, num_blocks * ctx->nkv_l * block_size * ctx->L, ctx->hd))
         return fail(ctx, SS_CUDA_ERROR, "cuTensorMapEncodeTiled failed (KV pool)");
     ctx->nblocks = num_blocks;
+    ++ctx->ws_gen;
     return SS_OK;
 }
 
@@ -1299,7 +1436,7 @@ SS_API ss_status ss_forward_enqueue(ss_ctx* ctx, const ss_batch* b) {
     if (!ctx || !b) return SS_INVALID_ARG;
     DevGuard dg(ctx->device);
     if (ss_status s = ensure_workspace(ctx, b->T, std::max(b->n_out, 1), b->part_rows)) return s;
-    return enqueue_forward(ctx, b);
+    return run_forward(ctx, b);
 }
 
 SS_API ss_status ss_read_outputs(ss_ctx* ctx, const ss_batch* b, float* logits, int32_t* next) {
@@ -1313,7 +1450,7 @@ SS_API ss_status ss_forward_hybrid(ss_ctx* ctx, const ss_batch_desc* desc, float
     if (!ctx) return SS_INVALID_ARG;
     DevGuard dg(ctx->device);
     if (ss_status s = upload(ctx, desc, &ctx->scratch, ctx->ev0)) return s;
-    if (ss_status s = enqueue_forward(ctx, &ctx->scratch)) return s;
+    if (ss_status s = run_forward(ctx, &ctx->scratch)) return s;
     CK(cudaEventRecord(ctx->ev1, ctx->st));
     if (ss_status s = read_outputs(ctx, &ctx->scratch, logits, next)) return s;
     CK(cudaEventSynchronize(ctx->ev1));
@@ -1346,6 +1483,31 @@ SS_API ss_status ss_kv_fill_synthetic(ss_ctx* ctx, const int32_t* block_table, i
     cudaError_t e2 = cudaStreamSynchronize(ctx->st);
     cudaFree(d);
     if (e != cudaSuccess || e2 != cudaSuccess) return fail(ctx, SS_CUDA_ERROR, "synthetic KV fill failed");
+    return SS_OK;
+}
+
+SS_API ss_status ss_set_graphs(ss_ctx* ctx, int32_t enabled) {
+    if (!ctx) return SS_INVALID_ARG;
+    DevGuard dg(ctx->device);
+    CK(cudaStreamSynchronize(ctx->st));
+    ctx->graphs = enabled != 0;
+    if (!ctx->graphs) graphs_clear(ctx);
+    return SS_OK;
+}
+
+SS_API ss_status ss_set_tp_allreduce(ss_ctx* ctx, int32_t algo) {
+    if (!ctx || algo < SS_AR_AUTO || algo > SS_AR_TWOSHOT) return fail(ctx, SS_INVALID_ARG, "bad all-reduce algorithm");
+    DevGuard dg(ctx->device);
+    CK(cudaStreamSynchronize(ctx->st));
+    ctx->ipc_algo = algo;
+    graphs_clear(ctx);
+    return SS_OK;
+}
+
+SS_API ss_status ss_graph_stats(ss_ctx* ctx, int64_t* captures, int64_t* replays) {
+    if (!ctx) return SS_INVALID_ARG;
+    if (captures) *captures = ctx->graph_captures;
+    if (replays) *replays = ctx->graph_replays;
     return SS_OK;
 }
 
@@ -1384,8 +1546,8 @@ SS_API ss_status ss_k_gemm(ss_ctx* ctx, const void* A, const void* B, void* D, i
     if (!gemm_prepare(p, A, uint64_t(M), B, M, N, K, D, ldo, epi, ctx->num_sms, ctx->tu))
         return fail(ctx, SS_INVALID_ARG, "gemm shape unsupported (N%32, K%8, SwiGLU N%64) or tensor map failed");
     p.part = ctx->sk_part;
-    p.flags = ctx->sk_flags;
-    p.epoch = ++ctx->sk_epoch;
+    p.flags = ctx->sk_flags + gemm_flag_words(ctx->num_sms);  // apart from the forward's flags
+    p.epoch = ++ctx->sk_single_epoch;
     return launch(ctx, SS_K_GEMM_QKV, 1, [&] { return gemm_launch(p, ctx->st); });
 }
 

@@ -18,9 +18,12 @@ __device__ __forceinline__ float warp_sum(float v) {
 }
 
 __global__ void embed_kernel(const int32_t* __restrict__ tokens, const __nv_bfloat16* __restrict__ table,
-                             float* __restrict__ x, __nv_bfloat16* __restrict__ xb, float* __restrict__ ssq, int h) {
+                             float* __restrict__ x, __nv_bfloat16* __restrict__ xb, float* __restrict__ ssq, int h,
+                             uint32_t* __restrict__ epoch_ctr, uint32_t epoch_stride) {
     pdl_launch_dependents();
     pdl_wait();
+    // previous forward complete (PDL completion chain): its epochs are no longer read
+    if (epoch_ctr && blockIdx.x == 0 && threadIdx.x == 0) *epoch_ctr += epoch_stride;
     const int t = blockIdx.x;
     const uint4* src = reinterpret_cast<const uint4*>(table + size_t(tokens[t]) * h);
     float4* dst = reinterpret_cast<float4*>(x + size_t(t) * h);
@@ -161,6 +164,11 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
     return t;
 }
 
+// The forward's device epoch base (written by embed, read after pdl_wait).
+__device__ __forceinline__ uint32_t ipc_epoch_base(const IpcPeers& pe) {
+    return pe.epoch_base ? *reinterpret_cast<const volatile uint32_t*>(pe.epoch_base) : 0u;
+}
+
 // Returns false (CTA-uniform) when a peer missed the collective: the error word is set
 // and the caller skips its work, so a stalled rank surfaces as a status, not a trap.
 __device__ __forceinline__ bool ipc_barrier(const IpcPeers& pe, uint32_t epoch) {
@@ -197,7 +205,7 @@ __global__ void ipc_allreduce_residual_kernel(float* __restrict__ x, const IpcPe
                                               int h) {
     pdl_launch_dependents();
     pdl_wait();  // this rank's partial is complete
-    if (!ipc_barrier(pe, epoch)) return;
+    if (!ipc_barrier(pe, epoch + ipc_epoch_base(pe))) return;
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;  // multiple of 32
     for (int64_t base = blockIdx.x * int64_t(blockDim.x); base < n8; base += stride) {
         const int64_t i = base + threadIdx.x;
@@ -230,12 +238,68 @@ __global__ void ipc_allreduce_residual_kernel(float* __restrict__ x, const IpcPe
     }
 }
 
+// Two-shot phase 1: sum this rank's share [lo, hi) of the uint4 (8 x bf16) units over every
+// rank's partial in rank order (fp32), store it bf16 into this rank's red buffer.
+__device__ __forceinline__ int64_t ipc_share(int64_t n8, int n) { return (n8 + n - 1) / n; }
+
+__global__ void ipc_reduce_scatter_kernel(const IpcPeers pe, int slot, uint32_t epoch, int64_t n8) {
+    pdl_launch_dependents();
+    pdl_wait();  // this rank's partial is complete
+    if (!ipc_barrier(pe, epoch + ipc_epoch_base(pe))) return;
+    const int64_t share = ipc_share(n8, pe.n), lo = share * pe.rank, hi = min(n8, lo + share);
+    uint4* dst = reinterpret_cast<uint4*>(pe.red[pe.rank]);
+    for (int64_t i = lo + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < hi; i += int64_t(gridDim.x) * blockDim.x) {
+        float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+        for (int r = 0; r < pe.n; ++r) {
+            const uint4 v = __ldcv(reinterpret_cast<const uint4*>(pe.buf[r][slot]) + i);
+            a.x += bf16_lo(v.x); a.y += bf16_hi(v.x); a.z += bf16_lo(v.y); a.w += bf16_hi(v.y);
+            b.x += bf16_lo(v.z); b.y += bf16_hi(v.z); b.z += bf16_lo(v.w); b.w += bf16_hi(v.w);
+        }
+        dst[i] = make_uint4(pack_bf16(a.x, a.y), pack_bf16(a.z, a.w), pack_bf16(b.x, b.y), pack_bf16(b.z, b.w));
+    }
+}
+
+// Two-shot phase 2: every rank's reduced share -> residual add (+ bf16 copy, sums of squares).
+__global__ void ipc_gather_residual_kernel(float* __restrict__ x, const IpcPeers pe, uint32_t epoch,
+                                           __nv_bfloat16* __restrict__ xb, float* __restrict__ ssq, int64_t n8,
+                                           int h) {
+    pdl_launch_dependents();
+    pdl_wait();  // this rank's share is stored
+    if (!ipc_barrier(pe, epoch + ipc_epoch_base(pe))) return;
+    const int64_t share = ipc_share(n8, pe.n);
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;  // multiple of 32
+    for (int64_t base = blockIdx.x * int64_t(blockDim.x); base < n8; base += stride) {
+        const int64_t i = base + threadIdx.x;
+        const bool act = i < n8;
+        float ss = 0.f;
+        if (act) {
+            const uint4 v = __ldcv(reinterpret_cast<const uint4*>(pe.red[i / share]) + i);
+            float4* d = reinterpret_cast<float4*>(x) + 2 * i;
+            float4 xa = d[0], xc = d[1];
+            xa.x += bf16_lo(v.x); xa.y += bf16_hi(v.x); xa.z += bf16_lo(v.y); xa.w += bf16_hi(v.y);
+            xc.x += bf16_lo(v.z); xc.y += bf16_hi(v.z); xc.z += bf16_lo(v.w); xc.w += bf16_hi(v.w);
+            d[0] = xa;
+            d[1] = xc;
+            reinterpret_cast<uint4*>(xb)[i] =
+                make_uint4(pack_bf16(xa.x, xa.y), pack_bf16(xa.z, xa.w), pack_bf16(xc.x, xc.y), pack_bf16(xc.z, xc.w));
+            ss = xa.x * xa.x + xa.y * xa.y + xa.z * xa.z + xa.w * xa.w + xc.x * xc.x + xc.y * xc.y + xc.z * xc.z +
+                 xc.w * xc.w;
+        }
+        ss += __shfl_xor_sync(0xffffffffu, ss, 1);
+        ss += __shfl_xor_sync(0xffffffffu, ss, 2);
+        if (act && (i & 3) == 0) {  // 4 threads = one 32-column chunk of one row
+            const int64_t row = i / (h / 8), g = i % (h / 8);
+            ssq[row * (h / 32) + g / 4] = ss;
+        }
+    }
+}
+
 // Vocab all-gather of the LM-head shards: logits[row][r * vl + c] = rank r's shard.
 __global__ void ipc_gather_logits_kernel(const IpcPeers pe, uint32_t epoch, float* __restrict__ out, int rows,
                                          int vl) {
     pdl_launch_dependents();
     pdl_wait();
-    if (!ipc_barrier(pe, epoch)) return;
+    if (!ipc_barrier(pe, epoch + ipc_epoch_base(pe))) return;
     const int64_t n = int64_t(pe.n) * rows * vl;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
         const int64_t r = i / (int64_t(rows) * vl), rem = i % (int64_t(rows) * vl), row = rem / vl, c = rem % vl;
@@ -420,8 +484,10 @@ int grid_for(int64_t n, int threads) {
 }  // namespace
 
 cudaError_t embed_launch(const int32_t* tokens, const __nv_bfloat16* table, float* x, __nv_bfloat16* xb, float* ssq,
-                         int T, int h, cudaStream_t st) {
-    return T > 0 ? launch_pdl(embed_kernel, dim3(T), dim3(256), 0, st, 1, tokens, table, x, xb, ssq, h) : cudaSuccess;
+                         int T, int h, uint32_t* epoch_ctr, uint32_t epoch_stride, cudaStream_t st) {
+    return T > 0 ? launch_pdl(embed_kernel, dim3(T), dim3(256), 0, st, 1, tokens, table, x, xb, ssq, h, epoch_ctr,
+                              epoch_stride)
+                 : cudaSuccess;
 }
 
 cudaError_t rmsnorm_launch(const float* x, const __nv_bfloat16* w, __nv_bfloat16* out, const int32_t* rows, int M,
@@ -453,6 +519,22 @@ cudaError_t ipc_allreduce_residual_launch(float* x, const IpcPeers& pe, int slot
     const int grid = int(std::min<int64_t>(grid_for(n8, 256), 4 * 148));
     return n8 > 0 ? launch_pdl(ipc_allreduce_residual_kernel, dim3(grid), dim3(256), 0, st, 1, x, pe, slot, epoch, xb,
                                ssq, n8, h)
+                  : cudaSuccess;
+}
+
+cudaError_t ipc_reduce_scatter_launch(const IpcPeers& pe, int slot, uint32_t epoch, int T, int h, cudaStream_t st) {
+    const int64_t n8 = int64_t(T) * h / 8;
+    const int grid = int(std::min<int64_t>(grid_for((n8 + pe.n - 1) / pe.n, 256), 4 * 148));
+    return n8 > 0 ? launch_pdl(ipc_reduce_scatter_kernel, dim3(grid), dim3(256), 0, st, 1, pe, slot, epoch, n8)
+                  : cudaSuccess;
+}
+
+cudaError_t ipc_gather_residual_launch(float* x, const IpcPeers& pe, uint32_t epoch, __nv_bfloat16* xb, float* ssq,
+                                       int T, int h, cudaStream_t st) {
+    const int64_t n8 = int64_t(T) * h / 8;
+    const int grid = int(std::min<int64_t>(grid_for(n8, 256), 4 * 148));
+    return n8 > 0 ? launch_pdl(ipc_gather_residual_kernel, dim3(grid), dim3(256), 0, st, 1, x, pe, epoch, xb, ssq,
+                               n8, h)
                   : cudaSuccess;
 }
 

@@ -528,6 +528,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         int acc = 0;
         uint32_t acc_ph = 0, eph = 0;
         SegIter sit(sk_mode, gid, G, num_kb, num_tiles, rg, sk_slices, P);
+        // flag epoch of this launch (after pdl_wait: the forward's base is final)
+        if (ea.epoch_base) epoch += *reinterpret_cast<const volatile uint32_t*>(ea.epoch_base);
         for (Seg sg; sit.next(sg);) {
             const int t = sg.t, kb0 = sg.kb0, kb1 = sg.kb1;
             const int m0 = row0 + (t % num_mt) * Cfg::TILE_M, n0 = (t / num_mt) * BN;

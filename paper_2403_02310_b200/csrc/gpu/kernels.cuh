@@ -43,6 +43,10 @@ struct EpiArgs {
     const int32_t* pf_bt = nullptr;
     const int32_t* pf_ctx_len = nullptr;
     int l2hint = 0;  // operand L2 priority bits: 1 A evict-last, 2 B evict-first
+    // Stream-K flag epochs are GemmPlan::epoch + *epoch_base when set: the forward's epoch
+    // base lives in device memory (advanced by the forward's first kernel, embed), so a
+    // CUDA graph of the forward replays with fresh epochs. Null: GemmPlan::epoch as is.
+    const uint32_t* epoch_base = nullptr;
 };
 
 // Developer tuning overrides (the SS_* environment variables the scripts/ A/B sweeps set),
@@ -166,8 +170,10 @@ cudaError_t attention_combine_launch(const AttnParams& p, cudaStream_t st);
 // ------------------------------------------------------------------ K2/K4 elementwise
 // x = embed[tokens] (fp32) plus the bf16 copy and per-chunk sums of squares the
 // first (norm-folded) QKV GEMM consumes.
+// epoch_ctr (nullable): the forward's device epoch base, advanced by epoch_stride once the
+// previous forward has completed (EpiArgs::epoch_base)
 cudaError_t embed_launch(const int32_t* tokens, const __nv_bfloat16* table, float* x, __nv_bfloat16* xb, float* ssq,
-                         int T, int h, cudaStream_t st);
+                         int T, int h, uint32_t* epoch_ctr, uint32_t epoch_stride, cudaStream_t st);
 cudaError_t rmsnorm_launch(const float* x, const __nv_bfloat16* w, __nv_bfloat16* out, const int32_t* rows, int M,
                            int h, float eps, cudaStream_t st);
 // RoPE (rotate-half) of q and k heads + paged KV append of k and v.
@@ -181,6 +187,9 @@ cudaError_t rope_append_launch(const __nv_bfloat16* qkv, __nv_bfloat16* q_out, c
 constexpr int kIpcMaxRanks = 8;
 struct IpcPeers {
     const __nv_bfloat16* buf[kIpcMaxRanks][2];
+    // two-shot all-reduce: rank r's reduced share of the sum (bf16 [T_cap][h], only the
+    // elements rank r owns are written), read by every rank in the gather phase
+    __nv_bfloat16* red[kIpcMaxRanks];
     const float* logits[kIpcMaxRanks];
     uint32_t* flags[kIpcMaxRanks];
     int n, rank;
@@ -189,10 +198,21 @@ struct IpcPeers {
     // error word, read by the host after the forward) and skip the collective's work.
     uint32_t* err;
     uint64_t timeout_ns;
+    // collective epochs are the launch's epoch + *epoch_base (see EpiArgs::epoch_base)
+    const uint32_t* epoch_base;
 };
 constexpr uint32_t kDevErrPeerTimeout = 1;
 cudaError_t ipc_allreduce_residual_launch(float* x, const IpcPeers& pe, int slot, uint32_t epoch,
                                           __nv_bfloat16* xb, float* ssq, int T, int h, cudaStream_t st);
+// Two-shot all-reduce (reduce-scatter + all-gather over peer memory), for tp >= 4 where
+// the one-shot pull reads (tp - 1) full messages per rank: phase 1 sums this rank's
+// 1/tp share of the elements over every rank's partial (fixed rank order, fp32) into its
+// red buffer; phase 2 reads every rank's share and adds it to the residual (+ xb / ssq).
+// Per-rank ingress 2 (tp - 1) / tp messages, the ring's figure. Each phase opens with a
+// flag barrier (its own epoch).
+cudaError_t ipc_reduce_scatter_launch(const IpcPeers& pe, int slot, uint32_t epoch, int T, int h, cudaStream_t st);
+cudaError_t ipc_gather_residual_launch(float* x, const IpcPeers& pe, uint32_t epoch, __nv_bfloat16* xb, float* ssq,
+                                       int T, int h, cudaStream_t st);
 cudaError_t ipc_gather_logits_launch(const IpcPeers& pe, uint32_t epoch, float* out, int rows, int vl,
                                      cudaStream_t st);
 // x += part (TP all-reduce result), also refreshing xb / ssq for the next norm-folded GEMM.

@@ -206,6 +206,22 @@ class HybridForward:
 
         return torch.cuda.ExternalStream(self.stream_ptr)
 
+    # ---- TP all-reduce algorithm of the IPC transport (ss_set_tp_allreduce)
+    ALLREDUCE = {"auto": 0, "oneshot": 1, "twoshot": 2}
+
+    def set_tp_allreduce(self, algo: str):
+        self._check(gpu_lib().ss_set_tp_allreduce(self._h, self.ALLREDUCE[algo]))
+
+    # ---- CUDA graphs of the forward (one per batch shape; ss_set_graphs)
+    def set_graphs(self, on: bool):
+        self._check(gpu_lib().ss_set_graphs(self._h, int(on)))
+
+    def graph_stats(self) -> Tuple[int, int]:
+        """(graphs captured, graph replays) since creation."""
+        cap, rep = C.c_int64(), C.c_int64()
+        self._check(gpu_lib().ss_graph_stats(self._h, C.byref(cap), C.byref(rep)))
+        return cap.value, rep.value
+
     # ---- profiling
     def set_profiling(self, on: bool):
         self._check(gpu_lib().ss_set_profiling(self._h, int(on)))
