@@ -117,6 +117,10 @@ def algorithmic_work(shape, desc_arrays, tp):
         "attention_flops": 4 * hd * nq * pairs,
         "lm_head": 2.0 * n_out * shape.vocab / tp * h,
     }
+    # the fused projection chain (one launch per layer at TP = 1): O + gate/up + down of the
+    # layer and the next layer's QKV (the last layer's chain has no QKV); per step
+    per_layer["gemm_chain_step"] = (L * (per_layer["gemm_o"] + per_layer["gemm_gate_up"] + per_layer["gemm_down"])
+                                    + (L - 1) * per_layer["gemm_qkv"])
     return {"bytes": bytes_w + bytes_kv_read + bytes_kv_write, "flops": flops, "per_layer": per_layer,
             "T": T, "n_out": n_out}
 
@@ -254,6 +258,9 @@ def run_ours(args):
         avg = ms / args.steps / L if per_layer_cls else ms / n
         if k in ("gemm_qkv", "gemm_o", "gemm_gate_up", "gemm_down", "lm_head"):
             ent["tflops"] = pl[k] / (avg * 1e-3) / 1e12
+        if k == "gemm_chain":  # flops of every chain launch of the step over their total time
+            ent["tflops"] = pl["gemm_chain_step"] / (ms / args.steps * 1e-3) / 1e12
+            ent["flops_per_launch"] = pl["gemm_chain_step"] / max(1.0, n / args.steps)
         if k == "attention":
             ent["gbs"] = pl["attention_bytes"] / (avg * 1e-3) / 1e9
         kernels[k] = ent

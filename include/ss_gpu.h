@@ -165,7 +165,8 @@ enum {
     SS_K_ALLREDUCE = 9,
     SS_K_LMHEAD = 10,
     SS_K_ARGMAX = 11,
-    SS_K_NUM_CLASSES = 12
+    SS_K_GEMM_CHAIN = 12, /* fused O -> gate/up -> down -> next QKV launch (TP = 1) */
+    SS_K_NUM_CLASSES = 13
 };
 ss_status ss_set_profiling(ss_ctx* ctx, int32_t enabled);
 /* ms_out/launches_out: SS_K_NUM_CLASSES entries accumulated since reset. */

@@ -217,6 +217,12 @@ struct ss_ctx {
     CUtensorMap ta32_xn, ta32_o, ta32_act, ta32_xo, ta32_xb;  // 32-row boxes (GemmPlan::ar == 32)
     bf16* xb = nullptr;   // bf16 copy of the residual stream (A of the norm-folded GEMMs)
     float* ssq = nullptr;  // per (row, 32-column chunk) sums of squares of the residual
+    // fused projection chain (gemm_chain_launch; TP = 1, T > 128): per-phase tile flags /
+    // counters and K-split partials, sized for T_cap
+    uint32_t* chain_flags = nullptr;
+    float* chain_part = nullptr;
+    size_t chain_flag_cap = 0, chain_part_cap = 0;
+    unsigned long long* chain_trace = nullptr;  // SS_CHAIN_TRACE: [L][kChainTraceItems][8] timeline
     CUtensorMap tm_k, tm_v;  // 2D TMA views of the paged K/V pools
 
     uint8_t* pinned = nullptr;
@@ -354,6 +360,42 @@ bool bmaps(WMaps& m, const bf16* w, int64_t rows, int64_t cols) {
     return m.get(128) != nullptr;  // validates the encode path once up front
 }
 
+// The fused projection chain of a layer (TP = 1, more than one 128-row tile of tokens):
+// O, gate/up, down, and the next layer's QKV as one persistent launch (gemm.cu).
+bool chain_enabled(const ss_ctx* ctx, int T) {
+    return ctx->tu.chain && ctx->tp == 1 && !ctx->grp && T > 128 && ctx->h % 256 == 0 && ctx->fuse_rope;
+}
+struct ChainDims {
+    int n = 4, num_mt = 0;
+    int N[4], K[4], S[4];
+};
+// K splits: about 64 k-blocks (a K = 4096 tile) per split, so every phase's tiles are
+// comparable work units (down at K = 14336: 4 splits); SS_CHAIN_S overrides.
+ChainDims chain_dims(const ss_ctx* ctx, int T) {
+    ChainDims d;
+    d.num_mt = (T + 255) / 256;
+    const int qd = ctx->nq_l * ctx->hd, qkvN = (ctx->nq_l + 2 * ctx->nkv_l) * ctx->hd;
+    const int N[4] = {ctx->h, 2 * ctx->ffn_l, ctx->h, qkvN}, K[4] = {qd, ctx->h, ctx->ffn_l, ctx->h};
+    for (int p = 0; p < 4; ++p) {
+        d.N[p] = N[p];
+        d.K[p] = K[p];
+        const int nkb = (K[p] + 63) / 64;
+        d.S[p] = ctx->tu.chain_splits[p] > 0 ? ctx->tu.chain_splits[p] : std::max(1, (nkb + 32) / 64);
+    }
+    return d;
+}
+size_t chain_flag_words(const ChainDims& d) {
+    size_t w = 0;
+    for (int p = 0; p < d.n; ++p) w += size_t(d.num_mt) * ((d.N[p] + 255) / 256) * 18;
+    return w;
+}
+size_t chain_part_floats(const ChainDims& d) {
+    size_t f = 0;
+    for (int p = 0; p < d.n; ++p)
+        if (d.S[p] > 1) f += size_t(d.num_mt) * ((d.N[p] + 255) / 256) * d.S[p] * 65536;
+    return f;
+}
+
 ss_status ensure_workspace(ss_ctx* ctx, int T, int n_out, int part_rows) {
     if (T > ctx->T_cap) {
         const int cap = std::max(T, std::max(2 * ctx->T_cap, 64));
@@ -423,6 +465,25 @@ ss_status ensure_workspace(ss_ctx* ctx, int T, int n_out, int part_rows) {
         CK(cudaMemsetAsync(ctx->comb_count, 0, size_t(cap) * 4, ctx->st));
         ctx->P_cap = cap;
         ++ctx->ws_gen;
+    }
+    if (chain_enabled(ctx, T)) {  // sized for T_cap: flags must start zeroed (counters self-reset)
+        const ChainDims d = chain_dims(ctx, ctx->T_cap);
+        const size_t fw = chain_flag_words(d), pf = chain_part_floats(d);
+        if (fw > ctx->chain_flag_cap) {
+            cudaFree(ctx->chain_flags);
+            ctx->chain_flags = nullptr;
+            CK(cudaMalloc(&ctx->chain_flags, fw * 4));
+            CK(cudaMemsetAsync(ctx->chain_flags, 0, fw * 4, ctx->st));
+            ctx->chain_flag_cap = fw;
+            ++ctx->ws_gen;
+        }
+        if (pf > ctx->chain_part_cap) {
+            cudaFree(ctx->chain_part);
+            ctx->chain_part = nullptr;
+            CK(cudaMalloc(&ctx->chain_part, pf * 4));
+            ctx->chain_part_cap = pf;
+            ++ctx->ws_gen;
+        }
     }
     return SS_OK;
 }
@@ -709,6 +770,7 @@ ss_status gemm(ss_ctx* ctx, int cls, const CUtensorMap& ta, WMaps& tb, int M, in
     p.force_sk = ctx->tu.gemm_sk;
     p.force_splits = ctx->tu.gemm_splits;
     p.debug = ctx->tu.gemm_debug;
+    p.max_groups = ctx->tu.gemm_max_groups;
     p.ea = ea;
     p.ea.l2hint = ctx->tu.gemm_l2hint;
     p.ea.epoch_base = ctx->d_epoch;
@@ -797,6 +859,105 @@ ss_status ipc_project_allreduce(ss_ctx* ctx, int cls, const CUtensorMap& ta, WMa
     });
 }
 
+// Epilogue operands of layer l's QKV projection: the folded RMSNorm, RoPE of q/k, q to the
+// attention layout, k/v appended into the paged pool at slot[t].
+EpiArgs qkv_args(const ss_ctx* ctx, const ss_batch* b, int l) {
+    EpiArgs ea;
+    ea.ssq_in = ctx->ssq;
+    ea.ssq_in_n = ctx->h / 32;
+    ea.inv_dim = 1.f / float(ctx->h);
+    ea.eps = ctx->cfg.rms_eps;
+    ea.pos = b->pos;
+    ea.slot = b->slot;
+    ea.rope = ctx->rope;
+    ea.q_out = ctx->q;
+    ea.kc = ctx->kc + size_t(l) * ctx->layer_stride;
+    ea.vc = ctx->vc + size_t(l) * ctx->layer_stride;
+    ea.nq = ctx->nq_l;
+    ea.nkv = ctx->nkv_l;
+    ea.hd = ctx->hd;
+    ea.bs = ctx->bs;
+    return ea;
+}
+
+constexpr int kChainTraceItems = 4096;
+
+// Layer l's O -> gate/up -> down projections and layer l + 1's QKV as one fused launch.
+ss_status chain_launch(ss_ctx* ctx, const ss_batch* b, int l) {
+    const int T = b->T, h = ctx->h;
+    const ChainDims d = chain_dims(ctx, T);
+    Layer& W = ctx->layers[size_t(l)];
+    const int np = l + 1 < ctx->L ? 4 : 3;
+    ChainPlan p;
+    p.n_phases = np;
+    p.M = T;
+    p.num_mt = d.num_mt;
+    p.num_sms = ctx->num_sms;
+    p.epoch = ++ctx->sk_epoch;  // offset within the forward; + the device base (embed)
+    p.epoch_base = ctx->d_epoch;
+    p.debug = ctx->tu.chain_debug;
+    EpiArgs norm_in;
+    norm_in.ssq_in = ctx->ssq;
+    norm_in.ssq_in_n = h / 32;
+    norm_in.inv_dim = 1.f / float(h);
+    norm_in.eps = ctx->cfg.rms_eps;
+    EpiArgs res_out;
+    res_out.xb_out = ctx->xb;
+    res_out.ssq_out = ctx->ssq;
+    struct Src {
+        const CUtensorMap* a;
+        WMaps* b;
+        int epi, dep, res_dep, out_cols;
+        void* out;
+        int ldo;
+        EpiArgs ea;
+    };
+    const Src src[4] = {
+        {&ctx->ta_o, &W.tb_o, EPI_RESADD, -1, -1, 256, ctx->x, h, res_out},
+        {&ctx->ta_xb, &W.tb_gu, EPI_SWIGLU, 0, -1, 128, ctx->act, ctx->ffn_l, norm_in},
+        {&ctx->ta_act, &W.tb_down, EPI_RESADD, 1, 0, 256, ctx->x, h, res_out},
+        {&ctx->ta_xb, np == 4 ? &ctx->layers[size_t(l) + 1].tb_qkv : nullptr, EPI_QKV, 2, -1, 256, nullptr,
+         d.N[3], np == 4 ? qkv_args(ctx, b, l + 1) : EpiArgs()},
+    };
+    uint32_t* fl = ctx->chain_flags;
+    float* pt = ctx->chain_part;
+    for (int i = 0; i < np; ++i) {
+        ChainPhase& ph = p.ph[i];
+        const CUtensorMap* mb = src[i].b->get(128);
+        if (!mb) return fail(ctx, SS_CUDA_ERROR, "cuTensorMapEncodeTiled failed (weight tile map)");
+        p.tmA[i] = *src[i].a;
+        p.tmB[i] = *mb;
+        ph.N = d.N[i];
+        ph.K = d.K[i];
+        ph.epi = src[i].epi;
+        ph.splits = d.S[i];
+        ph.dep = src[i].dep;
+        ph.res_dep = src[i].res_dep;
+        ph.out_cols = src[i].out_cols;
+        ph.out = src[i].out;
+        ph.ldo = src[i].ldo;
+        ph.ea = src[i].ea;
+        const size_t tiles = size_t(d.num_mt) * ((d.N[i] + 255) / 256);
+        ph.ready = fl;
+        ph.rcnt = fl + tiles;
+        ph.pcnt = fl + 2 * tiles;
+        fl += 18 * tiles;
+        if (d.S[i] > 1) {
+            ph.part = pt;
+            pt += tiles * d.S[i] * 65536;
+        }
+    }
+    gemm_chain_finalize(p);
+    if (ctx->tu.chain_trace && p.total_items <= kChainTraceItems) {
+        if (!ctx->chain_trace) {
+            CK(cudaMalloc(&ctx->chain_trace, size_t(ctx->L) * kChainTraceItems * 16 * 8));
+            CK(cudaMemset(ctx->chain_trace, 0, size_t(ctx->L) * kChainTraceItems * 16 * 8));
+        }
+        p.trace = ctx->chain_trace + size_t(l) * kChainTraceItems * 16;
+    }
+    return launch(ctx, SS_K_GEMM_CHAIN, 1, [&] { return gemm_chain_launch(p, ctx->st); });
+}
+
 ss_status enqueue_forward(ss_ctx* ctx, const ss_batch* b) {
     if (ctx->tp > 1 && !ctx->grp && !ctx->comm && !ctx->ipc)
         return fail(ctx, SS_INVALID_ARG, "tp > 1 needs an NCCL id at ss_create or the IPC transport (ss_ipc_open)");
@@ -826,6 +987,7 @@ ss_status enqueue_forward(ss_ctx* ctx, const ss_batch* b) {
     EpiArgs res_out;
     res_out.xb_out = ctx->xb;
     res_out.ssq_out = ctx->ssq;
+    const bool chain = chain_enabled(ctx, T);
     for (int l = 0; l < ctx->L; ++l) {
         Layer& W = ctx->layers[size_t(l)];
         EpiArgs qkv_ea = norm_in;  // + RoPE and the paged KV append (K2) in the epilogue
@@ -851,7 +1013,9 @@ ss_status enqueue_forward(ss_ctx* ctx, const ss_batch* b) {
             qkv_ea.pf_ctx_len = b->ctx_len;
             if (qkv_ea.pf_pages == 0) qkv_ea.pf_n = 0;
         }
-        if (ctx->fuse_rope) {
+        if (chain && l > 0) {
+            // this layer's QKV ran in the previous layer's chain launch
+        } else if (ctx->fuse_rope) {
             RUN(gemm(ctx, SS_K_GEMM_QKV, ctx->ta_xb, W.tb_qkv, T, qkvN, h, nullptr, qkvN, EPI_QKV, qkv_ea));
         } else {
             RUN(gemm(ctx, SS_K_GEMM_QKV, ctx->ta_xb, W.tb_qkv, T, qkvN, h, ctx->qkv, qkvN, EPI_BF16, norm_in));
@@ -866,6 +1030,10 @@ ss_status enqueue_forward(ss_ctx* ctx, const ss_batch* b) {
         RUN(launch(ctx, SS_K_ATTN, n_attn, [&] { return attention_launch(ap, ctx->tm_k, ctx->tm_v, ctx->st); }));
         if (b->n_combs && !ctx->fused_combine)
             RUN(launch(ctx, SS_K_ATTN_COMBINE, 1, [&] { return attention_combine_launch(ap, ctx->st); }));
+        if (chain) {
+            RUN(chain_launch(ctx, b, l));
+            continue;
+        }
         if (ctx->tp == 1) {
             RUN(gemm(ctx, SS_K_GEMM_O, ctx->ta_o, W.tb_o, T, h, qd, ctx->x, h, EPI_RESADD, res_out));
         } else if (ctx->ipc) {
@@ -1031,10 +1199,26 @@ void collect_prof(ss_ctx* ctx) {
 
 // ============================================================================ C ABI
 
+// Dev: the fused chain's per-item timeline of every layer (SS_CHAIN_TRACE=1 at ss_create):
+// n >= 0 copies min(n, L * 4096 * 16) u64 into out; n < 0 clears it.
+SS_API ss_status ss_debug_chain_trace(ss_ctx* ctx, unsigned long long* out, int64_t n) {
+    if (!ctx) return SS_INVALID_ARG;
+    DevGuard dg(ctx->device);
+    if (!ctx->chain_trace) return fail(ctx, SS_INVALID_ARG, "no chain trace (SS_CHAIN_TRACE=1, and a chain launch)");
+    const size_t total = size_t(ctx->L) * kChainTraceItems * 16;
+    CK(cudaStreamSynchronize(ctx->st));
+    if (n < 0) {
+        CK(cudaMemset(ctx->chain_trace, 0, total * 8));
+        return SS_OK;
+    }
+    CK(cudaMemcpy(out, ctx->chain_trace, std::min(size_t(n), total) * 8, cudaMemcpyDeviceToHost));
+    return SS_OK;
+}
+
 SS_API const char* ss_kernel_class_name(int32_t k) {
     static const char* names[SS_K_NUM_CLASSES] = {"embed",   "rmsnorm", "gemm_qkv",    "rope_kv_append",
                                                   "attention", "attn_combine", "gemm_o", "gemm_gate_up",
-                                                  "gemm_down", "nccl_allreduce", "lm_head", "argmax"};
+                                                  "gemm_down", "nccl_allreduce", "lm_head", "argmax", "gemm_chain"};
     return (k >= 0 && k < SS_K_NUM_CLASSES) ? names[k] : "unknown";
 }
 
@@ -1366,6 +1550,9 @@ SS_API void ss_destroy(ss_ctx* ctx) {
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     cudaFree(ctx->part_red);
+    cudaFree(ctx->chain_flags);
+    cudaFree(ctx->chain_part);
+    cudaFree(ctx->chain_trace);
     if (ctx->grp) {
         for (ss_ctx*& r : ctx->grp->ranks)
             if (r == ctx) r = nullptr;

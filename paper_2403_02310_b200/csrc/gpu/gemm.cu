@@ -1038,6 +1038,587 @@ cudaError_t launch_t(const GemmPlan& p, cudaStream_t st) {
 // Tile shapes compiled: CG=2 pairs with BN in steps of 32, CG=1 with 128 / 256.
 constexpr int kBn2[] = {64, 96, 128, 160, 192, 224, 256};
 
+// ============================================================== fused projection chain
+// (see ChainPlan in kernels.cuh). CTA pairs, 256 x 256 tiles, the same warp roles,
+// operand ring and TMEM double buffer as gemm_tcgen05_kernel<2, 256, *>.
+
+__device__ __forceinline__ uint32_t atom_add_acqrel_gpu(uint32_t* p, uint32_t v) {
+    uint32_t old;
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+// Bounded spin on a flag written by another CTA of this grid (a dependency of an earlier
+// work item, which every pair reaches in order: see the deadlock-freedom note below).
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void spin_flag(const uint32_t* f, uint32_t want) {
+    if (ld_acquire_gpu(f) == want) return;
+    const uint64_t t0 = globaltimer_ns();
+    uint32_t spins = 0;
+    while (ld_acquire_gpu(f) != want) {  // a schedule bug traps after 2 s instead of hanging the GPU
+        if ((++spins & 1023u) == 0 && globaltimer_ns() - t0 > 2000000000ull) __trap();
+    }
+}
+// Lane-parallel wait on n flags (n <= 32 per step), then a warp-wide acquire point.
+__device__ __forceinline__ void warp_wait_flags(const uint32_t* f, int n, uint32_t want, int lane) {
+    for (int i = lane; i - lane < n; i += 32)
+        if (i < n) spin_flag(f + i, want);
+    __syncwarp();
+    __threadfence();
+}
+
+struct ChainItem {
+    int p, m, n, s, kb0, kb1;
+};
+__device__ __forceinline__ ChainItem chain_item(const ChainPlan& P, int i) {
+    int p = 0;
+    while (p + 1 < P.n_phases && i >= P.ph[p + 1].item0) ++p;
+    const ChainPhase& ph = P.ph[p];
+    const int j = i - ph.item0, S = ph.splits;
+    ChainItem it;
+    it.p = p;
+    it.m = j % P.num_mt;
+    const int r = j / P.num_mt;
+    it.s = r % S;
+    it.n = r / S;
+    const int nkb = (ph.K + BK - 1) / BK;
+    it.kb0 = it.s * nkb / S;
+    it.kb1 = (it.s + 1) * nkb / S;
+    return it;
+}
+
+// Deadlock freedom: every pair walks its items in increasing global index; an item's
+// producer and epilogue wait only on flags of items of EARLIER phases (lower indices), and
+// K splits never wait on each other (the last arriver reduces). The lowest unfinished item
+// therefore always has its inputs and its pair free to run it. All pairs are co-resident
+// (the grid is one resident wave, checked at launch).
+__global__ void __launch_bounds__(kThreads, 1) gemm_chain_kernel(const __grid_constant__ ChainPlan P) {
+    constexpr int CG = 2, BN = 256;
+    using Cfg = GemmCfg<CG, BN, 128>;
+    constexpr int STAGES = Cfg::STAGES;
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + STAGES * Cfg::A_BYTES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2 + 8);
+
+    const int warp = threadIdx.x / 32;
+    const int lane = threadIdx.x % 32;
+    const uint32_t rank = cluster_rank();
+    const bool leader = rank == 0;
+    const int gid = blockIdx.x / CG, G = gridDim.x / CG;
+    const int M = P.M, num_mt = P.num_mt, total = P.total_items;
+
+    if (threadIdx.x == 0) {
+        for (int p = 0; p < P.n_phases; ++p) {
+            tma_prefetch(&P.tmA[p]);
+            tma_prefetch(&P.tmB[p]);
+        }
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 8 * CG);
+        }
+        mbar_fence_init();
+    }
+    if (warp == 1) tmem_alloc_cg<CG>(tmem_slot, Cfg::TMEM_COLS);
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    pdl_launch_dependents();
+
+    if (warp == 0) {  // ---------------- TMA producer (both CTAs; lane 0 issues, the warp checks flags)
+        const uint32_t full_leader = peer_addr(full, 0);
+        const uint64_t polA = l2_policy_evict_last();
+        const uint64_t polB = l2_policy_evict_first();
+        // the first item's first weight stages before the grid-dependency wait
+        int npre = 0;
+        if (gid < total) {
+            const ChainItem it = chain_item(P, gid);
+            const int n0 = it.n * BN + Cfg::B_ROWS * int(rank);
+            npre = it.kb1 - it.kb0 < STAGES ? it.kb1 - it.kb0 : STAGES;
+            if (lane == 0)
+                for (int j = 0; j < npre; ++j) {
+                    if (leader) mbar_arrive_expect_tx(&full[j], 2 * Cfg::STAGE_BYTES);
+                    tma_load_2d_cg2_hint(sB + j * Cfg::B_BYTES, &P.tmB[it.p], (it.kb0 + j) * BK, n0,
+                                         full_leader + uint32_t(j * 8), polB);
+                }
+        }
+        pdl_wait();
+        const uint32_t E = P.epoch + (P.epoch_base ? *reinterpret_cast<const volatile uint32_t*>(P.epoch_base) : 0u);
+        // Known-ready prefix of the dependency phase's tiles, per M-tile (lane m holds M-tile
+        // m's; more than 32 M-tiles: no cache). Flags only go up within a launch, so a tile
+        // seen ready stays ready: most items then need no flag traffic at all.
+        int kr = -1, kr_dep = -2;
+        int s = 0, itn = 0;
+        uint32_t ph = 0;
+        for (int i = gid; i < total; i += G) {
+            const ChainItem it = chain_item(P, i);
+            const ChainPhase& cp = P.ph[it.p];
+            if (P.trace && leader && lane == 0) P.trace[size_t(i) * 16 + 0] = globaltimer_ns();
+            const int m0 = it.m * Cfg::TILE_M + 128 * int(rank);
+            const int n0 = it.n * BN + Cfg::B_ROWS * int(rank);
+            const CUtensorMap* tA = &P.tmA[it.p];
+            const CUtensorMap* tB = &P.tmB[it.p];
+            const uint32_t* rdy = cp.dep >= 0 ? P.ph[cp.dep].ready + size_t(it.m) * P.ph[cp.dep].num_n : nullptr;
+            const int dcols = cp.dep >= 0 ? P.ph[cp.dep].out_cols : 1;
+            const int nd = cp.dep >= 0 ? P.ph[cp.dep].num_n : 0;
+            if (cp.dep != kr_dep) {
+                kr = -1;
+                kr_dep = cp.dep;
+            }
+            const bool cache = num_mt <= 32;
+            int known = cache ? __shfl_sync(0xffffffffu, kr, it.m & 31) : -1;
+            for (int kb = it.kb0; kb < it.kb1; ++kb, ++itn) {
+                if (rdy) {  // the producing phase's output tile covering these 64 columns
+                    const int ct = kb * BK / dcols;
+                    if (ct > known) {
+                        int cnt = 0;
+                        for (;;) {  // one round trip checks 32 tiles
+                            const int t = ct + lane;
+                            const bool ok = t >= nd || ld_acquire_gpu(rdy + t) == E;
+                            const unsigned nm = ~__ballot_sync(0xffffffffu, ok);
+                            cnt = nm ? __ffs(nm) - 1 : 32;
+                            if (cnt > 0) break;
+                            if (lane == 0) spin_flag(rdy + ct, E);
+                            __syncwarp();
+                        }
+                        known = ct + cnt - 1;
+                        if (cache && lane == (it.m & 31)) kr = known;
+                        __syncwarp();
+                        if (lane == 0) fence_proxy_async_global();
+                    }
+                }
+                if (lane == 0) {
+                    const bool pre = itn < npre;
+                    if (!pre) mbar_wait(&empty[s], ph ^ 1);
+                    const uint32_t fb = full_leader + uint32_t(s * 8);
+                    if (!pre) {
+                        if (leader) mbar_arrive_expect_tx(&full[s], 2 * Cfg::STAGE_BYTES);
+                        tma_load_2d_cg2_hint(sB + s * Cfg::B_BYTES, tB, kb * BK, n0, fb, polB);
+                    }
+                    tma_load_2d_cg2_hint(sA + s * Cfg::A_BYTES, tA, kb * BK, m0, fb, polA);
+                }
+                __syncwarp();
+                if (++s == STAGES) {
+                    s = 0;
+                    ph ^= 1;
+                }
+            }
+            if (P.trace && leader && lane == 0) P.trace[size_t(i) * 16 + 1] = globaltimer_ns();
+        }
+    } else if (warp == 1) {
+        if (leader) {  // ---------------- MMA issuer
+            constexpr uint32_t idesc = umma_idesc_bf16(Cfg::TILE_M, BN);
+            const uint64_t adesc0 = umma_desc_sw128(smem_u32(sA)), bdesc0 = umma_desc_sw128(smem_u32(sB));
+            int s = 0, acc = 0;
+            uint32_t ph = 0, acc_ph = 0;
+            for (int i = gid; i < total; i += G) {
+                const ChainItem it = chain_item(P, i);
+                mbar_wait(&tempty[acc], acc_ph ^ 1);
+                tc_fence_after();
+                if (P.trace && lane == 0) P.trace[size_t(i) * 16 + 2] = globaltimer_ns();
+                const uint32_t d_tmem = tmem_base + uint32_t(acc * BN);
+                const int nk = it.kb1 - it.kb0;
+                for (int k = 0; k < nk; ++k) {
+                    mbar_wait(&full[s], ph);
+                    const uint64_t ad = adesc0 + uint64_t((s * Cfg::A_BYTES) >> 4);
+                    const uint64_t bd = bdesc0 + uint64_t((s * Cfg::B_BYTES) >> 4);
+                    if (elect_one()) {
+#pragma unroll
+                        for (int kk = 0; kk < BK / 16; ++kk)
+                            mma_cg<CG>(d_tmem, ad + uint64_t(2 * kk), bd + uint64_t(2 * kk), idesc,
+                                       (k > 0 || kk > 0) ? 1u : 0u);
+                        commit_cg<CG>(&empty[s]);
+                    }
+                    __syncwarp();
+                    if (++s == STAGES) {
+                        s = 0;
+                        ph ^= 1;
+                    }
+                }
+                if (elect_one()) commit_cg<CG>(&tfull[acc]);
+                __syncwarp();
+                if (P.trace && lane == 0) P.trace[size_t(i) * 16 + 3] = globaltimer_ns();
+                if (++acc == 2) {
+                    acc = 0;
+                    acc_ph ^= 1;
+                }
+            }
+        }
+    } else {  // ---------------------------- epilogue warps 2..9
+        pdl_wait();
+        const uint32_t E = P.epoch + (P.epoch_base ? *reinterpret_cast<const volatile uint32_t*>(P.epoch_base) : 0u);
+        const int q = warp & 3;
+        const int ew = warp - 2, half = ew >> 2;
+        const uint32_t tempty_leader = peer_addr(tempty, 0);
+        const int rloc = 128 * int(rank) + q * 32 + lane;
+        uint4* ep = reinterpret_cast<uint4*>(smem + STAGES * Cfg::STAGE_BYTES + 1024 + ew * 4096);
+        const int crow = lane >> 3, cch = lane & 7;
+        int acc = 0;
+        uint32_t acc_ph = 0;
+        auto release_acc = [&]() {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster_relaxed(tempty_leader + uint32_t(acc * 8));
+            if (++acc == 2) {
+                acc = 0;
+                acc_ph ^= 1;
+            }
+        };
+        for (int i = gid; i < total; i += G) {
+            const ChainItem it = chain_item(P, i);
+            const ChainPhase& cp = P.ph[it.p];
+            const EpiArgs& ea = cp.ea;
+            const int S = cp.splits, EPI = cp.epi, N = cp.N, ldo = cp.ldo;
+            const int tile = it.m * cp.num_n + it.n;
+            const int m0 = it.m * Cfg::TILE_M, n0 = it.n * BN;
+            const int row = m0 + rloc, rbase = row - lane;
+            // inputs written by earlier items: acquire their tiles' flags, then read coherently
+            if (ea.ssq_in && cp.dep >= 0)
+                warp_wait_flags(P.ph[cp.dep].ready + size_t(it.m) * P.ph[cp.dep].num_n, P.ph[cp.dep].num_n, E, lane);
+            if (cp.res_dep >= 0) warp_wait_flags(P.ph[cp.res_dep].ready + tile, 1, E, lane);
+            float rs = 1.f;
+            if (ea.ssq_in) {  // folded RMSNorm row scale (coalesced loads + transpose-reduce)
+                const int n4 = ea.ssq_in_n >> 2;
+                float a[32];
+#pragma unroll
+                for (int r = 0; r < 32; ++r) a[r] = 0.f;
+                for (int k = lane; k - lane < n4; k += 32) {
+#pragma unroll
+                    for (int r = 0; r < 32; ++r) {
+                        if (k < n4 && rbase + r < M) {
+                            const float4 w = __ldcg(reinterpret_cast<const float4*>(ea.ssq_in + size_t(rbase + r) * ea.ssq_in_n) + k);
+                            a[r] += (w.x + w.y) + (w.z + w.w);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int off = 16; off >= 1; off >>= 1) {
+                    const bool up = lane & off;
+#pragma unroll
+                    for (int k = 0; k < off; ++k) {
+                        const float send = up ? a[k] : a[k + off];
+                        const float keep = up ? a[k + off] : a[k];
+                        a[k] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+                    }
+                }
+                rs = rsqrtf(a[0] * ea.inv_dim + ea.eps);
+            }
+            // QKV: position / slot of this row (batch inputs); the RoPE factors are read at use
+            // (L1-resident table rows; preloading them spilled registers)
+            int q_pos = 0;
+            int64_t q_slot = 0;
+            if (EPI == EPI_QKV && row < M) {
+                q_pos = ea.pos[row];
+                q_slot = ea.slot[row];
+            }
+            mbar_wait(&tfull[acc], acc_ph);
+            tc_fence_after();
+            if (P.trace && leader && ew == 0 && lane == 0) P.trace[size_t(i) * 16 + 4] = globaltimer_ns();
+            const uint32_t t_row = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN);
+            bool from_part = false;
+            if (S > 1) {
+                // publish this split's partial (staged swizzled image, copied out coalesced)
+                uint4* dst = reinterpret_cast<uint4*>(cp.part + (((size_t(tile) * S + it.s) * 2 + rank) * 8) * 4096 +
+                                                      (q * 32) * 32);
+#pragma unroll 1
+                for (int c = half; c < BN / 32; c += 2) {
+                    uint32_t v[32];
+                    tmem_ld32(t_row + uint32_t(c * 32), v);
+                    tmem_wait_ld();
+                    stage_rows(ep, v, lane);
+                    __syncwarp();
+                    uint4* d = dst + size_t(c) * 128 * 8;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) d[j * 32 + lane] = ep[j * 32 + lane];
+                    __syncwarp();
+                }
+                release_acc();
+                __threadfence();
+                __syncwarp();
+                uint32_t old = 0;
+                if (lane == 0) old = atom_add_acqrel_gpu(&cp.pcnt[(size_t(tile) * 2 + rank) * 8 + ew], 1u);
+                old = __shfl_sync(0xffffffffu, old, 0);
+                if (old != uint32_t(S - 1)) continue;  // another split finishes this slice
+                if (lane == 0) cp.pcnt[(size_t(tile) * 2 + rank) * 8 + ew] = 0u;
+                __syncwarp();
+                __threadfence();  // every split's partial (acquired by lane 0) before the reads below
+                from_part = true;
+            }
+            // chunk c (32 columns) of this warp's 32 rows: from TMEM, or the sum of every
+            // split's partial in split order
+            auto load_chunk = [&](int c, uint32_t (&v)[32]) {
+                if (!from_part) {
+                    tmem_ld32(t_row + uint32_t(c * 32), v);
+                    tmem_wait_ld();
+                    return;
+                }
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] = 0u;
+                for (int sp = 0; sp < S; ++sp) {  // added in split order (deterministic)
+                    const uint4* src = reinterpret_cast<const uint4*>(
+                        cp.part + (((size_t(tile) * S + sp) * 2 + rank) * 8) * 4096 + (size_t(c) * 128 + q * 32) * 32);
+                    // global -> smem without a register round trip (8 x 16 B in flight per lane)
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) cp_async16(smem_u32(ep + j * 32 + lane), src + j * 32 + lane);
+                    cp_async_commit();
+                    cp_async_wait<0>();
+                    __syncwarp();
+                    add_rows(v, ep, lane);
+                    __syncwarp();
+                }
+            };
+            if (EPI == EPI_QKV) {
+                const int ps = ea.hd / 64;
+                const int64_t blk = q_slot / ea.bs, off = q_slot % ea.bs;
+#pragma unroll 1
+                for (int pi = half; pi < (BN / ea.hd) * ps; pi += 2) {
+                    const int c = (pi / ps) * (2 * ps) + (pi % ps);
+                    uint32_t x1[32], x2[32];
+                    load_chunk(c, x1);
+                    load_chunk(c + ps, x2);
+                    const int col = n0 + c * 32;
+                    if (col >= N) continue;
+                    const int hh = col / ea.hd, i0 = col % ea.hd;
+                    const bool rot = hh < ea.nq + ea.nkv;
+                    const float4* cs = reinterpret_cast<const float4*>(ea.rope + size_t(q_pos) * (ea.hd / 2) + i0);
+#pragma unroll
+                    for (int jj = 0; jj < 4; ++jj) {
+                        uint32_t lo[4], hi[4];
+                        float4 rc[4];
+                        if (rot) {
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) rc[k] = __ldg(cs + 4 * jj + k);
+                        }
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const int j = 4 * jj + k;
+                            const float a0 = __uint_as_float(x1[2 * j]) * rs, a1 = __uint_as_float(x1[2 * j + 1]) * rs;
+                            const float b0 = __uint_as_float(x2[2 * j]) * rs, b1 = __uint_as_float(x2[2 * j + 1]) * rs;
+                            if (rot) {
+                                const float4 f = rc[k];
+                                lo[k] = pack_bf16(a0 * f.x - b0 * f.y, a1 * f.z - b1 * f.w);
+                                hi[k] = pack_bf16(b0 * f.x + a0 * f.y, b1 * f.z + a1 * f.w);
+                            } else {
+                                lo[k] = pack_bf16(a0, a1);
+                                hi[k] = pack_bf16(b0, b1);
+                            }
+                        }
+                        ep[lane * 8 + (jj ^ (lane & 7))] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+                        ep[lane * 8 + ((jj + 4) ^ (lane & 7))] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+                    }
+                    __nv_bfloat16* dst = nullptr;
+                    if (row < M) {
+                        if (hh < ea.nq) dst = ea.q_out + (size_t(row) * ea.nq + hh) * ea.hd;
+                        else if (hh < ea.nq + ea.nkv) dst = ea.kc + ((size_t(blk) * ea.nkv + (hh - ea.nq)) * ea.bs + off) * ea.hd;
+                        else dst = ea.vc + ((size_t(blk) * ea.nkv + (hh - ea.nq - ea.nkv)) * ea.bs + off) * ea.hd;
+                        dst += i0;
+                    }
+                    __syncwarp();
+                    const uint64_t dp = reinterpret_cast<uint64_t>(dst);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const int r = 4 * j + crow;
+                        const uint64_t d = (uint64_t(__shfl_sync(0xffffffffu, uint32_t(dp >> 32), r)) << 32) |
+                                           __shfl_sync(0xffffffffu, uint32_t(dp), r);
+                        if (d) {
+                            __nv_bfloat16* pp = reinterpret_cast<__nv_bfloat16*>(d) + (cch < 4 ? cch * 8 : ea.hd / 2 + (cch - 4) * 8);
+                            *reinterpret_cast<uint4*>(pp) = ep[r * 8 + (cch ^ (r & 7))];
+                        }
+                    }
+                    __syncwarp();
+                }
+            } else if (EPI == EPI_SWIGLU) {
+#pragma unroll 1
+                for (int c = 2 * half; c < BN / 32; c += 4) {
+                    uint32_t v[32], ut[32];
+                    load_chunk(c, v);
+                    load_chunk(c + 1, ut);
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        v[j] = __float_as_uint(silu(__uint_as_float(v[j]) * rs) * (__uint_as_float(ut[j]) * rs));
+                    stage_rows(ep, v, lane);
+                    __syncwarp();
+                    const int col = n0 + c * 32;
+                    if (col < N) {
+                        const int ccol = col / 2 + cch * 4;
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const int r = 4 * j + crow, grow = rbase + r;
+                            const uint4 u = ep[r * 8 + (cch ^ (r & 7))];
+                            if (grow < M)
+                                *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(cp.out) + size_t(grow) * ldo + ccol) =
+                                    make_uint2(pack_bf16(__uint_as_float(u.x), __uint_as_float(u.y)),
+                                               pack_bf16(__uint_as_float(u.z), __uint_as_float(u.w)));
+                        }
+                    }
+                    __syncwarp();
+                }
+            } else {  // EPI_RESADD (x_f32 += D, + bf16 copy and per-chunk sums of squares) / EPI_BF16
+                // residual of chunk c (coalesced layout, rows rbase + 4j + crow), loaded a chunk ahead
+                float4 xin[2][8];
+                auto load_res = [&](int c, float4 (&xr)[8]) {
+                    const int col = n0 + c * 32 + cch * 4;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const int grow = rbase + 4 * j + crow;
+                        xr[j] = (EPI == EPI_RESADD && grow < M && col < N)
+                                    ? __ldcg(reinterpret_cast<const float4*>(static_cast<const float*>(cp.out) + size_t(grow) * ldo + col))
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
+                };
+                if (EPI == EPI_RESADD) load_res(half, xin[0]);
+#pragma unroll
+                for (int ci = 0; ci < BN / 64; ++ci) {
+                    const int c = half + 2 * ci;
+                    if (EPI == EPI_RESADD && ci + 1 < BN / 64) load_res(c + 2, xin[(ci + 1) & 1]);
+                    uint32_t v[32];
+                    load_chunk(c, v);
+                    if (ea.ssq_in) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) * rs);
+                    }
+                    stage_rows(ep, v, lane);
+                    __syncwarp();
+                    const int col = n0 + c * 32;
+                    if (col < N) {
+                        const int ccol = col + cch * 4;
+                        float ss[8];
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const int r = 4 * j + crow, grow = rbase + r;
+                            const uint4 u = ep[r * 8 + (cch ^ (r & 7))];
+                            float4 d = make_float4(__uint_as_float(u.x), __uint_as_float(u.y), __uint_as_float(u.z),
+                                                   __uint_as_float(u.w));
+                            ss[j] = 0.f;
+                            if (grow < M) {
+                                if (EPI == EPI_RESADD) {
+                                    float* xp = static_cast<float*>(cp.out) + size_t(grow) * ldo + ccol;
+                                    const float4 x0 = xin[ci & 1][j];
+                                    d.x += x0.x;
+                                    d.y += x0.y;
+                                    d.z += x0.z;
+                                    d.w += x0.w;
+                                    ss[j] = d.x * d.x + d.y * d.y + d.z * d.z + d.w * d.w;
+                                    *reinterpret_cast<float4*>(xp) = d;
+                                    if (ea.xb_out)
+                                        *reinterpret_cast<uint2*>(ea.xb_out + size_t(grow) * ldo + ccol) =
+                                            make_uint2(pack_bf16(d.x, d.y), pack_bf16(d.z, d.w));
+                                } else {
+                                    *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(cp.out) + size_t(grow) * ldo + ccol) =
+                                        make_uint2(pack_bf16(d.x, d.y), pack_bf16(d.z, d.w));
+                                }
+                            }
+                        }
+                        if (EPI == EPI_RESADD && ea.xb_out) {
+#pragma unroll
+                            for (int mm = 1; mm <= 4; mm <<= 1)
+#pragma unroll
+                                for (int j = 0; j < 8; ++j) ss[j] += __shfl_xor_sync(0xffffffffu, ss[j], mm);
+                            if (cch == 0) {
+#pragma unroll
+                                for (int j = 0; j < 8; ++j) {
+                                    const int grow = rbase + 4 * j + crow;
+                                    if (grow < M) ea.ssq_out[size_t(grow) * (ldo / 32) + col / 32] = ss[j];
+                                }
+                            }
+                        }
+                    }
+                    __syncwarp();
+                    if (P.trace && leader && ew == 0 && lane == 0) P.trace[size_t(i) * 16 + 6 + ci] = globaltimer_ns();
+                }
+            }
+            if (P.trace && leader && ew == 0 && lane == 0) P.trace[size_t(i) * 16 + 14] = globaltimer_ns();
+            if (!from_part) release_acc();
+            // this warp's share of the tile is stored: count it; the 16th warp publishes the tile
+            fence_proxy_async_global();  // consumers read these stores through TMA (async proxy)
+            __threadfence();
+            __syncwarp();
+            if (lane == 0) {
+                const uint32_t old = atom_add_acqrel_gpu(&cp.rcnt[tile], 1u);
+                if (P.trace && leader && ew == 0) P.trace[size_t(i) * 16 + 15] = globaltimer_ns();
+                if (old == 2u * 8u - 1u) {
+                    cp.rcnt[tile] = 0u;
+                    st_release_gpu(&cp.ready[tile], E);
+                    if (P.trace) P.trace[size_t(i) * 16 + 5] = globaltimer_ns();
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    cluster_sync();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc_cg<CG>(tmem_base, Cfg::TMEM_COLS);
+    }
+}
+
+}  // namespace
+
+void gemm_chain_finalize(ChainPlan& p) {
+    int item = 0;
+    for (int i = 0; i < p.n_phases; ++i) {
+        ChainPhase& ph = p.ph[i];
+        ph.num_n = (ph.N + 255) / 256;
+        ph.item0 = item;
+        item += p.num_mt * ph.num_n * (ph.splits < 1 ? 1 : ph.splits);
+    }
+    p.total_items = item;
+}
+
+cudaError_t gemm_chain_launch(const ChainPlan& p, cudaStream_t st) {
+    using Cfg = GemmCfg<2, 256, 128>;
+    static DevOnce once;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+    if (!once.attr[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(gemm_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+        if (e != cudaSuccess) return e;
+        once.attr[dev] = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = Cfg::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    // every pair must be resident at once (flag waits between pairs)
+    if (once.resident[dev] == 0) {
+        cfg.gridDim = dim3(2 * (p.num_sms / 2));
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, gemm_chain_kernel, &cfg) != cudaSuccess || n <= 0) n = p.num_sms / 2;
+        once.resident[dev] = n > p.num_sms / 2 ? p.num_sms / 2 : n;
+    }
+    int groups = once.resident[dev];
+    if (groups > p.total_items) groups = p.total_items;
+    if (groups < 1) return cudaSuccess;
+    cfg.gridDim = dim3(2 * groups);
+    if (p.debug)
+        fprintf(stderr, "gemm chain M=%d phases=%d items=%d groups=%d\n", p.M, p.n_phases, p.total_items, groups);
+    return cudaLaunchKernelEx(&cfg, gemm_chain_kernel, p);
+}
+
+namespace {
 }  // namespace
 
 Tuning tuning_from_env() {
@@ -1057,6 +1638,12 @@ Tuning tuning_from_env() {
     if (getenv("SS_GEMM_AR128")) t.gemm_ar128 = 1;
     if (getenv("SS_GEMM_DEBUG")) t.gemm_debug = 1;
     geti("SS_GEMM_LDO_PAD", t.ldo_pad);
+    geti("SS_CHAIN", t.chain);
+    if (const char* f = getenv("SS_CHAIN_S"))
+        sscanf(f, "%d,%d,%d,%d", &t.chain_splits[0], &t.chain_splits[1], &t.chain_splits[2], &t.chain_splits[3]);
+    if (getenv("SS_CHAIN_DEBUG")) t.chain_debug = 1;
+    geti("SS_CHAIN_TRACE", t.chain_trace);
+    geti("SS_GEMM_MAXG", t.gemm_max_groups);
     static const char* names[5] = {"SS_GEMM_QKV", "SS_GEMM_O", "SS_GEMM_GATEUP", "SS_GEMM_DOWN", "SS_GEMM_LMHEAD"};
     for (int i = 0; i < 5; ++i)
         if (const char* f = getenv(names[i])) {
@@ -1162,6 +1749,7 @@ bool gemm_prepare(GemmPlan& p, const void* A, uint64_t a_rows, const void* B, in
     p.force_sk = tu.gemm_sk;
     p.force_splits = tu.gemm_splits;
     p.debug = tu.gemm_debug;
+    p.max_groups = tu.gemm_max_groups;
     p.cg = s.cg;
     p.bn = bn ? bn : s.bn;
     p.splits = s.splits;

@@ -66,6 +66,12 @@ struct Tuning {
     int gemm_debug = 0;       // SS_GEMM_DEBUG: print each launch's schedule
     int gemm_force[5][3] = {{-1, 0, 1}, {-1, 0, 1}, {-1, 0, 1}, {-1, 0, 1}, {-1, 0, 1}};  // SS_GEMM_<QKV|O|GATEUP|DOWN|LMHEAD>=mode,bn[,splits]
     int ldo_pad = 0;          // SS_GEMM_LDO_PAD (ss_k_gemm only)
+    int chain = 0;            // SS_CHAIN=1: the fused projection chain instead of separate launches
+                              // (measured slower on the canonical batch)
+    int chain_splits[4] = {0, 0, 0, 0};  // SS_CHAIN_S=o,gu,down,qkv: K splits per chain phase (0: auto)
+    int chain_debug = 0;      // SS_CHAIN_DEBUG: print each chain launch
+    int chain_trace = 0;      // SS_CHAIN_TRACE: record the chain's per-item timeline (ss_debug_chain_trace)
+    int gemm_max_groups = 0;  // SS_GEMM_MAXG: at most this many CTA groups per GEMM launch (dev scaling probe)
 };
 Tuning tuning_from_env();
 
@@ -92,6 +98,48 @@ struct GemmPlan {
     int max_groups = 0;  // > 0: at most this many CTA groups (SM budget of a concurrent launch)
     EpiArgs ea;
 } __attribute__((aligned(64)));
+
+// ---- Fused persistent chain of dependent projections (one launch per layer, TP = 1):
+// O -> gate/up -> down -> next layer's QKV. Every CTA pair walks one global list of
+// 256 x 256 tiles (phase-major; inside a phase column-tile-major, K slices, then M tiles),
+// round-robin. A tile's TMA producer waits, per 64-column k-block of A, on the ready flag of
+// the producing phase's output tile covering those columns, so a phase streams behind its
+// predecessor instead of waiting for the whole grid, and a pair's next tile (from any phase)
+// runs its main loop while its previous tile's epilogue drains (double-buffered TMEM): the
+// per-launch fill, drain and wave-quantisation tails of separate launches disappear.
+// K-split tiles publish fp32 partials; the last arriving split (per epilogue warp) sums all
+// splits in fixed split order (deterministic) and runs the epilogue. All flags carry the
+// launch epoch (epoch + *epoch_base), counters self-reset.
+constexpr int kChainMaxPhases = 4;
+struct ChainPhase {
+    int N = 0, K = 0, epi = 0, splits = 1;
+    int num_n = 0;       // 256-column tiles
+    int item0 = 0;       // first global work item of the phase
+    int dep = -1;        // phase whose output is this phase's A (-1: written before the launch)
+    int res_dep = -1;    // phase whose residual-add output this phase's residual add reads
+    int out_cols = 256;  // output columns per tile (SwiGLU: 128), for consumers' k-block mapping
+    void* out = nullptr;
+    int ldo = 0;
+    uint32_t* ready = nullptr;  // [num_mt][num_n] tile-done flags (value = launch epoch)
+    uint32_t* rcnt = nullptr;   // [num_mt][num_n] epilogue warps done (self-resetting)
+    uint32_t* pcnt = nullptr;   // [num_mt][num_n][2][8] split arrivals per epilogue warp (self-resetting)
+    float* part = nullptr;      // [num_mt][num_n][splits][2][8 chunks][128][32] fp32 split partials
+    EpiArgs ea;
+};
+struct ChainPlan {
+    CUtensorMap tmA[kChainMaxPhases], tmB[kChainMaxPhases];  // A box 128 x 64, B box 128 x 64
+    int n_phases = 0, M = 0, num_mt = 0, total_items = 0, num_sms = 148;
+    uint32_t epoch = 0;
+    const uint32_t* epoch_base = nullptr;
+    int debug = 0;
+    // dev timeline (SS_CHAIN_TRACE): per item, globaltimer ns at producer start / producer
+    // done / MMA start / MMA done / epilogue start / epilogue done (leader CTA), or null
+    unsigned long long* trace = nullptr;
+    ChainPhase ph[kChainMaxPhases];
+} __attribute__((aligned(64)));
+// Items of one phase: num_mt * num_n * splits; fills item0 / total_items.
+void gemm_chain_finalize(ChainPlan& p);
+cudaError_t gemm_chain_launch(const ChainPlan& p, cudaStream_t st);
 
 // Workspace sizes for gemm_launch (max over tile shapes) for num_sms SMs.
 inline size_t gemm_part_floats(int num_sms) { return size_t(num_sms) * 128 * 256; }

@@ -56,7 +56,7 @@ MODELS = {
 }
 
 KERNEL_CLASSES = ["embed", "rmsnorm", "gemm_qkv", "rope_kv_append", "attention", "attn_combine", "gemm_o",
-                  "gemm_gate_up", "gemm_down", "nccl_allreduce", "lm_head", "argmax"]
+                  "gemm_gate_up", "gemm_down", "nccl_allreduce", "lm_head", "argmax", "gemm_chain"]
 
 
 def nccl_unique_id() -> bytes:
