@@ -17,6 +17,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <condition_variable>
 #include <cstring>
@@ -248,6 +249,9 @@ struct ss_ctx {
     int ipc_algo = SS_AR_AUTO;   // ss_set_tp_allreduce / SS_TP_ALLREDUCE
 
     Tuning tu;  // dev overrides, read once at ss_create (tuning_from_env)
+    // host-side microseconds of the last ss_forward_hybrid: validate + work list + staging,
+    // enqueue (H2D + graph launch / eager launches + D2H), wait for the stream (ss_debug_host_times)
+    double host_us[3] = {};
     bool prof = false;
     std::vector<Prof> pend;
     std::vector<cudaEvent_t> free_ev;
@@ -761,7 +765,8 @@ ss_status gemm(ss_ctx* ctx, int cls, const CUtensorMap& ta, WMaps& tb, int M, in
         if (twin) p.tmA = *twin;
         else p.ar = 128;
     }
-    const CUtensorMap* mb = tb.get(p.bn / p.cg);
+    p.mc = gemm_mc(s, M, ctx->tu);
+    const CUtensorMap* mb = tb.get(p.bn / p.cg / p.mc);
     if (!mb) return fail(ctx, SS_CUDA_ERROR, "cuTensorMapEncodeTiled failed (weight tile map)");
     p.tmB = *mb;
     p.part = ctx->sk_part;
@@ -1636,12 +1641,28 @@ SS_API ss_status ss_forward_hybrid(ss_ctx* ctx, const ss_batch_desc* desc, float
                                    float* elapsed_ms) {
     if (!ctx) return SS_INVALID_ARG;
     DevGuard dg(ctx->device);
+    using clk = std::chrono::steady_clock;
+    const auto t0 = clk::now();
     if (ss_status s = upload(ctx, desc, &ctx->scratch, ctx->ev0)) return s;
+    const auto t1 = clk::now();
     if (ss_status s = run_forward(ctx, &ctx->scratch)) return s;
     CK(cudaEventRecord(ctx->ev1, ctx->st));
+    const auto t2 = clk::now();
     if (ss_status s = read_outputs(ctx, &ctx->scratch, logits, next)) return s;
     CK(cudaEventSynchronize(ctx->ev1));
+    const auto t3 = clk::now();
+    ctx->host_us[0] = std::chrono::duration<double, std::micro>(t1 - t0).count();
+    ctx->host_us[1] = std::chrono::duration<double, std::micro>(t2 - t1).count();
+    ctx->host_us[2] = std::chrono::duration<double, std::micro>(t3 - t2).count();
     if (elapsed_ms) CK(cudaEventElapsedTime(elapsed_ms, ctx->ev0, ctx->ev1));
+    return SS_OK;
+}
+
+// Dev: host-side phases of the last ss_forward_hybrid (us): [0] validate + work list +
+// staging (+ the H2D enqueue), [1] forward enqueue, [2] D2H + wait for the stream.
+SS_API ss_status ss_debug_host_times(ss_ctx* ctx, double* out3) {
+    if (!ctx || !out3) return SS_INVALID_ARG;
+    for (int i = 0; i < 3; ++i) out3[i] = ctx->host_us[i];
     return SS_OK;
 }
 

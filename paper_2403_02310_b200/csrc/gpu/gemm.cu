@@ -138,16 +138,26 @@ __device__ __forceinline__ void mma_cg(uint32_t d, uint64_t a, uint64_t b, uint3
 // Commit: arrive on `bar` (same smem offset) in every CTA of the group once the
 // issued MMAs retire.
 template <int CG>
-__device__ __forceinline__ void commit_cg(uint64_t* bar) {
+__device__ __forceinline__ void commit_cg(uint64_t* bar, uint16_t mask = 3) {
     if constexpr (CG == 1) {
         umma_commit(bar);
     } else {
         asm volatile(
             "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
                 smem_u32(bar)),
-            "h"(uint16_t(3))
+            "h"(mask)
             : "memory");
     }
+}
+// 2-SM TMA multicast: this CTA's slice lands at the same smem offset in every CTA of `mask`;
+// each destination's bytes complete on the barrier at this offset in its own pair leader.
+__device__ __forceinline__ void tma_load_2d_cg2_mc_hint(void* smem_dst, const CUtensorMap* m, int32_t c0, int32_t c1,
+                                                        uint32_t bar_cluster, uint16_t mask, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+        ".L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5, %6;" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(bar_cluster), "h"(mask), "l"(policy)
+        : "memory");
 }
 
 // One lane of the (fully active) warp: the issuer of single-thread tcgen05 ops.
@@ -310,7 +320,14 @@ __device__ __forceinline__ void add_rows(uint32_t (&v)[32], const uint4* ep, int
     }
 }
 
-template <int CG, int BN, int EPI, int AR>
+// MC = 2 (CG = 2 only): clusters of two CTA pairs that walk identical weight (B) k-blocks
+// (the two M-tile members of an M-lockstep stream-K super-group, or the two M-tiles of one
+// column in the whole-tile schedule with an even M-tile count). Each CTA loads half of its
+// B rows and multicasts them to its counterpart in the other pair, so every weight byte
+// crosses the L2 -> SM fabric once per cluster instead of once per pair (the main loop is
+// bound by that fabric when all pairs run, scripts/gemm_scaling.py). Both pairs' MMA
+// commits release a stage in all four CTAs (empty barriers count two arrivals).
+template <int CG, int BN, int EPI, int AR, int MC = 1>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M_rows,
                         int row0, int N, int K, void* __restrict__ out, int ldo, int num_mt, int num_tiles,
@@ -335,7 +352,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
     const int num_kb = (K + BK - 1) / BK;
-    const uint32_t rank = CG == 2 ? cluster_rank() : 0;
+    const uint32_t crank = CG == 2 ? cluster_rank() : 0;  // rank in the cluster (MC pairs)
+    const uint32_t rank = crank & 1u;                    // rank in the CTA pair
+    const uint32_t pidx = crank >> 1;                    // pair in the cluster (MC = 2)
+    const uint32_t lead_rank = crank & ~1u;
+    const uint16_t pair_mask = uint16_t(3u << (2 * pidx));
+    const uint16_t empty_mask = MC == 2 ? uint16_t(0xF) : pair_mask;
+    const uint16_t b_mask = uint16_t((1u << rank) | (1u << (2 + rank)));  // MC = 2: this rank in both pairs
     const bool leader = rank == 0;
     const int gid = blockIdx.x / CG, G = gridDim.x / CG;
     // stream-K super-group size (mode 3: one member per M-tile; else 1)
@@ -349,7 +372,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_prefetch(&tmB);
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], MC);  // MC = 2: both pairs' MMAs released the stage
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
@@ -389,7 +412,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (warp == 0) {
         if (lane == 0) {  // ---------------- TMA producer (both CTAs)
-            const uint32_t full_leader = CG == 2 ? peer_addr(full, 0) : 0;
+            const uint32_t full_leader = CG == 2 ? peer_addr(full, lead_rank) : 0;
+            // MC = 2: this CTA's half of its B rows, multicast to its counterpart
+            constexpr int B_LOAD_ROWS = Cfg::B_ROWS / MC;
+            const int b_half = MC == 2 ? int(pidx) * B_LOAD_ROWS : 0;
             const uint64_t polA = (ea.l2hint & 1) ? l2_policy_evict_last() : l2_policy_evict_normal();
             const uint64_t polB = (ea.l2hint & 2) ? l2_policy_evict_first() : l2_policy_evict_normal();
             // The weights (B) do not depend on the preceding kernels: the first
@@ -409,7 +435,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                             tma_load_2d_hint(sB + j * Cfg::B_BYTES, &tmB, kb * BK, n0, &full[j], polB);
                         } else {
                             if (leader) mbar_arrive_expect_tx(&full[j], 2 * Cfg::STAGE_BYTES);
-                            tma_load_2d_cg2_hint(sB + j * Cfg::B_BYTES, &tmB, kb * BK, n0, full_leader + uint32_t(j * 8), polB);
+                            if constexpr (MC == 2)
+                                tma_load_2d_cg2_mc_hint(sB + j * Cfg::B_BYTES + b_half * 128, &tmB, kb * BK, n0 + b_half,
+                                                        full_leader + uint32_t(j * 8), b_mask, polB);
+                            else
+                                tma_load_2d_cg2_hint(sB + j * Cfg::B_BYTES, &tmB, kb * BK, n0, full_leader + uint32_t(j * 8), polB);
                         }
                     }
                 }
@@ -440,7 +470,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const uint32_t fb = full_leader + uint32_t(s * 8);
                         if (!pre) {
                             if (leader) mbar_arrive_expect_tx(&full[s], 2 * Cfg::STAGE_BYTES);
-                            tma_load_2d_cg2_hint(sB + s * Cfg::B_BYTES, &tmB, kb * BK, n0, fb, polB);
+                            if constexpr (MC == 2)
+                                tma_load_2d_cg2_mc_hint(sB + s * Cfg::B_BYTES + b_half * 128, &tmB, kb * BK, n0 + b_half,
+                                                        fb, b_mask, polB);
+                            else
+                                tma_load_2d_cg2_hint(sB + s * Cfg::B_BYTES, &tmB, kb * BK, n0, fb, polB);
                         }
                         tma_load_2d_cg2_hint(sA + s * Cfg::A_BYTES, &tmA, kb * BK, m0, fb, polA);
                     }
@@ -489,7 +523,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             mma_cg<CG>(d_tmem, ad + uint64_t(2 * k), bd + uint64_t(2 * k), idesc,
                                        (i > 0 || k > 0) ? 1u : 0u);
 #endif
-                        commit_cg<CG>(&empty[s]);  // slot free (in both CTAs) once these MMAs retire
+                        commit_cg<CG>(&empty[s], empty_mask);  // slot free (in both CTAs) once these MMAs retire
                     }
                     __syncwarp();
                     if (++s == STAGES) {
@@ -497,7 +531,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         ph ^= 1;
                     }
                 }
-                if (elect_one()) commit_cg<CG>(&tfull[acc]);  // accumulator ready for both CTAs' epilogues
+                if (elect_one()) commit_cg<CG>(&tfull[acc], pair_mask);  // accumulator ready for both CTAs' epilogues
                 __syncwarp();
 #ifdef SS_GEMM_TRACE
                 if (seg_no < 4 && lane == 0) TRACE(3 + seg_no);
@@ -515,7 +549,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // the tile's 32-column chunks (pairs for SwiGLU) between them
         const int q = warp & 3;
         const int ew = warp - 2, half = ew >> 2;
-        const uint32_t tempty_leader = CG == 2 ? peer_addr(tempty, 0) : 0;
+        const uint32_t tempty_leader = CG == 2 ? peer_addr(tempty, lead_rank) : 0;
         const int rloc = 128 * int(rank) + q * 32 + lane;  // row within the group's tile
         // Stores leave through a per-warp 4 KB staging buffer: the accumulator arrives
         // one row per thread (tcgen05.ld 32x32b), is written to smem as 32 rows x 128 B
@@ -970,13 +1004,13 @@ struct DevOnce {
     int resident[kMaxDevices] = {};
 };
 
-template <int CG, int BN, int EPI, int AR = 128>
+template <int CG, int BN, int EPI, int AR = 128, int MC = 1>
 cudaError_t launch_t(const GemmPlan& p, cudaStream_t st) {
     using Cfg = GemmCfg<CG, BN, AR>;
     static DevOnce once;
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
-    auto kern = gemm_tcgen05_kernel<CG, BN, EPI, AR>;
+    auto kern = gemm_tcgen05_kernel<CG, BN, EPI, AR, MC>;
     if (!once.attr[dev]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
         if (e != cudaSuccess) return e;
@@ -992,7 +1026,7 @@ cudaError_t launch_t(const GemmPlan& p, cudaStream_t st) {
     cfg.stream = st;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.x = CG * MC;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1000,16 +1034,18 @@ cudaError_t launch_t(const GemmPlan& p, cudaStream_t st) {
     cfg.attrs = attr;
     cfg.numAttrs = 2;
     // Groups that can be co-resident: stream-K heads spin on other groups, so the
-    // grid must never exceed one resident wave.
+    // grid must never exceed one resident wave. (MC = 2: whole clusters of two pairs.)
     if (once.resident[dev] == 0) {
-        cfg.gridDim = dim3(CG * (p.num_sms / CG));
+        const int cs = CG * MC;
+        cfg.gridDim = dim3(cs * (p.num_sms / cs));
         int n = 0, r;
-        if (CG > 1 && cudaOccupancyMaxActiveClusters(&n, kern, &cfg) == cudaSuccess && n > 0) r = n;
-        else r = p.num_sms / CG;
+        if (CG > 1 && cudaOccupancyMaxActiveClusters(&n, kern, &cfg) == cudaSuccess && n > 0) r = n * MC;
+        else r = (p.num_sms / cs) * MC;
         once.resident[dev] = r > p.num_sms / CG ? p.num_sms / CG : r;
     }
     int resident = once.resident[dev];
     if (p.max_groups > 0 && p.max_groups < resident) resident = p.max_groups;
+    if (MC == 2) resident &= ~1;
     int mode = p.sk_mode, S = p.splits < 1 ? 1 : p.splits;
     if (mode < 0) mode = S > 1 ? 2 : 0;
     if (p.force_sk >= 0) mode = p.force_sk;
@@ -1027,10 +1063,13 @@ cudaError_t launch_t(const GemmPlan& p, cudaStream_t st) {
         if (gs > long(num_n) * ((p.K + BK - 1) / BK)) gs = long(num_n) * ((p.K + BK - 1) / BK);
         groups = int(gs) * num_mt;
     }
+    // MC = 2 needs both pairs of a cluster on identical weight k-block sequences: whole
+    // tiles or M-lockstep stream-K over an even M-tile count, an even number of pairs
+    if (MC == 2 && ((mode != 0 && mode != 3) || (num_mt & 1) || (groups & 1))) return cudaErrorInvalidConfiguration;
     cfg.gridDim = dim3(CG * groups);
     if (p.debug)
-        fprintf(stderr, "gemm cg=%d bn=%d epi=%d M=%d N=%d K=%d tiles=%d resident=%d mode=%d groups=%d\n", CG, BN,
-                EPI, p.M, p.N, p.K, tiles, resident, mode, groups);
+        fprintf(stderr, "gemm cg=%d bn=%d mc=%d epi=%d M=%d N=%d K=%d tiles=%d resident=%d mode=%d groups=%d\n", CG,
+                BN, MC, EPI, p.M, p.N, p.K, tiles, resident, mode, groups);
     return cudaLaunchKernelEx(&cfg, kern, p.tmA, p.tmB, p.M, p.row0, p.N, p.K, p.out, p.ldo, num_mt, tiles, p.part,
                               p.flags, p.epoch, mode, S, p.ea);
 }
@@ -1644,6 +1683,7 @@ Tuning tuning_from_env() {
     if (getenv("SS_CHAIN_DEBUG")) t.chain_debug = 1;
     geti("SS_CHAIN_TRACE", t.chain_trace);
     geti("SS_GEMM_MAXG", t.gemm_max_groups);
+    geti("SS_GEMM_MC", t.gemm_mc);
     static const char* names[5] = {"SS_GEMM_QKV", "SS_GEMM_O", "SS_GEMM_GATEUP", "SS_GEMM_DOWN", "SS_GEMM_LMHEAD"};
     for (int i = 0; i < 5; ++i)
         if (const char* f = getenv(names[i])) {
@@ -1735,6 +1775,12 @@ GemmShape gemm_pick(int M, int N, int K, int epi, int num_sms, const Tuning& tu)
     return best;
 }
 
+int gemm_mc(const GemmShape& s, int M, const Tuning& tu) {
+    if (!tu.gemm_mc || s.cg != 2 || (s.mode != 0 && s.mode != 3) || (s.bn != 128 && s.bn != 256)) return 1;
+    const int num_mt = (M + 255) / 256;
+    return num_mt % 2 == 0 ? 2 : 1;
+}
+
 bool gemm_prepare(GemmPlan& p, const void* A, uint64_t a_rows, const void* B, int M, int N, int K, void* out,
                   int ldo, int epi, int num_sms, const Tuning& tu, int bn) {
     if (M < 1 || N < 32 || K < 16 || N % 32 || K % 8 || (epi == EPI_SWIGLU && N % 64) || epi == EPI_QKV) return false;
@@ -1755,12 +1801,26 @@ bool gemm_prepare(GemmPlan& p, const void* A, uint64_t a_rows, const void* B, in
     p.splits = s.splits;
     p.sk_mode = s.mode;
     p.ar = (p.cg == 1 && p.bn == s.bn) ? s.ar : 128;
+    p.mc = p.bn == s.bn ? gemm_mc(s, M, tu) : 1;
     if (!make_tmap_2d(&p.tmA, A, a_rows, uint64_t(K), uint32_t(p.ar), BK)) return false;
-    if (!make_tmap_2d(&p.tmB, B, uint64_t(N), uint64_t(K), uint32_t(p.bn / p.cg), BK)) return false;
+    if (!make_tmap_2d(&p.tmB, B, uint64_t(N), uint64_t(K), uint32_t(p.bn / p.cg / p.mc), BK)) return false;
     return true;
 }
 
 cudaError_t gemm_launch(const GemmPlan& p, cudaStream_t st) {
+    if (p.cg == 2 && p.mc == 2) {
+#define SS_GEMM_CASE_MC(BNv)                                                          \
+    if (p.bn == BNv) {                                                               \
+        if (p.epi == EPI_BF16) return launch_t<2, BNv, EPI_BF16, 128, 2>(p, st);     \
+        if (p.epi == EPI_RESADD) return launch_t<2, BNv, EPI_RESADD, 128, 2>(p, st); \
+        if (p.epi == EPI_SWIGLU) return launch_t<2, BNv, EPI_SWIGLU, 128, 2>(p, st); \
+        if (p.epi == EPI_QKV) return launch_t<2, BNv, EPI_QKV, 128, 2>(p, st);       \
+    }
+        SS_GEMM_CASE_MC(128)
+        SS_GEMM_CASE_MC(256)
+#undef SS_GEMM_CASE_MC
+        return cudaErrorInvalidValue;
+    }
 #define SS_GEMM_CASE(CGv, BNv)                                                      \
     if (p.cg == CGv && p.bn == BNv) {                                               \
         if (p.epi == EPI_BF16) return launch_t<CGv, BNv, EPI_BF16>(p, st);          \

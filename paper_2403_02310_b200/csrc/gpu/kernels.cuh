@@ -72,6 +72,8 @@ struct Tuning {
     int chain_debug = 0;      // SS_CHAIN_DEBUG: print each chain launch
     int chain_trace = 0;      // SS_CHAIN_TRACE: record the chain's per-item timeline (ss_debug_chain_trace)
     int gemm_max_groups = 0;  // SS_GEMM_MAXG: at most this many CTA groups per GEMM launch (dev scaling probe)
+    int gemm_mc = 0;          // SS_GEMM_MC=1: weight-tile multicast between the CTA pairs of 4-CTA
+                              // clusters (measured neutral: only 66 such clusters are co-resident)
 };
 Tuning tuning_from_env();
 
@@ -96,6 +98,8 @@ struct GemmPlan {
     int splits = 1;    // K slices per tile for mode 2 (tiles * splits must fit one resident wave)
     int force_sk = -1, force_splits = 0, debug = 0;  // Tuning overrides applied at launch
     int max_groups = 0;  // > 0: at most this many CTA groups (SM budget of a concurrent launch)
+    int mc = 1;          // 2: clusters of two CTA pairs sharing weight tiles by TMA multicast
+                         // (gemm_mc; tmB's box is then bn / cg / 2 rows)
     EpiArgs ea;
 } __attribute__((aligned(64)));
 
@@ -152,6 +156,9 @@ struct GemmShape {
 
 bool make_tmap_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
                   uint32_t box_cols);
+// 2 when the picked shape shares weight tiles between the two M-tile pairs of a cluster by
+// TMA multicast (CTA pairs, whole tiles or M-lockstep stream-K, even M-tile count), else 1.
+int gemm_mc(const GemmShape& s, int M, const Tuning& tu);
 // Tile shape for an M x N GEMM: minimises wave-quantised time over the compiled shapes.
 GemmShape gemm_pick(int M, int N, int K, int epi, int num_sms, const Tuning& tu);
 // A is [a_rows >= M][K] bf16; B is [N][K] bf16; out row stride ldo elements.
