@@ -575,6 +575,23 @@ __global__ void __launch_bounds__(MODE > 0 ? TcCfg<HD, MODE>::THREADS : (kWarps 
     if (p.wait_at_end) {
         pdl_launch_dependents();
     } else {
+        if (key_mode && p.kv_pf_pages > 0) {
+            // The cached pages of this decode item do not depend on the preceding kernels
+            // (only the last page receives this step's K/V, from the QKV epilogue): CTAs that
+            // PDL makes resident while the QKV GEMM still runs (on the SMs its tiles leave
+            // idle) ask L2 for the first pages, using HBM the GEMM leaves idle. The block
+            // table and items were uploaded before the forward's first kernel.
+            const int32_t* bt = p.block_table + size_t(it.entry) * p.max_blocks;
+            const int pg0 = it.key0 >> 4;
+            const int npg = min(p.kv_pf_pages, ((it.key1 - 1) >> 4) - pg0);
+            const uint32_t page_bytes = uint32_t(p.block_size) * HD * 2;
+            for (int i = threadIdx.x; i < 2 * npg; i += blockDim.x) {
+                const int32_t blk = __ldg(bt + pg0 + (i >> 1));
+                const __nv_bfloat16* src =
+                    ((i & 1) ? p.vc : p.kc) + (size_t(blk) * p.nkv_l + it.kv_head) * size_t(p.block_size) * HD;
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(page_bytes) : "memory");
+            }
+        }
         pdl_wait();  // q / KV of this layer come from the preceding kernels
         pdl_launch_dependents();
     }

@@ -715,6 +715,7 @@ AttnParams attn_params(const ss_ctx* ctx, const ss_batch* b, const bf16* q, bf16
     p.num_sms = ctx->num_sms;
     p.kv_hint = ctx->tu.attn_l2hint;
     p.tc2_first = ctx->tu.attn_tc2_first;
+    p.kv_pf_pages = ctx->tu.attn_pf_pages;
     p.part_o = ctx->part_o;
     p.part_ml = ctx->part_ml;
     p.comb_count = ctx->comb_count;

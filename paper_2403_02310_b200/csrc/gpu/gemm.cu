@@ -1669,6 +1669,7 @@ Tuning tuning_from_env() {
     geti("SS_ATTN_ORDER", t.attn_order);
     geti("SS_ATTN_L2HINT", t.attn_l2hint);
     geti("SS_ATTN_TC2_FIRST", t.attn_tc2_first);
+    geti("SS_ATTN_PF_PAGES", t.attn_pf_pages);
     geti("SS_GEMM_L2HINT", t.gemm_l2hint);
     geti("SS_GEMM_SK", t.gemm_sk);
     geti("SS_GEMM_SPLITS", t.gemm_splits);

@@ -57,6 +57,7 @@ struct Tuning {
     int attn_order = 0;       // SS_ATTN_ORDER=1: prefill row tiles first in the work list
     int attn_l2hint = 1;      // SS_ATTN_L2HINT: K/V L2 priority bits (AttnParams::kv_hint)
     int attn_tc2_first = 0;   // SS_ATTN_TC2_FIRST: compact prefill launch before the decodes
+    int attn_pf_pages = 0;    // SS_ATTN_PF_PAGES: AttnParams::kv_pf_pages
     int gemm_l2hint = 3;      // SS_GEMM_L2HINT: operand L2 priority bits (EpiArgs::l2hint)
     int gemm_sk = -1;         // SS_GEMM_SK: force the schedule mode
     int gemm_splits = 0;      // SS_GEMM_SPLITS: force the split count
@@ -216,6 +217,8 @@ struct AttnParams {
     int32_t num_sms;
     int32_t kv_hint;             // L2 priority bits: 1 decode K/V evict-first, 2 prefill K/V evict-last
     int32_t tc2_first;           // Tuning::attn_tc2_first
+    int32_t kv_pf_pages;         // decode items: cached K/V pages each CTA asks L2 for before its grid-
+                                 // dependency wait (the CTAs PDL lands on SMs the QKV GEMM leaves idle)
 };
 // 2D TMA views [L * nblocks * nkv * 16][hd] of the K and V pools (box 16 x 64, SWIZZLE_128B).
 bool attention_tmaps(CUtensorMap* tk, CUtensorMap* tv, const void* kc, const void* vc, int64_t total_rows, int hd);
