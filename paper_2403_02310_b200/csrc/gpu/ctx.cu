@@ -222,7 +222,7 @@ struct ss_ctx {
     // counters and K-split partials, sized for T_cap
     uint32_t* chain_flags = nullptr;
     float* chain_part = nullptr;
-    size_t chain_flag_cap = 0, chain_part_cap = 0;
+    size_t chain_flag_cap = 0, chain_part_cap = 0;  // flag buffer: max tiles per phase (stride)
     unsigned long long* chain_trace = nullptr;  // SS_CHAIN_TRACE: [L][kChainTraceItems][8] timeline
     CUtensorMap tm_k, tm_v;  // 2D TMA views of the paged K/V pools
 
@@ -367,31 +367,44 @@ bool bmaps(WMaps& m, const bf16* w, int64_t rows, int64_t cols) {
 // The fused projection chain of a layer (TP = 1, more than one 128-row tile of tokens):
 // O, gate/up, down, and the next layer's QKV as one persistent launch (gemm.cu).
 bool chain_enabled(const ss_ctx* ctx, int T) {
-    return ctx->tu.chain && ctx->tp == 1 && !ctx->grp && T > 128 && ctx->h % 256 == 0 && ctx->fuse_rope;
+    // Tuning::chain bits: 1 CTA-pair chain (T > 128), 2 single-CTA weight-streaming chain (T <= 128)
+    const int bit = T > 128 ? 1 : 2;
+    return (ctx->tu.chain & bit) && ctx->tp == 1 && !ctx->grp && ctx->h % 256 == 0 && ctx->fuse_rope;
 }
 struct ChainDims {
-    int n = 4, num_mt = 0;
+    int n = 4, num_mt = 0, cg = 2, ar = 128;
     int N[4], K[4], S[4];
 };
-// K splits: about 64 k-blocks (a K = 4096 tile) per split, so every phase's tiles are
-// comparable work units (down at K = 14336: 4 splits); SS_CHAIN_S overrides.
+// Tiles: CTA pairs (256 rows) above 128 tokens, else single CTAs (128 rows; 32-row A stages
+// up to 32 tokens). K splits: CTA pairs take about 64 k-blocks (a K = 4096 tile) per split,
+// so the phases' tiles are comparable work units (down at K = 14336: 4 splits); single CTAs
+// (weight streaming) split each phase over about one item per SM, at least 8 k-blocks each.
+// SS_CHAIN_S overrides.
 ChainDims chain_dims(const ss_ctx* ctx, int T) {
     ChainDims d;
-    d.num_mt = (T + 255) / 256;
+    d.cg = T > 128 ? 2 : 1;
+    d.ar = d.cg == 1 && T <= 32 ? 32 : 128;
+    d.num_mt = (T + 128 * d.cg - 1) / (128 * d.cg);
     const int qd = ctx->nq_l * ctx->hd, qkvN = (ctx->nq_l + 2 * ctx->nkv_l) * ctx->hd;
     const int N[4] = {ctx->h, 2 * ctx->ffn_l, ctx->h, qkvN}, K[4] = {qd, ctx->h, ctx->ffn_l, ctx->h};
     for (int p = 0; p < 4; ++p) {
         d.N[p] = N[p];
         d.K[p] = K[p];
         const int nkb = (K[p] + 63) / 64;
-        d.S[p] = ctx->tu.chain_splits[p] > 0 ? ctx->tu.chain_splits[p] : std::max(1, (nkb + 32) / 64);
+        const int tiles = d.num_mt * ((N[p] + 255) / 256);
+        const int auto_s = d.cg == 2 ? std::max(1, (nkb + 32) / 64)
+                                     : std::max(1, std::min(nkb / 8, (ctx->num_sms + tiles - 1) / tiles));
+        d.S[p] = ctx->tu.chain_splits[p] > 0 ? ctx->tu.chain_splits[p] : auto_s;
     }
     return d;
 }
-size_t chain_flag_words(const ChainDims& d) {
-    size_t w = 0;
-    for (int p = 0; p < d.n; ++p) w += size_t(d.num_mt) * ((d.N[p] + 255) / 256) * 18;
-    return w;
+// Largest tile count of any phase. The flag buffer is laid out with this fixed stride —
+// ready flags [4][maxt] | warp counters [4][maxt] | split counters [4][maxt][16] — so a slot is
+// always the same kind (epoch flag or self-resetting counter) whatever the batch shape.
+size_t chain_max_tiles(const ChainDims& d) {
+    size_t t = 0;
+    for (int p = 0; p < d.n; ++p) t = std::max(t, size_t(d.num_mt) * ((d.N[p] + 255) / 256));
+    return t;
 }
 size_t chain_part_floats(const ChainDims& d) {
     size_t f = 0;
@@ -470,15 +483,16 @@ ss_status ensure_workspace(ss_ctx* ctx, int T, int n_out, int part_rows) {
         ctx->P_cap = cap;
         ++ctx->ws_gen;
     }
-    if (chain_enabled(ctx, T)) {  // sized for T_cap: flags must start zeroed (counters self-reset)
-        const ChainDims d = chain_dims(ctx, ctx->T_cap);
-        const size_t fw = chain_flag_words(d), pf = chain_part_floats(d);
-        if (fw > ctx->chain_flag_cap) {
+    if (chain_enabled(ctx, T)) {  // flags must start zeroed (counters self-reset)
+        const ChainDims d = chain_dims(ctx, T), dc = chain_dims(ctx, ctx->T_cap);
+        const size_t maxt = std::max(chain_max_tiles(d), chain_max_tiles(dc));
+        const size_t pf = std::max(chain_part_floats(d), chain_part_floats(dc));
+        if (maxt > ctx->chain_flag_cap) {
             cudaFree(ctx->chain_flags);
             ctx->chain_flags = nullptr;
-            CK(cudaMalloc(&ctx->chain_flags, fw * 4));
-            CK(cudaMemsetAsync(ctx->chain_flags, 0, fw * 4, ctx->st));
-            ctx->chain_flag_cap = fw;
+            CK(cudaMalloc(&ctx->chain_flags, maxt * 4 * 18 * 4));
+            CK(cudaMemsetAsync(ctx->chain_flags, 0, maxt * 4 * 18 * 4, ctx->st));
+            ctx->chain_flag_cap = maxt;
             ++ctx->ws_gen;
         }
         if (pf > ctx->chain_part_cap) {
@@ -895,6 +909,8 @@ ss_status chain_launch(ss_ctx* ctx, const ss_batch* b, int l) {
     Layer& W = ctx->layers[size_t(l)];
     const int np = l + 1 < ctx->L ? 4 : 3;
     ChainPlan p;
+    p.cg = d.cg;
+    p.ar = d.ar;
     p.n_phases = np;
     p.M = T;
     p.num_mt = d.num_mt;
@@ -918,18 +934,19 @@ ss_status chain_launch(ss_ctx* ctx, const ss_batch* b, int l) {
         int ldo;
         EpiArgs ea;
     };
+    const bool a32 = d.ar == 32;  // the activation maps with 32-row boxes
     const Src src[4] = {
-        {&ctx->ta_o, &W.tb_o, EPI_RESADD, -1, -1, 256, ctx->x, h, res_out},
-        {&ctx->ta_xb, &W.tb_gu, EPI_SWIGLU, 0, -1, 128, ctx->act, ctx->ffn_l, norm_in},
-        {&ctx->ta_act, &W.tb_down, EPI_RESADD, 1, 0, 256, ctx->x, h, res_out},
-        {&ctx->ta_xb, np == 4 ? &ctx->layers[size_t(l) + 1].tb_qkv : nullptr, EPI_QKV, 2, -1, 256, nullptr,
-         d.N[3], np == 4 ? qkv_args(ctx, b, l + 1) : EpiArgs()},
+        {a32 ? &ctx->ta32_o : &ctx->ta_o, &W.tb_o, EPI_RESADD, -1, -1, 256, ctx->x, h, res_out},
+        {a32 ? &ctx->ta32_xb : &ctx->ta_xb, &W.tb_gu, EPI_SWIGLU, 0, -1, 128, ctx->act, ctx->ffn_l, norm_in},
+        {a32 ? &ctx->ta32_act : &ctx->ta_act, &W.tb_down, EPI_RESADD, 1, 0, 256, ctx->x, h, res_out},
+        {a32 ? &ctx->ta32_xb : &ctx->ta_xb, np == 4 ? &ctx->layers[size_t(l) + 1].tb_qkv : nullptr, EPI_QKV, 2, -1,
+         256, nullptr, d.N[3], np == 4 ? qkv_args(ctx, b, l + 1) : EpiArgs()},
     };
-    uint32_t* fl = ctx->chain_flags;
+    const size_t maxt = ctx->chain_flag_cap;  // fixed stride of the flag buffer (chain_max_tiles)
     float* pt = ctx->chain_part;
     for (int i = 0; i < np; ++i) {
         ChainPhase& ph = p.ph[i];
-        const CUtensorMap* mb = src[i].b->get(128);
+        const CUtensorMap* mb = src[i].b->get(256 / d.cg);
         if (!mb) return fail(ctx, SS_CUDA_ERROR, "cuTensorMapEncodeTiled failed (weight tile map)");
         p.tmA[i] = *src[i].a;
         p.tmB[i] = *mb;
@@ -944,10 +961,10 @@ ss_status chain_launch(ss_ctx* ctx, const ss_batch* b, int l) {
         ph.ldo = src[i].ldo;
         ph.ea = src[i].ea;
         const size_t tiles = size_t(d.num_mt) * ((d.N[i] + 255) / 256);
-        ph.ready = fl;
-        ph.rcnt = fl + tiles;
-        ph.pcnt = fl + 2 * tiles;
-        fl += 18 * tiles;
+        if (tiles > maxt) return fail(ctx, SS_CUDA_ERROR, "chain flag buffer smaller than the batch's tiles");
+        ph.ready = ctx->chain_flags + i * maxt;
+        ph.rcnt = ctx->chain_flags + (4 + i) * maxt;
+        ph.pcnt = ctx->chain_flags + 8 * maxt + i * maxt * 16;
         if (d.S[i] > 1) {
             ph.part = pt;
             pt += tiles * d.S[i] * 65536;

@@ -1093,18 +1093,23 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
+// Pollers back off exponentially (64 ns .. 1 us): thousands of threads polling the few lines
+// that hold a phase's flags would saturate their L2 slice and slow every epilogue whose
+// stores land there.
 __device__ __forceinline__ void spin_flag(const uint32_t* f, uint32_t want) {
     if (ld_acquire_gpu(f) == want) return;
     const uint64_t t0 = globaltimer_ns();
-    uint32_t spins = 0;
+    uint32_t ns = 64;
     while (ld_acquire_gpu(f) != want) {  // a schedule bug traps after 2 s instead of hanging the GPU
-        if ((++spins & 1023u) == 0 && globaltimer_ns() - t0 > 2000000000ull) __trap();
+        __nanosleep(ns);
+        if (ns < 1024) ns *= 2;
+        if (globaltimer_ns() - t0 > 2000000000ull) __trap();
     }
 }
-// Lane-parallel wait on n flags (n <= 32 per step), then a warp-wide acquire point.
+// Wait on n flags (one polling lane), then a warp-wide acquire point.
 __device__ __forceinline__ void warp_wait_flags(const uint32_t* f, int n, uint32_t want, int lane) {
-    for (int i = lane; i - lane < n; i += 32)
-        if (i < n) spin_flag(f + i, want);
+    if (lane == 0)
+        for (int i = 0; i < n; ++i) spin_flag(f + i, want);
     __syncwarp();
     __threadfence();
 }
@@ -1112,6 +1117,18 @@ __device__ __forceinline__ void warp_wait_flags(const uint32_t* f, int n, uint32
 struct ChainItem {
     int p, m, n, s, kb0, kb1;
 };
+// The k-th (0..3) of the four 32-column chunks an epilogue warp owns in a 256-column tile, the
+// same set the store epilogues walk: RESADD / BF16 every second chunk from `half`; SwiGLU
+// gate/up pairs (c, c + 1); QKV rotate-half pairs (c, c + hd / 64). A K-split warp publishes and
+// later reduces exactly these chunks.
+__device__ __forceinline__ int warp_chunk(int epi, int hd, int half, int k) {
+    if (epi == EPI_SWIGLU) return 2 * half + 4 * (k >> 1) + (k & 1);
+    if (epi == EPI_QKV) {
+        const int ps = hd / 64, pi = half + 2 * (k >> 1), c = (pi / ps) * (2 * ps) + (pi % ps);
+        return (k & 1) ? c + ps : c;
+    }
+    return half + 2 * k;
+}
 __device__ __forceinline__ ChainItem chain_item(const ChainPlan& P, int i) {
     int p = 0;
     while (p + 1 < P.n_phases && i >= P.ph[p + 1].item0) ++p;
@@ -1134,9 +1151,12 @@ __device__ __forceinline__ ChainItem chain_item(const ChainPlan& P, int i) {
 // K splits never wait on each other (the last arriver reduces). The lowest unfinished item
 // therefore always has its inputs and its pair free to run it. All pairs are co-resident
 // (the grid is one resident wave, checked at launch).
+// CG = 2: CTA pairs, 256 x 256 tiles (M > 128). CG = 1: single CTAs, 128 x 256 tiles whose A
+// stages hold AR rows (decode-sized batches: the projections stream weights, one CTA per SM).
+template <int CG, int AR>
 __global__ void __launch_bounds__(kThreads, 1) gemm_chain_kernel(const __grid_constant__ ChainPlan P) {
-    constexpr int CG = 2, BN = 256;
-    using Cfg = GemmCfg<CG, BN, 128>;
+    constexpr int BN = 256;
+    using Cfg = GemmCfg<CG, BN, AR>;
     constexpr int STAGES = Cfg::STAGES;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
@@ -1151,10 +1171,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_chain_kernel(const __grid_co
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
-    const uint32_t rank = cluster_rank();
+    const uint32_t rank = CG == 2 ? cluster_rank() : 0;
     const bool leader = rank == 0;
     const int gid = blockIdx.x / CG, G = gridDim.x / CG;
     const int M = P.M, num_mt = P.num_mt, total = P.total_items;
+    constexpr uint32_t kStageTx = CG * Cfg::STAGE_BYTES;  // bytes a stage's full barrier expects
 
     if (threadIdx.x == 0) {
         for (int p = 0; p < P.n_phases; ++p) {
@@ -1173,13 +1194,28 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_chain_kernel(const __grid_co
     }
     if (warp == 1) tmem_alloc_cg<CG>(tmem_slot, Cfg::TMEM_COLS);
     tc_fence_before();
-    cluster_sync();
+    if constexpr (CG == 2) cluster_sync();
+    else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     pdl_launch_dependents();
 
+    // one stage's B (weights) / A (activations) tile, completing on the (pair leader's) full barrier
+    auto load_b = [&](int st, const CUtensorMap* tB, int kb, int n0, uint32_t full_leader, uint64_t pol) {
+        if constexpr (CG == 1)
+            tma_load_2d_hint(sB + st * Cfg::B_BYTES, tB, kb * BK, n0, &full[st], pol);
+        else
+            tma_load_2d_cg2_hint(sB + st * Cfg::B_BYTES, tB, kb * BK, n0, full_leader + uint32_t(st * 8), pol);
+    };
+    auto load_a = [&](int st, const CUtensorMap* tA, int kb, int m0, uint32_t full_leader, uint64_t pol) {
+        if constexpr (CG == 1)
+            tma_load_2d_hint(sA + st * Cfg::A_BYTES, tA, kb * BK, m0, &full[st], pol);
+        else
+            tma_load_2d_cg2_hint(sA + st * Cfg::A_BYTES, tA, kb * BK, m0, full_leader + uint32_t(st * 8), pol);
+    };
+
     if (warp == 0) {  // ---------------- TMA producer (both CTAs; lane 0 issues, the warp checks flags)
-        const uint32_t full_leader = peer_addr(full, 0);
+        const uint32_t full_leader = CG == 2 ? peer_addr(full, 0) : 0;
         const uint64_t polA = l2_policy_evict_last();
         const uint64_t polB = l2_policy_evict_first();
         // the first item's first weight stages before the grid-dependency wait
@@ -1190,9 +1226,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_chain_kernel(const __grid_co
             npre = it.kb1 - it.kb0 < STAGES ? it.kb1 - it.kb0 : STAGES;
             if (lane == 0)
                 for (int j = 0; j < npre; ++j) {
-                    if (leader) mbar_arrive_expect_tx(&full[j], 2 * Cfg::STAGE_BYTES);
-                    tma_load_2d_cg2_hint(sB + j * Cfg::B_BYTES, &P.tmB[it.p], (it.kb0 + j) * BK, n0,
-                                         full_leader + uint32_t(j * 8), polB);
+                    if (leader) mbar_arrive_expect_tx(&full[j], kStageTx);
+                    load_b(j, &P.tmB[it.p], it.kb0 + j, n0, full_leader, polB);
                 }
         }
         pdl_wait();
@@ -1221,6 +1256,16 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_chain_kernel(const __grid_co
             const bool cache = num_mt <= 32;
             int known = cache ? __shfl_sync(0xffffffffu, kr, it.m & 31) : -1;
             for (int kb = it.kb0; kb < it.kb1; ++kb, ++itn) {
+                // the stage's weight tile first: it depends on nothing, so weight streaming
+                // runs ahead of the activations' readiness
+                if (lane == 0) {
+                    const bool pre = itn < npre;
+                    if (!pre) {
+                        mbar_wait(&empty[s], ph ^ 1);
+                        if (leader) mbar_arrive_expect_tx(&full[s], kStageTx);
+                        load_b(s, tB, kb, n0, full_leader, polB);
+                    }
+                }
                 if (rdy) {  // the producing phase's output tile covering these 64 columns
                     const int ct = kb * BK / dcols;
                     if (ct > known) {
@@ -1240,16 +1285,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_chain_kernel(const __grid_co
                         if (lane == 0) fence_proxy_async_global();
                     }
                 }
-                if (lane == 0) {
-                    const bool pre = itn < npre;
-                    if (!pre) mbar_wait(&empty[s], ph ^ 1);
-                    const uint32_t fb = full_leader + uint32_t(s * 8);
-                    if (!pre) {
-                        if (leader) mbar_arrive_expect_tx(&full[s], 2 * Cfg::STAGE_BYTES);
-                        tma_load_2d_cg2_hint(sB + s * Cfg::B_BYTES, tB, kb * BK, n0, fb, polB);
-                    }
-                    tma_load_2d_cg2_hint(sA + s * Cfg::A_BYTES, tA, kb * BK, m0, fb, polA);
-                }
+                if (lane == 0) load_a(s, tA, kb, m0, full_leader, polA);
                 __syncwarp();
                 if (++s == STAGES) {
                     s = 0;
@@ -1302,7 +1338,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_chain_kernel(const __grid_co
         const uint32_t E = P.epoch + (P.epoch_base ? *reinterpret_cast<const volatile uint32_t*>(P.epoch_base) : 0u);
         const int q = warp & 3;
         const int ew = warp - 2, half = ew >> 2;
-        const uint32_t tempty_leader = peer_addr(tempty, 0);
+        const uint32_t tempty_leader = CG == 2 ? peer_addr(tempty, 0) : smem_u32(tempty);
+        const int trace_ew = M <= 32 ? 2 : 0;  // dev timeline: a warp whose rows hold tokens
         const int rloc = 128 * int(rank) + q * 32 + lane;
         uint4* ep = reinterpret_cast<uint4*>(smem + STAGES * Cfg::STAGE_BYTES + 1024 + ew * 4096);
         const int crow = lane >> 3, cch = lane & 7;
@@ -1325,6 +1362,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_chain_kernel(const __grid_co
             const int tile = it.m * cp.num_n + it.n;
             const int m0 = it.m * Cfg::TILE_M, n0 = it.n * BN;
             const int row = m0 + rloc, rbase = row - lane;
+            const bool live = rbase < M;  // warp-uniform: this warp's 32 rows hold tokens
             // inputs written by earlier items: acquire their tiles' flags, then read coherently
             if (ea.ssq_in && cp.dep >= 0)
                 warp_wait_flags(P.ph[cp.dep].ready + size_t(it.m) * P.ph[cp.dep].num_n, P.ph[cp.dep].num_n, E, lane);
@@ -1366,15 +1404,16 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_chain_kernel(const __grid_co
             }
             mbar_wait(&tfull[acc], acc_ph);
             tc_fence_after();
-            if (P.trace && leader && ew == 0 && lane == 0) P.trace[size_t(i) * 16 + 4] = globaltimer_ns();
+            if (P.trace && leader && ew == trace_ew && lane == 0) P.trace[size_t(i) * 16 + 4] = globaltimer_ns();
             const uint32_t t_row = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN);
             bool from_part = false;
             if (S > 1) {
                 // publish this split's partial (staged swizzled image, copied out coalesced)
-                uint4* dst = reinterpret_cast<uint4*>(cp.part + (((size_t(tile) * S + it.s) * 2 + rank) * 8) * 4096 +
+                uint4* dst = reinterpret_cast<uint4*>(cp.part + (((size_t(tile) * S + it.s) * CG + rank) * 8) * 4096 +
                                                       (q * 32) * 32);
 #pragma unroll 1
-                for (int c = half; c < BN / 32; c += 2) {
+                for (int k = 0; k < BN / 64 && live; ++k) {
+                    const int c = warp_chunk(EPI, ea.hd, half, k);
                     uint32_t v[32];
                     tmem_ld32(t_row + uint32_t(c * 32), v);
                     tmem_wait_ld();
@@ -1388,6 +1427,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_chain_kernel(const __grid_co
                 release_acc();
                 __threadfence();
                 __syncwarp();
+                if (P.trace && leader && ew == trace_ew && lane == 0) P.trace[size_t(i) * 16 + 12] = globaltimer_ns();
                 uint32_t old = 0;
                 if (lane == 0) old = atom_add_acqrel_gpu(&cp.pcnt[(size_t(tile) * 2 + rank) * 8 + ew], 1u);
                 old = __shfl_sync(0xffffffffu, old, 0);
@@ -1407,9 +1447,29 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_chain_kernel(const __grid_co
                 }
 #pragma unroll
                 for (int j = 0; j < 32; ++j) v[j] = 0u;
+                if (CG == 1 && M <= 32) {
+                    // only row quarter 0 holds tokens: the idle warps' staging buffers of this
+                    // half (4 x 4 KB, contiguous) take four splits' chunks per round trip
+                    uint4* stg4 = reinterpret_cast<uint4*>(smem + STAGES * Cfg::STAGE_BYTES + 1024 + (4 * half) * 4096);
+                    for (int sp0 = 0; sp0 < S; sp0 += 4) {
+                        const int n = S - sp0 < 4 ? S - sp0 : 4;
+                        for (int i = 0; i < n; ++i) {
+                            const uint4* src = reinterpret_cast<const uint4*>(
+                                cp.part + (((size_t(tile) * S + sp0 + i) * CG + rank) * 8) * 4096 + (size_t(c) * 128 + q * 32) * 32);
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) cp_async16(smem_u32(stg4 + i * 256 + j * 32 + lane), src + j * 32 + lane);
+                        }
+                        cp_async_commit();
+                        cp_async_wait<0>();
+                        __syncwarp();
+                        for (int i = 0; i < n; ++i) add_rows(v, stg4 + i * 256, lane);  // split order
+                        __syncwarp();
+                    }
+                    return;
+                }
                 for (int sp = 0; sp < S; ++sp) {  // added in split order (deterministic)
                     const uint4* src = reinterpret_cast<const uint4*>(
-                        cp.part + (((size_t(tile) * S + sp) * 2 + rank) * 8) * 4096 + (size_t(c) * 128 + q * 32) * 32);
+                        cp.part + (((size_t(tile) * S + sp) * CG + rank) * 8) * 4096 + (size_t(c) * 128 + q * 32) * 32);
                     // global -> smem without a register round trip (8 x 16 B in flight per lane)
 #pragma unroll
                     for (int j = 0; j < 8; ++j) cp_async16(smem_u32(ep + j * 32 + lane), src + j * 32 + lane);
@@ -1420,7 +1480,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_chain_kernel(const __grid_co
                     __syncwarp();
                 }
             };
-            if (EPI == EPI_QKV) {
+            if (!live) {
+                // no token rows in this warp's quarter of the tile: nothing to store
+            } else if (EPI == EPI_QKV) {
                 const int ps = ea.hd / 64;
                 const int64_t blk = q_slot / ea.bs, off = q_slot % ea.bs;
 #pragma unroll 1
@@ -1577,10 +1639,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_chain_kernel(const __grid_co
                         }
                     }
                     __syncwarp();
-                    if (P.trace && leader && ew == 0 && lane == 0) P.trace[size_t(i) * 16 + 6 + ci] = globaltimer_ns();
+                    if (P.trace && leader && ew == trace_ew && lane == 0) P.trace[size_t(i) * 16 + 6 + ci] = globaltimer_ns();
                 }
             }
-            if (P.trace && leader && ew == 0 && lane == 0) P.trace[size_t(i) * 16 + 14] = globaltimer_ns();
+            if (P.trace && leader && ew == trace_ew && lane == 0) P.trace[size_t(i) * 16 + 14] = globaltimer_ns();
             if (!from_part) release_acc();
             // this warp's share of the tile is stored: count it; the 16th warp publishes the tile
             fence_proxy_async_global();  // consumers read these stores through TMA (async proxy)
@@ -1588,8 +1650,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_chain_kernel(const __grid_co
             __syncwarp();
             if (lane == 0) {
                 const uint32_t old = atom_add_acqrel_gpu(&cp.rcnt[tile], 1u);
-                if (P.trace && leader && ew == 0) P.trace[size_t(i) * 16 + 15] = globaltimer_ns();
-                if (old == 2u * 8u - 1u) {
+                if (P.trace && leader && ew == trace_ew) P.trace[size_t(i) * 16 + 15] = globaltimer_ns();
+                if (old == uint32_t(CG) * 8u - 1u) {
                     cp.rcnt[tile] = 0u;
                     st_release_gpu(&cp.ready[tile], E);
                     if (P.trace) P.trace[size_t(i) * 16 + 5] = globaltimer_ns();
@@ -1598,7 +1660,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_chain_kernel(const __grid_co
         }
     }
     tc_fence_before();
-    cluster_sync();
+    if constexpr (CG == 2) cluster_sync();
+    else __syncthreads();
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc_cg<CG>(tmem_base, Cfg::TMEM_COLS);
@@ -1618,13 +1681,16 @@ void gemm_chain_finalize(ChainPlan& p) {
     p.total_items = item;
 }
 
-cudaError_t gemm_chain_launch(const ChainPlan& p, cudaStream_t st) {
-    using Cfg = GemmCfg<2, 256, 128>;
+namespace {
+template <int CG, int AR>
+cudaError_t chain_launch_t(const ChainPlan& p, cudaStream_t st) {
+    using Cfg = GemmCfg<CG, 256, AR>;
     static DevOnce once;
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+    auto kern = gemm_chain_kernel<CG, AR>;
     if (!once.attr[dev]) {
-        cudaError_t e = cudaFuncSetAttribute(gemm_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
         if (e != cudaSuccess) return e;
         once.attr[dev] = true;
     }
@@ -1634,27 +1700,36 @@ cudaError_t gemm_chain_launch(const ChainPlan& p, cudaStream_t st) {
     cfg.stream = st;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.x = CG;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    // every pair must be resident at once (flag waits between pairs)
+    // every group must be resident at once (flag waits between groups)
     if (once.resident[dev] == 0) {
-        cfg.gridDim = dim3(2 * (p.num_sms / 2));
+        cfg.gridDim = dim3(CG * (p.num_sms / CG));
         int n = 0;
-        if (cudaOccupancyMaxActiveClusters(&n, gemm_chain_kernel, &cfg) != cudaSuccess || n <= 0) n = p.num_sms / 2;
-        once.resident[dev] = n > p.num_sms / 2 ? p.num_sms / 2 : n;
+        if (CG == 1 || cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) n = p.num_sms / CG;
+        once.resident[dev] = n > p.num_sms / CG ? p.num_sms / CG : n;
     }
     int groups = once.resident[dev];
     if (groups > p.total_items) groups = p.total_items;
     if (groups < 1) return cudaSuccess;
-    cfg.gridDim = dim3(2 * groups);
+    cfg.gridDim = dim3(CG * groups);
     if (p.debug)
-        fprintf(stderr, "gemm chain M=%d phases=%d items=%d groups=%d\n", p.M, p.n_phases, p.total_items, groups);
-    return cudaLaunchKernelEx(&cfg, gemm_chain_kernel, p);
+        fprintf(stderr, "gemm chain cg=%d ar=%d M=%d phases=%d items=%d groups=%d\n", CG, AR, p.M, p.n_phases,
+                p.total_items, groups);
+    return cudaLaunchKernelEx(&cfg, kern, p);
+}
+}  // namespace
+
+cudaError_t gemm_chain_launch(const ChainPlan& p, cudaStream_t st) {
+    if (p.cg == 2) return chain_launch_t<2, 128>(p, st);
+    if (p.cg == 1 && p.ar == 32) return chain_launch_t<1, 32>(p, st);
+    if (p.cg == 1) return chain_launch_t<1, 128>(p, st);
+    return cudaErrorInvalidValue;
 }
 
 namespace {

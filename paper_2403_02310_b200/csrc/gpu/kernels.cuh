@@ -67,8 +67,9 @@ struct Tuning {
     int gemm_debug = 0;       // SS_GEMM_DEBUG: print each launch's schedule
     int gemm_force[5][3] = {{-1, 0, 1}, {-1, 0, 1}, {-1, 0, 1}, {-1, 0, 1}, {-1, 0, 1}};  // SS_GEMM_<QKV|O|GATEUP|DOWN|LMHEAD>=mode,bn[,splits]
     int ldo_pad = 0;          // SS_GEMM_LDO_PAD (ss_k_gemm only)
-    int chain = 0;            // SS_CHAIN=1: the fused projection chain instead of separate launches
-                              // (measured slower on the canonical batch)
+    int chain = 0;            // SS_CHAIN bits: the fused projection chain instead of separate launches,
+                              // 1 for batches above 128 tokens (CTA pairs; measured slower on the
+                              // canonical batch), 2 up to 128 (weight streaming)
     int chain_splits[4] = {0, 0, 0, 0};  // SS_CHAIN_S=o,gu,down,qkv: K splits per chain phase (0: auto)
     int chain_debug = 0;      // SS_CHAIN_DEBUG: print each chain launch
     int chain_trace = 0;      // SS_CHAIN_TRACE: record the chain's per-item timeline (ss_debug_chain_trace)
@@ -128,11 +129,13 @@ struct ChainPhase {
     uint32_t* ready = nullptr;  // [num_mt][num_n] tile-done flags (value = launch epoch)
     uint32_t* rcnt = nullptr;   // [num_mt][num_n] epilogue warps done (self-resetting)
     uint32_t* pcnt = nullptr;   // [num_mt][num_n][2][8] split arrivals per epilogue warp (self-resetting)
-    float* part = nullptr;      // [num_mt][num_n][splits][2][8 chunks][128][32] fp32 split partials
+    float* part = nullptr;      // [num_mt][num_n][splits][cg][8 chunks][128][32] fp32 split partials
     EpiArgs ea;
 };
 struct ChainPlan {
-    CUtensorMap tmA[kChainMaxPhases], tmB[kChainMaxPhases];  // A box 128 x 64, B box 128 x 64
+    CUtensorMap tmA[kChainMaxPhases], tmB[kChainMaxPhases];  // A box ar x 64, B box (256 / cg) x 64
+    int cg = 2;   // 2: CTA pairs, 256-row tiles; 1: single CTAs, 128-row tiles (decode-sized M)
+    int ar = 128; // rows of A per stage (32: M <= 32)
     int n_phases = 0, M = 0, num_mt = 0, total_items = 0, num_sms = 148;
     uint32_t epoch = 0;
     const uint32_t* epoch_base = nullptr;

@@ -1,4 +1,4 @@
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-SS_GEMM_DEBUG=1 timeout 120 python scripts/mc_check.py > gpurun_out/mc_check.txt 2>&1
-grep -v "^gemm cg" gpurun_out/mc_check.txt | tail -12
+timeout 60 ./scripts/epi_store_bench > gpurun_out/epi_store_bench.txt 2>&1
+cat gpurun_out/epi_store_bench.txt

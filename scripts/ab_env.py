@@ -1,5 +1,5 @@
 """A/B of dev tuning environment settings on the canonical batch (dev tool).
-  AB='SS_ATTN_PF_PAGES=0;SS_ATTN_PF_PAGES=32' TAU=512 python scripts/ab_env.py
+  AB='SS_ATTN_PF_PAGES=0;SS_ATTN_PF_PAGES=32 SS_GEMM_MC=1' TAU=512 python scripts/ab_env.py
 Each setting gets its own context (the tuning is read at ss_create); settings are timed in
 interleaved rounds (ROUNDS x STEPS back-to-back forwards, CUDA events, graphs on), median."""
 import os
@@ -26,7 +26,7 @@ else:
     d = host.Descriptor.build([host.BatchEntry(i, "decode", 1, 4096) for i in range(NDEC)], vocab=shape.vocab, token_seed=1)
 ctxs = []
 for st in settings:
-    kv = dict(x.split("=") for x in st.split(",") if x)
+    kv = dict(x.split("=", 1) for x in st.split() if x)  # space-separated KEY=VALUE pairs
     old = {k: os.environ.get(k) for k in kv}
     os.environ.update(kv)
     f = gpu.HybridForward(shape, weight_seed=1234)

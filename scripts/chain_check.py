@@ -18,10 +18,17 @@ PREFIX = int(os.environ.get("PREFIX", "0"))
 REPS = int(os.environ.get("REPS", "20"))
 
 
+DECODE = int(os.environ.get("DECODE", "0"))  # > 0: a decode-only batch of DECODE sequences @ 4096
+
+
 def run(chain):
-    os.environ["SS_CHAIN"] = "1" if chain else "0"
+    os.environ["SS_CHAIN"] = ("2" if DECODE else "1") if chain else "0"
     f = gpu.HybridForward(shape, weight_seed=1234)
-    d = host.Descriptor.canonical(TAU, 32, 4096, PREFIX, vocab=shape.vocab, token_seed=1)
+    if DECODE:
+        d = host.Descriptor.build([host.BatchEntry(i, "decode", 1, 4096) for i in range(DECODE)], vocab=shape.vocab,
+                                  token_seed=1)
+    else:
+        d = host.Descriptor.canonical(TAU, 32, 4096, PREFIX, vocab=shape.vocab, token_seed=1)
     f.kv_alloc(d.pool_blocks)
     f.fill_descriptor_prefixes(d, seed=5)
     lg, nt, _ = f.forward(d)
@@ -47,6 +54,6 @@ def run(chain):
 a, a2, ta = run(False)
 c, c2, tc = run(True)
 rel = float(np.linalg.norm(c - a) / np.linalg.norm(a))
-print(f"{MODEL} L={shape.num_layers} tau={TAU} prefix={PREFIX}: separate {ta:.3f} ms, chain {tc:.3f} ms; "
+print(f"{MODEL} L={shape.num_layers} tau={TAU} prefix={PREFIX} decode-only={DECODE}: separate {ta:.3f} ms, chain {tc:.3f} ms; "
       f"rel-L2(chain vs separate) {rel:.2e}, top-1 agree {float((c.argmax(1) == a.argmax(1)).mean()):.3f}, "
       f"chain repeatable {bool((c == c2).all())}, separate repeatable {bool((a == a2).all())}")

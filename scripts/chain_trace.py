@@ -8,6 +8,7 @@ import os
 import sys
 
 os.environ.setdefault("SS_CHAIN_TRACE", "1")
+os.environ.setdefault("SS_CHAIN", "2" if int(os.environ.get("DECODE", "0")) else "1")
 sys.path.insert(0, os.path.abspath(os.path.join(os.path.dirname(__file__), "..")))
 import numpy as np
 
@@ -25,7 +26,13 @@ lib.ss_debug_chain_trace.argtypes = [C.c_void_p, C.c_void_p, C.c_int64]
 
 f = gpu.HybridForward(shape, weight_seed=1234)
 f.set_graphs(False)
-d = host.Descriptor.canonical(TAU, 32, 4096, 0, vocab=shape.vocab, token_seed=1)
+DECODE = int(os.environ.get("DECODE", "0"))  # > 0: decode-only batch (the single-CTA weight-streaming chain)
+if DECODE:
+    d = host.Descriptor.build([host.BatchEntry(i, "decode", 1, 4096) for i in range(DECODE)], vocab=shape.vocab,
+                              token_seed=1)
+    TAU = DECODE
+else:
+    d = host.Descriptor.canonical(TAU, 32, 4096, 0, vocab=shape.vocab, token_seed=1)
 f.kv_alloc(d.pool_blocks)
 f.fill_descriptor_prefixes(d, seed=5)
 b = f.upload(d)
@@ -46,7 +53,8 @@ rel = lambda v: (v - t0) / 1e3
 # phase boundaries from the chain's own item counts
 h, ffn, T = shape.hidden, shape.ffn, TAU
 nq, nkv, hd = shape.num_q_heads, shape.num_kv_heads, shape.head_dim
-num_mt = (T + 255) // 256
+cg = 2 if T > 128 else 1
+num_mt = (T + 128 * cg - 1) // (128 * cg)
 S = [int(x) for x in os.environ.get("SS_CHAIN_S", "0,0,0,0").split(",")]
 K = [nq * hd, h, ffn, h]
 N = [h, 2 * ffn, h, (nq + 2 * nkv) * hd]
@@ -55,7 +63,10 @@ start = 0
 print(f"# {MODEL} tau={TAU} layer {LAYER}: {len(items)} items, span {rel(tr[live][:, 5].max()):.1f} us "
       f"(from the first producer start)")
 for p in range(4):
-    s = S[p] if S[p] > 0 else max(1, ((K[p] + 63) // 64 + 32) // 64)
+    nkb = (K[p] + 63) // 64
+    tiles = num_mt * ((N[p] + 255) // 256)
+    auto = max(1, (nkb + 32) // 64) if cg == 2 else max(1, min(nkb // 8, (148 + tiles - 1) // tiles))
+    s = S[p] if S[p] > 0 else auto
     cnt = num_mt * ((N[p] + 255) // 256) * s
     sel = [i for i in items if start <= i < start + cnt]
     start += cnt

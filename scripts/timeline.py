@@ -27,7 +27,12 @@ PREFIX = int(os.environ.get("PREFIX", "0"))
 GRAPHS = os.environ.get("GRAPHS", "1") == "1"
 
 f = gpu.HybridForward(shape, weight_seed=1234)
-d = host.Descriptor.canonical(TAU, 32, 4096, PREFIX, vocab=shape.vocab, token_seed=1)
+NDEC = int(os.environ.get("NDEC", "32"))
+if os.environ.get("DECODE_ONLY"):  # NDEC decodes at 4096, no chunk (the TBT-critical step)
+    d = host.Descriptor.build([host.BatchEntry(i, "decode", 1, 4096) for i in range(NDEC)], vocab=shape.vocab,
+                              token_seed=1)
+else:
+    d = host.Descriptor.canonical(TAU, NDEC, 4096, PREFIX, vocab=shape.vocab, token_seed=1)
 f.kv_alloc(d.pool_blocks)
 f.fill_descriptor_prefixes(d, seed=5)
 b = f.upload(d)
