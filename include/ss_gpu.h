@@ -123,6 +123,30 @@ ss_status ss_forward_enqueue(ss_ctx* ctx, const ss_batch* batch);
 ss_status ss_read_outputs(ss_ctx* ctx, const ss_batch* batch, float* logits_out,
                           int32_t* next_tokens_out);
 void ss_batch_free(ss_ctx* ctx, ss_batch* batch);
+
+/* Pipeline parallelism (reference engine.cpp:42-81, the stage model behind
+ * iteration_time(..., pp) = t / pp, costmodel.cpp:55): a context holding stage
+ * `stage` of `n_stages` of the model — layers [stage*L/n, (stage+1)*L/n), the
+ * reference's even split; the embedding on stage 0, the final norm + LM head on
+ * the last stage; the same synthetic weights and caches as the unpipelined model
+ * (layers keep their global indices). tp_size 1. Each stage needs ss_kv_alloc
+ * (its pool covers its own layers) and the same fills. Stages may sit on
+ * different devices. */
+ss_status ss_create_pp_stage(const ss_model_cfg* cfg, int32_t stage, int32_t n_stages,
+                             uint64_t weight_seed, int32_t device, ss_ctx** out);
+/* One stage of a forward of `batch` (uploaded on this stage's context).
+ * prev = stage - 1 (NULL for stage 0): its residual stream for the batch is
+ * handed over (device-to-device / peer copy ordered after prev's forward by an
+ * event; prev's next forward waits for the copy). Outputs: ss_read_outputs on
+ * the last stage. */
+ss_status ss_forward_stage_enqueue(ss_ctx* ctx, const ss_batch* batch, ss_ctx* prev);
+/* ss_forward_hybrid over a pipeline: stages[i] must be stage i of n. Uploads
+ * the descriptor to every stage, runs the stages in order with the hand-offs,
+ * reads the last stage's outputs; stage_ms (nullable, n entries): each stage's
+ * device time, from its hand-off (stage 0: the descriptor upload) to its end. */
+ss_status ss_forward_pipeline(ss_ctx* const* stages, int32_t n, const ss_batch_desc* desc,
+                              float* logits_out, int32_t* next_tokens_out, float* stage_ms);
+
 /* cudaStream_t of the context, for external event timing. */
 void* ss_stream(ss_ctx* ctx);
 ss_status ss_synchronize(ss_ctx* ctx);

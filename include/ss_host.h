@@ -112,6 +112,12 @@ typedef struct {
     ss_ctx* gpu;
     uint64_t token_seed;
     int32_t check_block_tables; /* assert block counts == ledger counts each issue */
+    /* pipeline-parallel model step (pp_degree == n_gpu_stages > 1): gpu_stages[i] is
+     * stage i (ss_create_pp_stage); every issued batch runs ss_forward_pipeline and
+     * the slowest stage's device time is the per-stage time of the reference's
+     * pipeline model (engine.cpp:42-81). gpu must then be NULL. */
+    ss_ctx* const* gpu_stages;
+    int32_t n_gpu_stages;
 } ssh_sim_opts;
 
 typedef struct ssh_report ssh_report;

@@ -102,7 +102,8 @@ class Latency(C.Structure):
 
 class SimOpts(C.Structure):
     _fields_ = [("keep_events", C.c_int32), ("max_events", C.c_int64), ("gpu", C.c_void_p),
-                ("token_seed", C.c_uint64), ("check_block_tables", C.c_int32)]
+                ("token_seed", C.c_uint64), ("check_block_tables", C.c_int32),
+                ("gpu_stages", C.c_void_p), ("n_gpu_stages", C.c_int32)]
 
 
 class CapacityProbe(C.Structure):
@@ -154,6 +155,9 @@ def gpu_lib():
         _sig(lib, "ss_forward_hybrid", I32, [P, C.POINTER(BatchDesc), P, P, C.POINTER(F)])
         _sig(lib, "ss_create_local_group", I32, [C.POINTER(ModelCfg), I32, C.c_uint64, I32, C.POINTER(P)])
         _sig(lib, "ss_forward_local_group", I32, [C.POINTER(P), I32, C.POINTER(BatchDesc), P, P, C.POINTER(F)])
+        _sig(lib, "ss_create_pp_stage", I32, [C.POINTER(ModelCfg), I32, I32, C.c_uint64, I32, C.POINTER(P)])
+        _sig(lib, "ss_forward_stage_enqueue", I32, [P, P, P])
+        _sig(lib, "ss_forward_pipeline", I32, [C.POINTER(P), I32, C.POINTER(BatchDesc), P, P, P])
         _sig(lib, "ss_batch_upload", I32, [P, C.POINTER(BatchDesc), C.POINTER(P)])
         _sig(lib, "ss_forward_enqueue", I32, [P, P])
         _sig(lib, "ss_read_outputs", I32, [P, P, P, P])
@@ -229,7 +233,8 @@ def host_check(status: int) -> None:
 
 
 GPU_EXPORTS = [
-    "ss_create", "ss_create_local_group", "ss_forward_local_group", "ss_destroy", "ss_model_config", "ss_nccl_unique_id", "ss_ipc_export", "ss_ipc_open", "ss_kv_alloc", "ss_forward_hybrid",
+    "ss_create", "ss_create_local_group", "ss_forward_local_group", "ss_create_pp_stage", "ss_forward_stage_enqueue",
+    "ss_forward_pipeline", "ss_destroy", "ss_model_config", "ss_nccl_unique_id", "ss_ipc_export", "ss_ipc_open", "ss_kv_alloc", "ss_forward_hybrid",
     "ss_batch_upload", "ss_forward_enqueue", "ss_read_outputs", "ss_batch_free", "ss_stream", "ss_synchronize",
     "ss_set_graphs", "ss_graph_stats", "ss_set_tp_allreduce",
     "ss_kv_fill_synthetic", "ss_set_profiling", "ss_kernel_times", "ss_kernel_class_name", "ss_launch_count",

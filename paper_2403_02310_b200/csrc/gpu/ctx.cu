@@ -168,6 +168,11 @@ struct LocalGroup {
 struct ss_ctx {
     ss_model_cfg cfg{};
     int rank = 0, tp = 1, device = 0, num_sms = 148;
+    // pipeline parallelism (ss_create_pp_stage): this context holds layers
+    // [layer0, layer0 + L) of cfg.num_layers; the embedding on stage 0, the final norm + LM
+    // head on the last stage. ev_stage marks the end of this stage's last forward.
+    int stage = 0, n_stages = 1, layer0 = 0;
+    cudaEvent_t ev_stage = nullptr;
     uint64_t seed = 0;
     int h = 0, L = 0, hd = 0, nq_l = 0, nkv_l = 0, G = 1, ffn_l = 0, vocab_l = 0;
     cudaStream_t st = nullptr;
@@ -994,10 +999,14 @@ ss_status enqueue_forward(ss_ctx* ctx, const ss_batch* b) {
     // epoch offsets restart every forward; embed advances the device base (d_epoch)
     ctx->sk_epoch = 0;
     ctx->ipc_epoch = 0;
-    RUN(launch(ctx, SS_K_EMBED, 1, [&] {
-        return embed_launch(b->tokens, ctx->embed, ctx->x, ctx->xb, ctx->ssq, T, h, ctx->d_epoch, kEpochStride,
-                            ctx->st);
-    }));
+    if (ctx->stage == 0) {
+        RUN(launch(ctx, SS_K_EMBED, 1, [&] {
+            return embed_launch(b->tokens, ctx->embed, ctx->x, ctx->xb, ctx->ssq, T, h, ctx->d_epoch, kEpochStride,
+                                ctx->st);
+        }));
+    } else {  // later pipeline stage: the residual stream came from the previous stage (ss_forward_stage_enqueue)
+        RUN(launch(ctx, SS_K_EMBED, 1, [&] { return epoch_advance_launch(ctx->d_epoch, kEpochStride, ctx->st); }));
+    }
     // RMSNorm is folded into the QKV / gate-up GEMMs: they consume the bf16 copy of
     // the residual (xb) and scale rows by rsqrt(mean(x^2) + eps) from the
     // per-chunk sums of squares (ssq) that embed / the residual-add epilogues
@@ -1082,7 +1091,7 @@ ss_status enqueue_forward(ss_ctx* ctx, const ss_batch* b) {
                        [&] { return residual_add_launch(ctx->x, sum, ctx->xb, ctx->ssq, T, h, ctx->st); }));
         }
     }
-    if (b->n_out > 0) {
+    if (b->n_out > 0 && ctx->stage == ctx->n_stages - 1) {
         RUN(launch(ctx, SS_K_RMSNORM, 1, [&] {
             return rmsnorm_launch(ctx->x, ctx->final_norm, ctx->xo, b->out_rows, b->n_out, h, eps, ctx->st);
         }));
@@ -1129,7 +1138,7 @@ std::vector<int64_t> graph_key(const ss_ctx* ctx, const ss_batch* b) {
 // for per-kernel profiling (events between launches) and for the one-device local group
 // (host barriers between ranks), and on NCCL (dlopen'ed library; not captured).
 ss_status run_forward(ss_ctx* ctx, const ss_batch* b) {
-    if (!ctx->graphs || ctx->prof || ctx->grp || ctx->comm) return enqueue_forward(ctx, b);
+    if (!ctx->graphs || ctx->prof || ctx->grp || ctx->comm || ctx->n_stages > 1) return enqueue_forward(ctx, b);
     if (ctx->graphs_gen != ctx->ws_gen) {
         graphs_clear(ctx);
         ctx->graphs_gen = ctx->ws_gen;
@@ -1197,6 +1206,8 @@ ss_status check_dev_err(ss_ctx* ctx) {
 }
 
 ss_status read_outputs(ss_ctx* ctx, const ss_batch* b, float* logits, int32_t* next) {
+    if (ctx->stage != ctx->n_stages - 1 && (logits || next) && b->n_out > 0)
+        return fail(ctx, SS_INVALID_ARG, "logits come from the last pipeline stage");
     if (b->n_out > 0) {
         const float* full = ctx->tp > 1 ? ctx->logits : ctx->logits_l;
         if (logits)
@@ -1324,11 +1335,15 @@ static void group_release(LocalGroup* g) {
 }
 
 static ss_status create_impl(const ss_model_cfg* cfg, int32_t tp_rank, int32_t tp_size, const void* nccl_id,
-                             uint64_t weight_seed, int32_t device, LocalGroup* grp, ss_ctx** out) {
+                             uint64_t weight_seed, int32_t device, LocalGroup* grp, ss_ctx** out, int32_t stage = 0,
+                             int32_t n_stages = 1) {
     ss_ctx* ctx = nullptr;
     if (!cfg || !out) return fail(ctx, SS_INVALID_ARG, "null argument");
     const ss_model_cfg& c = *cfg;
     if (tp_size < 1 || tp_rank < 0 || tp_rank >= tp_size) return fail(ctx, SS_INVALID_ARG, "bad tp rank/size");
+    if (n_stages < 1 || stage < 0 || stage >= n_stages || n_stages > c.num_layers)
+        return fail(ctx, SS_INVALID_ARG, "bad pipeline stage (need 0 <= stage < n_stages <= num_layers)");
+    if (n_stages > 1 && tp_size > 1) return fail(ctx, SS_INVALID_ARG, "pipeline stages are tp_size 1 contexts");
     if (c.num_layers < 1 || c.hidden % 64 || c.num_q_heads % tp_size || c.num_kv_heads % tp_size ||
         c.num_q_heads % c.num_kv_heads || (c.head_dim != 64 && c.head_dim != 128) || c.ffn % (32 * tp_size) ||
         c.vocab % tp_size || (c.vocab / tp_size) % 32 || c.max_positions < 1)
@@ -1350,7 +1365,11 @@ static ss_status create_impl(const ss_model_cfg* cfg, int32_t tp_rank, int32_t t
     ctx->device = device;
     ctx->num_sms = prop.multiProcessorCount;
     ctx->h = c.hidden;
-    ctx->L = c.num_layers;
+    ctx->stage = stage;
+    ctx->n_stages = n_stages;
+    // the reference's even split of layers over stages (PP degree divides the model)
+    ctx->layer0 = int(int64_t(stage) * c.num_layers / n_stages);
+    ctx->L = int(int64_t(stage + 1) * c.num_layers / n_stages) - ctx->layer0;
     ctx->hd = c.head_dim;
     ctx->nq_l = c.num_q_heads / tp_size;
     ctx->nkv_l = c.num_kv_heads / tp_size;
@@ -1392,22 +1411,25 @@ static ss_status create_impl(const ss_model_cfg* cfg, int32_t tp_rank, int32_t t
         return bail(fail(ctx, SS_CUDA_ERROR, "stream create"));
     cudaEventCreate(&ctx->ev0);
     cudaEventCreate(&ctx->ev1);
+    cudaEventCreateWithFlags(&ctx->ev_stage, cudaEventDisableTiming);
 
     // ---- weights: one allocation
     const int64_t h = c.hidden, hd = c.head_dim;
     const int64_t qkv_rows = int64_t(ctx->nq_l + 2 * ctx->nkv_l) * hd, qd = int64_t(ctx->nq_l) * hd;
     const int64_t per_layer = qkv_rows * h + h * qd + 2 * int64_t(ctx->ffn_l) * h + h * ctx->ffn_l + 2 * h;
-    size_t bytes = size_t(per_layer + 256 * 6) * 2 * size_t(c.num_layers) +
-                   size_t(int64_t(c.vocab) * h + int64_t(ctx->vocab_l) * h + h) * 2 + 4096;
+    const bool first = stage == 0, last = stage == n_stages - 1;
+    size_t bytes = size_t(per_layer + 256 * 6) * 2 * size_t(ctx->L) +
+                   size_t((first ? int64_t(c.vocab) * h : 0) + (last ? int64_t(ctx->vocab_l) * h + h : 0)) * 2 + 4096;
     if (cudaMalloc(&ctx->wmem, bytes) != cudaSuccess) return bail(fail(ctx, SS_OUT_OF_MEMORY, "weights allocation"));
     uint8_t* p = ctx->wmem;
-    ctx->layers.resize(size_t(c.num_layers));
+    ctx->layers.resize(size_t(ctx->L));
     const float s_qkv = ss_weight_scale(SS_T_Q, h, c.num_layers);
     const float s_o = ss_weight_scale(SS_T_O, int64_t(c.num_q_heads) * hd, c.num_layers);
     const float s_gu = ss_weight_scale(SS_T_GATE, h, c.num_layers);
     const float s_dn = ss_weight_scale(SS_T_DOWN, c.ffn, c.num_layers);
-    for (int l = 0; l < c.num_layers; ++l) {
-        Layer& W = ctx->layers[size_t(l)];
+    for (int ll = 0; ll < ctx->L; ++ll) {
+        const int l = ctx->layer0 + ll;  // global layer index: the same synthetic weights on every stage split
+        Layer& W = ctx->layers[size_t(ll)];
         W.wqkv = carve<bf16>(p, size_t(qkv_rows * h));
         W.wo = carve<bf16>(p, size_t(h * qd));
         W.wgu = carve<bf16>(p, size_t(2 * ctx->ffn_l * h));
@@ -1431,13 +1453,15 @@ static ss_status create_impl(const ss_model_cfg* cfg, int32_t tp_rank, int32_t t
             !bmaps(W.tb_gu, W.wgu, 2 * ctx->ffn_l, h) || !bmaps(W.tb_down, W.wdown, h, ctx->ffn_l))
             return bail(fail(ctx, SS_CUDA_ERROR, "cuTensorMapEncodeTiled failed (weights)"));
     }
-    ctx->embed = carve<bf16>(p, size_t(int64_t(c.vocab) * h));
-    ctx->lm_head = carve<bf16>(p, size_t(int64_t(ctx->vocab_l) * h));
-    ctx->final_norm = carve<bf16>(p, size_t(h));
-    {
+    if (first) {
+        ctx->embed = carve<bf16>(p, size_t(int64_t(c.vocab) * h));
+        if (ss_status s = init_weight(ctx, ctx->embed, W_EMBED, 0, c.vocab, h, ss_embed_scale(), 0, 0)) return bail(s);
+    }
+    if (last) {
+        ctx->lm_head = carve<bf16>(p, size_t(int64_t(ctx->vocab_l) * h));
+        ctx->final_norm = carve<bf16>(p, size_t(h));
         ss_status s;
-        if ((s = init_weight(ctx, ctx->embed, W_EMBED, 0, c.vocab, h, ss_embed_scale(), 0, 0)) ||
-            (s = init_weight(ctx, ctx->lm_head, W_LMHEAD, 0, ctx->vocab_l, h, ss_weight_scale(-1, h, c.num_layers), 0,
+        if ((s = init_weight(ctx, ctx->lm_head, W_LMHEAD, 0, ctx->vocab_l, h, ss_weight_scale(-1, h, c.num_layers), 0,
                              0)) ||
             (s = init_weight(ctx, ctx->final_norm, W_NORM, 0, 1, h, 1, 1, 1, SS_NORM_FINAL)))
             return bail(s);
@@ -1476,6 +1500,11 @@ static ss_status create_impl(const ss_model_cfg* cfg, int32_t tp_rank, int32_t t
 SS_API ss_status ss_create(const ss_model_cfg* cfg, int32_t tp_rank, int32_t tp_size, const void* nccl_id,
                            uint64_t weight_seed, int32_t device, ss_ctx** out) {
     return create_impl(cfg, tp_rank, tp_size, nccl_id, weight_seed, device, nullptr, out);
+}
+
+SS_API ss_status ss_create_pp_stage(const ss_model_cfg* cfg, int32_t stage, int32_t n_stages, uint64_t weight_seed,
+                                    int32_t device, ss_ctx** out) {
+    return create_impl(cfg, 0, 1, nullptr, weight_seed, device, nullptr, out, stage, n_stages);
 }
 
 SS_API ss_status ss_create_local_group(const ss_model_cfg* cfg, int32_t tp_size, uint64_t weight_seed,
@@ -1576,6 +1605,7 @@ SS_API void ss_destroy(ss_ctx* ctx) {
     cudaFree(ctx->chain_flags);
     cudaFree(ctx->chain_part);
     cudaFree(ctx->chain_trace);
+    if (ctx->ev_stage) cudaEventDestroy(ctx->ev_stage);
     if (ctx->grp) {
         for (ss_ctx*& r : ctx->grp->ranks)
             if (r == ctx) r = nullptr;
@@ -1649,6 +1679,76 @@ SS_API ss_status ss_forward_enqueue(ss_ctx* ctx, const ss_batch* b) {
     return run_forward(ctx, b);
 }
 
+// Pipeline hand-off: stage ctx (> 0) starts from the residual stream (fp32 x, its bf16 copy and
+// the per-chunk sums of squares the first norm-folded QKV consumes) that stage prev left for the
+// same batch; the copy runs on ctx's stream after prev's forward (event), over NVLink / peer
+// memory when the stages are on different devices, and prev's stream then waits for the copy
+// before its next forward may overwrite the buffers.
+ss_status stage_handoff(ss_ctx* ctx, ss_ctx* prev, int T) {
+    if (!prev || prev->stage != ctx->stage - 1 || prev->n_stages != ctx->n_stages || prev->h != ctx->h ||
+        prev->T_cap < T)
+        return fail(ctx, SS_INVALID_ARG, "pipeline stage s > 0 needs stage s - 1 of the same model and batch");
+    CK(cudaStreamWaitEvent(ctx->st, prev->ev_stage, 0));
+    const size_t h = size_t(ctx->h);
+    CK(cudaMemcpyAsync(ctx->x, prev->x, size_t(T) * h * 4, cudaMemcpyDefault, ctx->st));
+    CK(cudaMemcpyAsync(ctx->xb, prev->xb, size_t(T) * h * 2, cudaMemcpyDefault, ctx->st));
+    CK(cudaMemcpyAsync(ctx->ssq, prev->ssq, size_t(T) * (h / 32) * 4, cudaMemcpyDefault, ctx->st));
+    CK(cudaEventRecord(ctx->ev_stage, ctx->st));
+    CK(cudaStreamWaitEvent(prev->st, ctx->ev_stage, 0));
+    return SS_OK;
+}
+
+SS_API ss_status ss_forward_stage_enqueue(ss_ctx* ctx, const ss_batch* b, ss_ctx* prev) {
+    if (!ctx || !b) return SS_INVALID_ARG;
+    DevGuard dg(ctx->device);
+    if ((ctx->stage == 0) != (prev == nullptr))
+        return fail(ctx, SS_INVALID_ARG, "stage 0 takes no previous stage; every later stage needs stage - 1");
+    if (ss_status s = ensure_workspace(ctx, b->T, std::max(b->n_out, 1), b->part_rows)) return s;
+    if (prev)
+        if (ss_status s = stage_handoff(ctx, prev, b->T)) return s;
+    if (ss_status s = run_forward(ctx, b)) return s;
+    CK(cudaEventRecord(ctx->ev_stage, ctx->st));
+    return SS_OK;
+}
+
+SS_API ss_status ss_forward_pipeline(ss_ctx* const* stages, int32_t n, const ss_batch_desc* desc, float* logits,
+                                     int32_t* next, float* stage_ms) {
+    if (!stages || n < 1 || !desc) return fail(nullptr, SS_INVALID_ARG, "null argument");
+    for (int i = 0; i < n; ++i)
+        if (!stages[i] || stages[i]->stage != i || stages[i]->n_stages != n)
+            return fail(stages[i], SS_INVALID_ARG, "stages[i] must be pipeline stage i of n");
+    for (int i = 0; i < n; ++i) {  // every stage validates and uploads the same descriptor
+        ss_ctx* c = stages[i];
+        DevGuard dg(c->device);
+        if (ss_status s = upload(c, desc, &c->scratch, i == 0 ? c->ev0 : nullptr)) return s;
+    }
+    for (int i = 0; i < n; ++i) {
+        ss_ctx* ctx = stages[i];
+        DevGuard dg(ctx->device);
+        if (i > 0) {
+            // this stage's own time starts at the hand-off, once the previous stage is done
+            CK(cudaStreamWaitEvent(ctx->st, stages[i - 1]->ev_stage, 0));
+            CK(cudaEventRecord(ctx->ev0, ctx->st));
+            if (ss_status s = stage_handoff(ctx, stages[i - 1], ctx->scratch.T)) return s;
+        }
+        if (ss_status s = run_forward(ctx, &ctx->scratch)) return s;
+        CK(cudaEventRecord(ctx->ev1, ctx->st));
+        CK(cudaEventRecord(ctx->ev_stage, ctx->st));
+    }
+    ss_ctx* last = stages[n - 1];
+    {
+        DevGuard dg(last->device);
+        if (ss_status s = read_outputs(last, &last->scratch, logits, next)) return s;
+    }
+    for (int i = 0; i < n; ++i) {
+        ss_ctx* ctx = stages[i];
+        DevGuard dg(ctx->device);
+        CK(cudaEventSynchronize(ctx->ev1));
+        if (stage_ms) CK(cudaEventElapsedTime(&stage_ms[i], ctx->ev0, ctx->ev1));
+    }
+    return SS_OK;
+}
+
 SS_API ss_status ss_read_outputs(ss_ctx* ctx, const ss_batch* b, float* logits, int32_t* next) {
     if (!ctx || !b) return SS_INVALID_ARG;
     DevGuard dg(ctx->device);
@@ -1705,7 +1805,8 @@ SS_API ss_status ss_kv_fill_synthetic(ss_ctx* ctx, const int32_t* block_table, i
     CK(cudaMalloc(&d, size_t(std::max(n_blocks, 1)) * 4));
     CK(cudaMemcpy(d, block_table, size_t(n_blocks) * 4, cudaMemcpyHostToDevice));
     cudaError_t e = kv_fill_launch(ctx->kc, ctx->vc, ctx->layer_stride, ctx->L, d, n_tokens, rid, ctx->nkv_l,
-                                   ctx->rank * ctx->nkv_l, ctx->cfg.num_kv_heads, ctx->hd, ctx->bs, seed, ctx->st);
+                                   ctx->rank * ctx->nkv_l, ctx->cfg.num_kv_heads, ctx->hd, ctx->bs, seed, ctx->layer0,
+                                   ctx->st);
     cudaError_t e2 = cudaStreamSynchronize(ctx->st);
     cudaFree(d);
     if (e != cudaSuccess || e2 != cudaSuccess) return fail(ctx, SS_CUDA_ERROR, "synthetic KV fill failed");
@@ -1820,6 +1921,8 @@ SS_API ss_status ss_weight_ptr(ss_ctx* ctx, const char* name, int32_t layer, voi
     if (!ctx || !name) return SS_INVALID_ARG;
     const std::string n(name);
     const int64_t h = ctx->h, qkv = int64_t(ctx->nq_l + 2 * ctx->nkv_l) * ctx->hd, qd = int64_t(ctx->nq_l) * ctx->hd;
+    if ((n == "embed" && !ctx->embed) || ((n == "lm_head" || n == "final_norm") && !ctx->lm_head))
+        return fail(ctx, SS_INVALID_ARG, "this pipeline stage holds no " + n);
     if (n == "embed") { *ptr = ctx->embed; *rows = ctx->cfg.vocab; *cols = h; return SS_OK; }
     if (n == "lm_head") { *ptr = ctx->lm_head; *rows = ctx->vocab_l; *cols = h; return SS_OK; }
     if (n == "final_norm") { *ptr = ctx->final_norm; *rows = 1; *cols = h; return SS_OK; }

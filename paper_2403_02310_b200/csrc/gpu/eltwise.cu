@@ -458,7 +458,7 @@ __global__ void fold_gain_kernel(__nv_bfloat16* __restrict__ w, const __nv_bfloa
 
 __global__ void kv_fill_kernel(__nv_bfloat16* __restrict__ kb, __nv_bfloat16* __restrict__ vb, int64_t lstride,
                                int L, const int32_t* __restrict__ bt, int n_tokens, int rid, int nkv_l, int kv_off,
-                               int nkv_g, int hd, int bs, uint64_t seed) {
+                               int nkv_g, int hd, int bs, uint64_t seed, int layer0) {
     const int64_t per_layer = int64_t(n_tokens) * nkv_l * hd;
     const int64_t n = per_layer * L * 2;
     for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < n;
@@ -469,7 +469,7 @@ __global__ void kv_fill_kernel(__nv_bfloat16* __restrict__ kb, __nv_bfloat16* __
         const int64_t e = rem % per_layer;
         const int pos = int(e / (int64_t(nkv_l) * hd));
         const int h = int((e / hd) % nkv_l), d = int(e % hd);
-        const uint16_t v = ss_synth_kv(seed, layer, which, rid, pos, kv_off + h, d, nkv_g, hd);
+        const uint16_t v = ss_synth_kv(seed, layer0 + layer, which, rid, pos, kv_off + h, d, nkv_g, hd);
         const int64_t blk = bt[pos / bs];
         const int64_t off = layer * lstride + ((blk * nkv_l + h) * bs + pos % bs) * hd + d;
         (which ? vb : kb)[off] = __ushort_as_bfloat16(v);
@@ -574,12 +574,23 @@ cudaError_t fold_gain_launch(__nv_bfloat16* w, const __nv_bfloat16* gain, int64_
 
 cudaError_t kv_fill_launch(__nv_bfloat16* kb, __nv_bfloat16* vb, int64_t lstride, int L, const int32_t* bt,
                            int n_tokens, int rid, int nkv_l, int kv_off, int nkv_g, int hd, int bs, uint64_t seed,
-                           cudaStream_t st) {
+                           int layer0, cudaStream_t st) {
     const int64_t n = int64_t(n_tokens) * nkv_l * hd * L * 2;
     if (n > 0)
         kv_fill_kernel<<<grid_for(n, 256), 256, 0, st>>>(kb, vb, lstride, L, bt, n_tokens, rid, nkv_l, kv_off, nkv_g,
-                                                         hd, bs, seed);
+                                                         hd, bs, seed, layer0);
     return cudaGetLastError();
+}
+
+namespace {
+__global__ void epoch_advance_kernel(uint32_t* ctr, uint32_t stride) {
+    pdl_wait();  // the previous forward's kernels have completed (their epochs are no longer read)
+    *ctr += stride;
+}
+}  // namespace
+
+cudaError_t epoch_advance_launch(uint32_t* epoch_ctr, uint32_t epoch_stride, cudaStream_t st) {
+    return launch_pdl(epoch_advance_kernel, dim3(1), dim3(1), 0, st, 1, epoch_ctr, epoch_stride);
 }
 
 }  // namespace ssk

@@ -302,9 +302,13 @@ cudaError_t init_weight_launch(__nv_bfloat16* w, const WeightInit& wi, cudaStrea
 // w[r][c] = bf16(w[r][c] * gain[c]): an RMSNorm gain folded into the consuming projection
 // (x_hat * g) . W^T = x_hat . (W diag(g))^T.
 cudaError_t fold_gain_launch(__nv_bfloat16* w, const __nv_bfloat16* gain, int64_t rows, int64_t cols, cudaStream_t st);
+// layer0: global index of the pool's first layer (a pipeline stage holds layers layer0 ..).
 cudaError_t kv_fill_launch(__nv_bfloat16* kbase, __nv_bfloat16* vbase, int64_t layer_stride, int L,
                            const int32_t* bt_dev, int n_tokens, int rid, int nkv_l, int kv_off, int nkv_g, int hd,
-                           int bs, uint64_t seed, cudaStream_t st);
+                           int bs, uint64_t seed, int layer0, cudaStream_t st);
+// Advances the forward's device epoch base (what embed does on the first pipeline stage) for
+// a later stage, whose forward starts from the previous stage's residual stream.
+cudaError_t epoch_advance_launch(uint32_t* epoch_ctr, uint32_t epoch_stride, cudaStream_t st);
 
 }  // namespace ssk
 

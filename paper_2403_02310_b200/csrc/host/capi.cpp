@@ -142,6 +142,48 @@ private:
     int32_t vocab_ = 0;
 };
 
+// Pipeline-parallel model step: the batch runs through every stage (ss_forward_pipeline); the
+// engine's pipeline model (engine.cpp:42-81) takes one per-stage time per micro-batch, the
+// reference's iteration_time / pp (costmodel.cpp:55): here the slowest stage's measured time.
+class GpuPipelineExecutor final : public ss::StepExecutor {
+public:
+    GpuPipelineExecutor(ss_ctx* const* stages, int32_t n, std::uint64_t seed, const ss::ReplicaConfig& rc)
+        : stages_(stages, stages + n), seed_(seed), ms_(size_t(n)) {
+        if (n < 2 || rc.pp != n)
+            throw ss::ContractViolation("GPU pipeline: pp_degree must equal the number of stage contexts (>= 2)");
+        if (rc.tp != 1) throw ss::ContractViolation("GPU pipeline: tp_degree must be 1");
+        ss_model_cfg mc;
+        int32_t r, t;
+        if (ss_model_config(stages[0], &mc, &r, &t) != SS_OK) throw ss::ContractViolation("invalid GPU context");
+        vocab_ = mc.vocab;
+    }
+    double step_ms(const ss::Batch& b, const ss::KvLedger& kv, const std::vector<ss::Request>& reqs) override {
+        const ss::HostDesc d = ss::build_desc(b, kv, reqs, seed_, vocab_);
+        const ss_batch_desc v = d.view();
+        const ss_status st = ss_forward_pipeline(stages_.data(), int32_t(stages_.size()), &v, nullptr, nullptr, ms_.data());
+        if (st == SS_OUT_OF_KV) throw ss::OutOfKvBlocks(std::string("GPU forward: ") + ss_last_error(stages_.back()));
+        if (st != SS_OK) throw std::runtime_error(std::string("GPU pipeline forward failed: ") + ss_last_error(stages_.back()));
+        double worst = 0.0;
+        for (float x : ms_) worst = std::max(worst, double(x));
+        return worst;
+    }
+
+private:
+    std::vector<ss_ctx*> stages_;
+    std::uint64_t seed_;
+    std::vector<float> ms_;
+    int32_t vocab_ = 0;
+};
+
+std::unique_ptr<ss::StepExecutor> make_executor(ss_ctx* gpu, ss_ctx* const* stages, int32_t n_stages,
+                                                std::uint64_t token_seed, const ss::ReplicaConfig& rc,
+                                                const ss::CostParams& cp) {
+    if (gpu && n_stages > 0) throw ss::ContractViolation("set either gpu or gpu_stages");
+    if (n_stages > 0) return std::make_unique<GpuPipelineExecutor>(stages, n_stages, token_seed, rc);
+    if (gpu) return std::make_unique<GpuExecutor>(gpu, token_seed, rc);
+    return std::make_unique<ss::CostModelExecutor>(cp, rc.tp, rc.pp);
+}
+
 ssh_desc* make_desc(const ss::Batch& b, const std::vector<bool>& completes, int32_t bs, int32_t vocab,
                     std::uint64_t seed) {
     if (vocab < 1) throw ss::ContractViolation("vocab must be >= 1");
@@ -228,19 +270,21 @@ ss_status ssh_simulate(const ssh_replica_cfg* cfg, const ssh_cost_params* params
         for (int32_t i = 0; i < n; ++i) reqs.emplace_back(i, trace[i].arrival_us, trace[i].prompt_tokens, trace[i].output_tokens);
         ss::SimOptions so;
         ss_ctx* gpu = nullptr;
+        ss_ctx* const* stages = nullptr;
+        int32_t n_stages = 0;
         std::uint64_t token_seed = 0;
         if (opts) {
             so.keep_events = opts->keep_events != 0;
             if (opts->max_events > 0) so.max_events = opts->max_events;
             so.check_block_tables = opts->check_block_tables != 0;
             gpu = opts->gpu;
+            stages = opts->gpu_stages;
+            n_stages = opts->gpu_stages ? opts->n_gpu_stages : 0;
             token_seed = opts->token_seed;
         }
         const ss::ReplicaConfig rc = to_cfg(*cfg);
         const ss::CostParams cp = to_params(*params);
-        std::unique_ptr<ss::StepExecutor> exec;
-        if (gpu) exec = std::make_unique<GpuExecutor>(gpu, token_seed, rc);
-        else exec = std::make_unique<ss::CostModelExecutor>(cp, rc.tp, rc.pp);
+        std::unique_ptr<ss::StepExecutor> exec = make_executor(gpu, stages, n_stages, token_seed, rc, cp);
         auto r = std::make_unique<ssh_report>();
         r->rep = ss::simulate(rc, cp, reqs, *exec, so);
         *out = r.release();
@@ -354,15 +398,16 @@ ss_status ssh_capacity_search(const ssh_replica_cfg* cfg, const ssh_cost_params*
             o.parallel = opts->parallel;
         }
         ss_ctx* gpu = sim ? sim->gpu : nullptr;
-        if (gpu && o.parallel != 1) throw ss::ContractViolation("GPU capacity probes run one at a time (parallel = 1)");
+        ss_ctx* const* stages = sim ? sim->gpu_stages : nullptr;
+        const int32_t n_stages = stages ? sim->n_gpu_stages : 0;
+        if ((gpu || n_stages) && o.parallel != 1)
+            throw ss::ContractViolation("GPU capacity probes run one at a time (parallel = 1)");
         const std::uint64_t token_seed = sim ? sim->token_seed : 0;
         const ss::Probe probe = [&](double qps) {
             const std::vector<ss::Request> trace = ss::make_trace(*w, qps, probe_requests, seed);
             ss::SimOptions so;
             so.keep_events = false;  // probe_sim_options, cli.cpp:373-379
-            std::unique_ptr<ss::StepExecutor> exec;
-            if (gpu) exec = std::make_unique<GpuExecutor>(gpu, token_seed, rc);
-            else exec = std::make_unique<ss::CostModelExecutor>(cp, rc.tp, rc.pp);
+            std::unique_ptr<ss::StepExecutor> exec = make_executor(gpu, stages, n_stages, token_seed, rc, cp);
             return ss::summarize(ss::simulate(rc, cp, trace, *exec, so));
         };
         const ss::CapacityResult r = ss::capacity_search(probe, slo_ms, o);

@@ -10,7 +10,7 @@ from __future__ import annotations
 
 import ctypes as C
 from dataclasses import dataclass
-from typing import Optional, Tuple
+from typing import Optional, Sequence, Tuple
 
 import numpy as np
 
@@ -316,3 +316,59 @@ class LocalTPGroup:
     def close(self):
         for r in self.ranks:
             r.close()
+
+
+class PipelineGroup:
+    """Pipeline-parallel stages (ss_create_pp_stage): stage s holds layers
+    [s*L/pp, (s+1)*L/pp) (the reference's even split, engine.cpp:42-81), the
+    embedding on stage 0 and the LM head on the last; the residual stream is handed
+    from stage to stage (a peer copy when the stages sit on different devices).
+    `devices` places the stages (default: all on `device`)."""
+
+    def __init__(self, shape: ModelShape, pp: int, weight_seed: int = 1234, device: int = 0,
+                 devices: Optional[Sequence[int]] = None):
+        self.shape, self.pp = shape, pp
+        devices = list(devices) if devices is not None else [device] * pp
+        assert len(devices) == pp
+        hs = (C.c_void_p * pp)()
+        self.stages = []
+        for s in range(pp):
+            h = C.c_void_p()
+            st = gpu_lib().ss_create_pp_stage(C.byref(shape.c()), s, pp, weight_seed, devices[s], C.byref(h))
+            if st:
+                for x in self.stages:
+                    x.close()
+                _lib.raise_for(st, gpu_lib().ss_last_error(None).decode())
+            hs[s] = h.value
+            self.stages.append(HybridForward._adopt(shape, h.value, 0, 1))
+        self._hs = hs
+        self.stage_ms = [0.0] * pp
+
+    @property
+    def handles(self):
+        return self._hs
+
+    def kv_alloc(self, num_blocks: int, block_size: int = 16):
+        for s in self.stages:
+            s.kv_alloc(num_blocks, block_size)
+
+    def fill_descriptor_prefixes(self, desc, seed: int):
+        for s in self.stages:
+            s.fill_descriptor_prefixes(desc, seed)
+
+    def forward(self, desc, logits: bool = True) -> Tuple[Optional[np.ndarray], np.ndarray, float]:
+        """ss_forward_pipeline; returns (logits, next tokens, slowest stage's device ms);
+        every stage's time is left in self.stage_ms."""
+        v = desc.view if hasattr(desc, "view") else desc
+        lg = np.empty((v.n_out, self.shape.vocab), np.float32) if logits else None
+        nt = np.empty(v.n_out, np.int32)
+        ms = (C.c_float * self.pp)()
+        st = gpu_lib().ss_forward_pipeline(self._hs, self.pp, C.byref(v), lg.ctypes.data if logits else None,
+                                           nt.ctypes.data, ms)
+        self.stages[-1]._check(st)
+        self.stage_ms = [float(x) for x in ms]
+        return lg, nt, max(self.stage_ms)
+
+    def close(self):
+        for s in self.stages:
+            s.close()

@@ -177,12 +177,22 @@ class SimReport:
             yield self.microbatch(i)
 
 
+def _sim_opts(gpu, token_seed: int, keep_events: bool = False, check_block_tables: bool = False):
+    """SimOpts for a cost-model clock (gpu None), one GPU context, or a pipeline group."""
+    if gpu is not None and hasattr(gpu, "stages"):
+        return _lib.SimOpts(int(keep_events), 0, None, token_seed, int(check_block_tables),
+                            C.cast(gpu.handles, C.c_void_p), len(gpu.stages))
+    h = gpu.handle.value if gpu is not None else None
+    return _lib.SimOpts(int(keep_events), 0, h, token_seed, int(check_block_tables), None, 0)
+
+
 def simulate(cfg: ReplicaConfig, params: CostModelParams, trace: Sequence[Request], *, keep_events: bool = True,
              gpu=None, token_seed: int = 0, check_block_tables: bool = False) -> SimReport:
     """engine.cpp:326-330. With gpu (a gpu.HybridForward) every issued batch runs
-    the real forward and its measured time replaces iteration_time()."""
-    opts = _lib.SimOpts(int(keep_events), 0, gpu.handle if gpu is not None else None, token_seed,
-                        int(check_block_tables))
+    the real forward and its measured time replaces iteration_time(); with a
+    gpu.PipelineGroup (pp_degree stages) the batch runs through every stage and the
+    slowest stage's time is the pipeline model's per-stage time."""
+    opts = _sim_opts(gpu, token_seed, keep_events, check_block_tables)
     h = C.c_void_p()
     host_check(host_lib().ssh_simulate(C.byref(cfg._c()), C.byref(params._c()), _rows(trace), len(trace),
                                        C.byref(opts), C.byref(h)))
@@ -279,7 +289,7 @@ def capacity_search(cfg: ReplicaConfig, params: CostModelParams, workload: str, 
     with gpu (a gpu.HybridForward) every probe runs real forwards. Raises InfeasibleSlo
     when qps_low fails."""
     opts = _lib.CapacityOpts(qps_low, max_qps, rel_width, parallel)
-    sim = _lib.SimOpts(0, 0, gpu.handle.value if gpu is not None else None, token_seed, 0)
+    sim = _sim_opts(gpu, token_seed)
     qps = C.c_double()
     mono = C.c_int32()
     cap = 256

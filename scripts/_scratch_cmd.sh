@@ -1,4 +1,4 @@
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-timeout 60 ./scripts/epi_store_bench > gpurun_out/epi_store_bench.txt 2>&1
-cat gpurun_out/epi_store_bench.txt
+timeout 900 python -m pytest tests/test_gpu_pp.py -q -x -p no:cacheprovider > gpurun_out/test_pp.txt 2>&1
+tail -15 gpurun_out/test_pp.txt
