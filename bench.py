@@ -233,15 +233,17 @@ def run_ours(args):
         for _ in range(3):  # the shape's graph is captured on its second forward
             fwd.forward(desc, logits=False)
         barrier()
+        call_ms = []
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            fwd.forward(view, logits=False)
+            call_ms.append(fwd.forward(view, logits=False)[2])  # the call's own device time (its events)
         barrier()
-        return max_over_ranks((time.perf_counter() - t0) * 1e3 / args.e2e_steps)
+        wall = max_over_ranks((time.perf_counter() - t0) * 1e3 / args.e2e_steps)
+        return wall, max_over_ranks(sum(call_ms) / len(call_ms))
 
-    e2e_ms = e2e_time()  # CUDA graph replays (default)
+    e2e_ms, e2e_call_dev = e2e_time()  # CUDA graph replays (default)
     fwd.set_graphs(False)
-    e2e_eager_ms = e2e_time()  # the same calls with eager launches, for the graph effect
+    e2e_eager_ms, e2e_eager_dev = e2e_time()  # the same calls with eager launches, for the graph effect
     fwd.set_graphs(True)
 
     peaks, peak_src = load_peaks()
@@ -333,8 +335,12 @@ def run_ours(args):
                 "d2h_bytes_per_step": d2h, "api": "ss_forward_hybrid (host descriptor arrays -> next tokens)",
                 "graphs": "CUDA graph replay of the batch shape (ss_set_graphs, default on)",
                 "gap_vs_device_ms": e2e_ms - ms_step,
+                # host time per call: wall minus the call's own device time (H2D .. D2H events);
+                # the gap above also counts that back-to-back device steps overlap (PDL)
+                "call_device_ms": e2e_call_dev, "gap_vs_call_device_ms": e2e_ms - e2e_call_dev,
                 "graphs_off": {"value": T / (e2e_eager_ms * 1e-3), "ms_per_step": e2e_eager_ms,
-                               "gap_vs_device_ms": e2e_eager_ms - ms_step}},
+                               "gap_vs_device_ms": e2e_eager_ms - ms_step,
+                               "gap_vs_call_device_ms": e2e_eager_ms - e2e_eager_dev}},
         "gpu_launches": launches,
         "roofline": roof,
         "whole_step_roofline": {"ms": whole_roof_ms, "frac": whole_roof_ms / ms_step, "alg_bytes": work["bytes"],

@@ -767,7 +767,7 @@ ss_status gemm(ss_ctx* ctx, int cls, const CUtensorMap& ta, WMaps& tb, int M, in
         const int idx = cls == SS_K_GEMM_QKV ? 0 : cls == SS_K_GEMM_O ? 1 : cls == SS_K_GEMM_GATEUP ? 2
                       : cls == SS_K_GEMM_DOWN ? 3 : 4;
         const int* f = ctx->tu.gemm_force[idx];
-        if (f[0] >= 0) s = GemmShape{M > 128 ? 2 : 1, f[1], f[2], f[0]};
+        if (f[0] >= 0) s = GemmShape{M > 128 ? 2 : 1, f[1], f[2], f[0], M <= 32 && !ctx->tu.gemm_ar128 ? 32 : 128};
     }
     p.cg = s.cg;
     p.bn = s.bn;

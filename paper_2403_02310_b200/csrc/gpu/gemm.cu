@@ -49,7 +49,9 @@ struct GemmCfg {
     static constexpr int B_BYTES = B_ROWS * BK * 2;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int STAGES_FIT = kSmemBudget / STAGE_BYTES;
-    static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
+    // narrow weight-streaming tiles (decode-sized M) keep more, smaller stages in flight
+    static constexpr int STAGES_MAX = STAGE_BYTES <= 16384 ? 16 : 8;
+    static constexpr int STAGES = STAGES_FIT > STAGES_MAX ? STAGES_MAX : STAGES_FIT;
     static constexpr int TMEM_COLS = 2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512);
     // + barriers (1 KB slot) + the epilogue warps' 4 KB staging buffers
     static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + 1024 + 8 * 4096;
@@ -1800,7 +1802,7 @@ GemmShape gemm_pick(int M, int N, int K, int epi, int num_sms, const Tuning& tu)
     // Whole tiles go round-robin (mode 0); a ragged last wave can be split in K
     // (mode 2); mode 3 balances every group exactly.
     auto tile_us = [](int c, int b) {
-        if (c == 1) return b == 256 ? 28.6 : 20.4;
+        if (c == 1) return b == 256 ? 28.6 : b == 128 ? 20.4 : 11.0;  // 64: weight streaming, 16 stages
         return 15.0 + 0.0135 * b;
     };
     const double kscale = double((K + BK - 1) / BK) / 64.0;
@@ -1844,6 +1846,7 @@ GemmShape gemm_pick(int M, int N, int K, int epi, int num_sms, const Tuning& tu)
     if (M <= 128 || force_cg == 1) {
         consider(1, 256);
         consider(1, 128);
+        if (M <= 32 && !tu.gemm_ar128) consider(1, 64);  // 32-row A stages only
     }
     best.ar = (best.cg == 1 && M <= 32 && !tu.gemm_ar128) ? 32 : 128;
     if (M > 128 && force_cg != 1)
@@ -1914,6 +1917,7 @@ cudaError_t gemm_launch(const GemmPlan& p, cudaStream_t st) {
         if (p.epi == EPI_SWIGLU) return launch_t<1, BNv, EPI_SWIGLU, 32>(p, st);         \
         if (p.epi == EPI_QKV) return launch_t<1, BNv, EPI_QKV, 32>(p, st);               \
     }
+        SS_GEMM_CASE32(64)
         SS_GEMM_CASE32(128)
         SS_GEMM_CASE32(256)
 #undef SS_GEMM_CASE32

@@ -1,4 +1,6 @@
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_pp.py -q -x -p no:cacheprovider > gpurun_out/test_pp.txt 2>&1
-tail -15 gpurun_out/test_pp.txt
+timeout 300 python scripts/pp_probe.py > gpurun_out/pp_probe.txt 2>&1
+cat gpurun_out/pp_probe.txt
+TAUS=1024,2048 timeout 3000 python scripts/capacity_b200.py > gpurun_out/capacity_mistral7b_1024_2048.json 2> gpurun_out/capacity_b.err
+tail -3 gpurun_out/capacity_b.err

@@ -24,6 +24,24 @@ def small():
     f.close()
 
 
+@pytest.fixture
+def tuned(monkeypatch):
+    """A context created after the test's SS_* settings: the dev tuning is read once, at
+    ss_create (the module-scoped `small` would keep the defaults)."""
+    made = []
+
+    def make(env):
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        f = gpu.HybridForward(SMALL, weight_seed=7)
+        made.append(f)
+        return f
+
+    yield make
+    for f in made:
+        f.close()
+
+
 def _rand(shape, scale=1.0, seed=0):
     g = torch.Generator(device="cuda").manual_seed(seed)
     return (torch.randn(shape, generator=g, device="cuda") * scale).to(torch.bfloat16)
@@ -82,12 +100,11 @@ def test_gemm_stream_k_shapes(small, M, N, K):
                                  {"SS_GEMM_SK": "0"}, {"SS_GEMM_SK": "3", "SS_GEMM_BN": "128"},
                                  {"SS_GEMM_SK": "3", "SS_GEMM_BN": "256"}])
 @pytest.mark.parametrize("epi", [0, 1, 2, 3])
-def test_gemm_forced_split_schedules(small, monkeypatch, env, epi):
+def test_gemm_forced_split_schedules(tuned, env, epi):
     """Every epilogue through the split-K fixups (stream-K; lockstep split of the ragged
     wave with the staged smem/bulk-copy reduction; M-lockstep stream-K): values and
     bitwise repeatability."""
-    for k, v in env.items():
-        monkeypatch.setenv(k, v)
+    small = tuned(env)
     M, N, K = 512, 28672 if epi == 2 else 4096, 4096
     A = _rand((M, K), 1.0, 11)
     B = _rand((N, K), 1.0 / math.sqrt(K), 12)
@@ -281,15 +298,18 @@ def test_prefill_paired_tiles(nq, nkv, hd):
     f.close()
 
 
-@pytest.mark.parametrize("env", [{"SS_GEMM_SK": "3", "SS_GEMM_BN": "128"}, {"SS_GEMM_SK": "3", "SS_GEMM_BN": "256"},
-                                 {"SS_GEMM_SPLITS": "4", "SS_GEMM_BN": "128"}])
-@pytest.mark.parametrize("M", [33, 100])
+@pytest.mark.parametrize("env,M", [(e, m) for e in ({"SS_GEMM_SK": "3", "SS_GEMM_BN": "128"},
+                                                      {"SS_GEMM_SK": "3", "SS_GEMM_BN": "256"},
+                                                      {"SS_GEMM_SPLITS": "4", "SS_GEMM_BN": "128"}) for m in (33, 100)]
+                         + [(e, m) for e in ({"SS_GEMM_SK": "0", "SS_GEMM_BN": "64"},
+                                             {"SS_GEMM_SPLITS": "2", "SS_GEMM_BN": "64"},
+                                             {"SS_GEMM_SK": "3", "SS_GEMM_BN": "64"}) for m in (1, 8, 32)])
 @pytest.mark.parametrize("epi", [0, 1, 2, 3])
-def test_gemm_small_m_split_schedules(small, monkeypatch, env, M, epi):
+def test_gemm_small_m_split_schedules(tuned, env, M, epi):
     """Single-CTA (M <= 128) tiles through stream-K and split-K: every epilogue, values and
-    bitwise repeatability (decode-only batches take these schedules)."""
-    for k, v in env.items():
-        monkeypatch.setenv(k, v)
+    bitwise repeatability (decode-only batches take these schedules; BN = 64 weight-streaming
+    tiles with 32-row A stages up to M = 32)."""
+    small = tuned(dict(env, SS_GEMM_DEBUG="1"))
     N, K = (2048 if epi == 2 else 1024), 4096
     A = _rand((M, K), 1.0, 31)
     B = _rand((N, K), 1.0 / math.sqrt(K), 32)
