@@ -1846,7 +1846,9 @@ GemmShape gemm_pick(int M, int N, int K, int epi, int num_sms, const Tuning& tu)
     if (M <= 128 || force_cg == 1) {
         consider(1, 256);
         consider(1, 128);
-        if (M <= 32 && !tu.gemm_ar128) consider(1, 64);  // 32-row A stages only
+        // BN = 64 weight-streaming tiles (32-row A stages): only when forced — measured slower
+        // on the decode-only step (6.33 vs 6.14 ms, profiles/r02/ab_decode_bn64.txt)
+        if (M <= 32 && !tu.gemm_ar128 && force_bn == 64) consider(1, 64);
     }
     best.ar = (best.cg == 1 && M <= 32 && !tu.gemm_ar128) ? 32 : 128;
     if (M > 128 && force_cg != 1)
