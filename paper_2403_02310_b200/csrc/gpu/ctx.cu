@@ -353,6 +353,7 @@ ss_status init_weight(ss_ctx* ctx, bf16* w, int kind, int layer, int64_t rows, i
     wi.nq_l = ctx->nq_l;
     wi.nkv_l = ctx->nkv_l;
     wi.hd = ctx->hd;
+    wi.qkv_interleave = ctx->fuse_rope;  // the fused QKV epilogue reads rotate-half pairs as adjacent chunks
     wi.ffn_l = ctx->ffn_l;
     wi.vocab_l = ctx->vocab_l;
     wi.seed = ctx->seed;

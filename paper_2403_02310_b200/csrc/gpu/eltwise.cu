@@ -400,6 +400,11 @@ __global__ void init_weight_kernel(__nv_bfloat16* __restrict__ w, const WeightIn
         switch (wi.kind) {
             case W_QKV: {
                 const int64_t qr = int64_t(wi.nq_l) * wi.hd, kr = int64_t(wi.nkv_l) * wi.hd;
+                int64_t i = idx / wi.cols;  // logical row (per-head chunk order restored)
+                if (wi.qkv_interleave && wi.hd == 128) {
+                    const int64_t off = i % 128, k = off / 32;
+                    i += ((k == 1) ? 32 : (k == 2) ? -32 : 0);  // stored chunk k holds logical chunk {0,2,1,3}[k]
+                }
                 if (i < qr) {
                     tag = SS_TAG_LAYER(wi.layer, SS_T_Q);
                     gr = uint64_t(wi.rank * qr + i);

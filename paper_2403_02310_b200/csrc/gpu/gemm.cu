@@ -645,12 +645,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (kb0 == 0 && row < M) {
                     q_pos = ea.pos[row];
                     q_slot = ea.slot[row];
-                    const int ps = ea.hd / 64;
-                    if (half < (BN / ea.hd) * ps) {
-                        const int c = (half / ps) * (2 * ps) + (half % ps);
-                        const int col = n0 + c * 32;
-                        if (col < N && col / ea.hd < ea.nq + ea.nkv) {
-                            const float4* cs = reinterpret_cast<const float4*>(ea.rope + size_t(q_pos) * (ea.hd / 2) + col % ea.hd);
+                    // this warp's chunk pairs (2 pi, 2 pi + 1), pi = half, half + 2: 128 columns
+                    // apart, so the same offset i0 inside their heads (hd = 64 or 128)
+                    if (half < BN / 64) {
+                        const int col = n0 + 2 * half * 32;
+                        if (col < N) {
+                            const float4* cs = reinterpret_cast<const float4*>(ea.rope + size_t(q_pos) * (ea.hd / 2) +
+                                                                               (col % ea.hd) / 2);
 #pragma unroll
                             for (int j = 0; j < 16; ++j)
                                 asm volatile("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];"
@@ -798,22 +799,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 };
                 if constexpr (EPI == EPI_QKV) {
-                    // chunk pairs (c, c + ps) hold the rotate-half partners i, i + hd/2 of one head
-                    const int ps = ea.hd / 64;
+                    // chunk pairs (c, c + 1), c even, hold the rotate-half partners i, i + hd/2 of
+                    // one head (Wqkv stores each head's 32-row chunks as [0, 2, 1, 3] for hd = 128)
                     const int64_t blk = q_slot / ea.bs, off = q_slot % ea.bs;
 #pragma unroll 1
-                    for (int pi = half; pi < (BN / ea.hd) * ps; pi += 2) {
-                        const int c = (pi / ps) * (2 * ps) + (pi % ps);
+                    for (int pi = half; pi < BN / 64; pi += 2) {
+                        const int c = 2 * pi;
                         uint32_t x1[32], x2[32];
                         tmem_ld32(t_row + uint32_t(c * 32), x1);
-                        tmem_ld32(t_row + uint32_t((c + ps) * 32), x2);
+                        tmem_ld32(t_row + uint32_t((c + 1) * 32), x2);
                         tmem_wait_ld();
                         if (pi < half + 4) TRACE2(7 + 3 * ((pi - half) >> 1));
                         add_pieces(x1, c);
-                        add_pieces(x2, c + ps);
+                        add_pieces(x2, c + 1);
                         const int col = n0 + c * 32;
                         if (col >= N) continue;  // warp-uniform
-                        const int hh = col / ea.hd, i0 = col % ea.hd;  // i0 < hd/2
+                        const int hh = col / ea.hd, i0 = (col % ea.hd) / 2;  // i0 < hd/2
                         // this row's packed bf16 result, staged as [lo 64 B | hi 64 B] (lo = columns
                         // i0.., hi = i0 + hd/2..), four 16-byte chunks at a time
                         const bool rot = hh < ea.nq + ea.nkv;  // q or k head: rotate (warp-uniform)
@@ -1125,10 +1126,7 @@ struct ChainItem {
 // later reduces exactly these chunks.
 __device__ __forceinline__ int warp_chunk(int epi, int hd, int half, int k) {
     if (epi == EPI_SWIGLU) return 2 * half + 4 * (k >> 1) + (k & 1);
-    if (epi == EPI_QKV) {
-        const int ps = hd / 64, pi = half + 2 * (k >> 1), c = (pi / ps) * (2 * ps) + (pi % ps);
-        return (k & 1) ? c + ps : c;
-    }
+    if (epi == EPI_QKV) return 2 * (half + 2 * (k >> 1)) + (k & 1);  // rotate-half pairs (c, c + 1)
     return half + 2 * k;
 }
 __device__ __forceinline__ ChainItem chain_item(const ChainPlan& P, int i) {
@@ -1485,17 +1483,16 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_chain_kernel(const __grid_co
             if (!live) {
                 // no token rows in this warp's quarter of the tile: nothing to store
             } else if (EPI == EPI_QKV) {
-                const int ps = ea.hd / 64;
                 const int64_t blk = q_slot / ea.bs, off = q_slot % ea.bs;
 #pragma unroll 1
-                for (int pi = half; pi < (BN / ea.hd) * ps; pi += 2) {
-                    const int c = (pi / ps) * (2 * ps) + (pi % ps);
+                for (int pi = half; pi < BN / 64; pi += 2) {  // rotate-half pairs (c, c + 1), c even
+                    const int c = 2 * pi;
                     uint32_t x1[32], x2[32];
                     load_chunk(c, x1);
-                    load_chunk(c + ps, x2);
+                    load_chunk(c + 1, x2);
                     const int col = n0 + c * 32;
                     if (col >= N) continue;
-                    const int hh = col / ea.hd, i0 = col % ea.hd;
+                    const int hh = col / ea.hd, i0 = (col % ea.hd) / 2;
                     const bool rot = hh < ea.nq + ea.nkv;
                     const float4* cs = reinterpret_cast<const float4*>(ea.rope + size_t(q_pos) * (ea.hd / 2) + i0);
 #pragma unroll
@@ -1808,7 +1805,7 @@ GemmShape gemm_pick(int M, int N, int K, int epi, int num_sms, const Tuning& tu)
     const double kscale = double((K + BK - 1) / BK) / 64.0;
     auto consider = [&](int cg, int bn) {
         if (swiglu && bn % 64) return;
-        if (epi == EPI_QKV && bn % 128) return;  // whole heads per tile (hd 64 or 128)
+        if (epi == EPI_QKV && bn % 64) return;  // whole rotate-half chunk pairs per tile
         if (force_bn && bn != force_bn) return;
         if (force_cg && cg != force_cg) return;
         const long num_mt = (M + 128 * cg - 1) / (128 * cg), num_n = (N + bn - 1) / bn;
@@ -1908,7 +1905,7 @@ cudaError_t gemm_launch(const GemmPlan& p, cudaStream_t st) {
         if (p.epi == EPI_RESADD) return launch_t<CGv, BNv, EPI_RESADD>(p, st);      \
         if (p.epi == EPI_F32) return launch_t<CGv, BNv, EPI_F32>(p, st);            \
         if (p.epi == EPI_SWIGLU && BNv % 64 == 0) return launch_t<CGv, (BNv % 64 == 0 ? BNv : 64), EPI_SWIGLU>(p, st); \
-        if (p.epi == EPI_QKV && BNv % 128 == 0) return launch_t<CGv, (BNv % 128 == 0 ? BNv : 128), EPI_QKV>(p, st); \
+        if (p.epi == EPI_QKV && BNv % 64 == 0) return launch_t<CGv, (BNv % 64 == 0 ? BNv : 64), EPI_QKV>(p, st); \
     }
     if (p.cg == 1 && p.ar == 32) {
 #define SS_GEMM_CASE32(BNv)                                                              \

@@ -297,6 +297,10 @@ struct WeightInit {
     uint64_t seed;
     float scale_a, scale_b, scale_c;  // per-tag scales (q/k/v or gate/up)
     int norm;                         // W_NORM: which gain (SS_NORM_*)
+    // W_QKV, hd = 128: store each head's 32-row chunks as [0-31, 64-95, 32-63, 96-127], so
+    // every rotate-half partner pair is two adjacent 32-column chunks of the QKV output (the
+    // fused QKV epilogue then needs no whole-head tiles: any 64-column multiple works)
+    int qkv_interleave;
 };
 cudaError_t init_weight_launch(__nv_bfloat16* w, const WeightInit& wi, cudaStream_t st);
 // w[r][c] = bf16(w[r][c] * gain[c]): an RMSNorm gain folded into the consuming projection

@@ -1,6 +1,6 @@
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-AB='SS_GEMM_DEBUG=0;SS_GEMM_O=2,128,3 SS_GEMM_DOWN=2,128,3 SS_GEMM_GATEUP=0,256;SS_GEMM_O=2,64,2 SS_GEMM_DOWN=2,64,2;SS_GEMM_GATEUP=3,64 SS_GEMM_DOWN=0,64' TAU=32 NDEC=32 ROUNDS=3 timeout 600 python scripts/ab_env.py > gpurun_out/ab_dec64.txt 2>&1
+AB=';SS_GEMM_O=2,128,3 SS_GEMM_DOWN=2,128,3 SS_GEMM_GATEUP=0,256;SS_GEMM_O=2,64,2 SS_GEMM_DOWN=2,64,2;SS_GEMM_GATEUP=3,64 SS_GEMM_DOWN=0,64' TAU=32 NDEC=32 ROUNDS=3 timeout 600 python scripts/ab_env.py > gpurun_out/ab_dec64.txt 2>&1
 tail -6 gpurun_out/ab_dec64.txt
 SS_GEMM_DEBUG=1 timeout 120 python -c "
 import sys; sys.path.insert(0,'.')
