@@ -50,7 +50,12 @@ struct GemmCfg {
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int STAGES_FIT = kSmemBudget / STAGE_BYTES;
     // narrow weight-streaming tiles (decode-sized M) keep more, smaller stages in flight
-    static constexpr int STAGES_MAX = STAGE_BYTES <= 16384 ? 16 : 8;
+#ifndef SS_GEMM_STAGES_CAP  // dev: cap the operand ring depth (latency-sensitivity probes)
+#define SS_GEMM_STAGES_CAP 16
+#endif
+    static constexpr int STAGES_MAX = (STAGE_BYTES <= 16384 ? 16 : 8) < SS_GEMM_STAGES_CAP
+                                          ? (STAGE_BYTES <= 16384 ? 16 : 8)
+                                          : SS_GEMM_STAGES_CAP;
     static constexpr int STAGES = STAGES_FIT > STAGES_MAX ? STAGES_MAX : STAGES_FIT;
     static constexpr int TMEM_COLS = 2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512);
     // + barriers (1 KB slot) + the epilogue warps' 4 KB staging buffers

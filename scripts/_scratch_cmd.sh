@@ -1,7 +1,12 @@
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_forward.py tests/test_gpu_tp_local.py tests/test_gpu_chain.py -q -x -p no:cacheprovider > gpurun_out/test_qkv.txt 2>&1
-tail -4 gpurun_out/test_qkv.txt
-AB=';SS_GEMM_QKV=0,256;SS_GEMM_QKV=2,192,2' ROUNDS=3 timeout 600 python scripts/ab_env.py > gpurun_out/ab_qkv.txt 2>&1
-tail -4 gpurun_out/ab_qkv.txt
-SS_GEMM_DEBUG=1 LAYERS=2 timeout 120 python scripts/chain_check.py 2>&1 | grep "epi=4" | sort | uniq | head
+cp paper_2403_02310_b200/libss_gpu.so /tmp/orig.so
+for v in st4 st5; do
+cp build_variants/$v/libss_gpu.so paper_2403_02310_b200/libss_gpu.so
+echo "== $v" >> gpurun_out/gemm_stages.txt
+timeout 300 python scripts/gemm_scaling_power.py >> gpurun_out/gemm_stages.txt 2>&1
+done
+cp /tmp/orig.so paper_2403_02310_b200/libss_gpu.so
+echo "== 6 (default)" >> gpurun_out/gemm_stages.txt
+timeout 300 python scripts/gemm_scaling_power.py >> gpurun_out/gemm_stages.txt 2>&1
+cat gpurun_out/gemm_stages.txt
