@@ -28,7 +28,8 @@ $(PKG)/libss_gpu.so: $(GPU_SRCS) $(GPU_HDRS)
 $(PKG)/libss_host.so: $(HOST_SRCS) $(HOST_HDRS) $(PKG)/libss_gpu.so
 	$(CXX) $(HOSTFLAGS) -shared -o $@ $(HOST_SRCS) -L$(PKG) -lss_gpu -Wl,-rpath,'$$ORIGIN'
 
-oracle:
+# (after both libraries: oracle/_ref/ref_engine_gpu links them)
+oracle: $(PKG)/libss_gpu.so $(PKG)/libss_host.so
 	$(MAKE) -C oracle
 
 clean:
