@@ -339,3 +339,28 @@ def test_gemm_small_m_split_schedules(tuned, env, M, epi):
         torch.testing.assert_close(D.float(), want, rtol=2e-2, atol=2e-2)
     else:
         torch.testing.assert_close(D, ref, rtol=2e-4, atol=2e-4)
+
+
+@pytest.mark.parametrize("epi", [0, 1, 2])
+@pytest.mark.parametrize("M,sk", [(512, "0"), (512, "3"), (2048, "0")])
+def test_gemm_weight_multicast_matches_unicast(tuned, epi, M, sk):
+    """4-CTA clusters sharing weight tiles by TMA multicast (SS_GEMM_MC=1; opt-in): the same
+    tile schedule as the unicast kernel -> bitwise equal outputs (whole tiles), or equal to
+    the unicast result within bf16 rounding (stream-K: the pair count, hence the split, differs)."""
+    N, K = (4096 if epi == 2 else 2048), 1024
+    A = _rand((M, K), 1.0, 41)
+    B = _rand((N, K), 1.0 / math.sqrt(K), 42)
+    outs = []
+    for mc in ("0", "1"):
+        f = tuned({"SS_GEMM_MC": mc, "SS_GEMM_SK": sk, "SS_GEMM_BN": "256"})
+        if epi == 1:
+            D = torch.ones((M, N), device="cuda")
+        else:
+            D = torch.empty((M, N // 2 if epi == 2 else N), dtype=torch.bfloat16, device="cuda")
+        f.k_gemm(A, B, D, M, N, K, epi)
+        torch.cuda.synchronize()
+        outs.append(D.float())
+    if sk == "0":
+        assert torch.equal(outs[0], outs[1])
+    else:
+        torch.testing.assert_close(outs[1], outs[0], rtol=1e-2, atol=1e-2)
