@@ -92,8 +92,9 @@ ss_status ss_ipc_export(ss_ctx* ctx, int32_t max_tokens, void* handle_out_64_byt
 ss_status ss_ipc_open(ss_ctx* ctx, const void* handles);
 
 /* Paged KV pool: num_blocks blocks of block_size tokens for every layer and
- * this rank's KV heads. Layout per layer: [num_blocks][kv_heads_local][bs][hd]
- * bf16 for K and for V. */
+ * this rank's KV heads. Layout per layer: [num_blocks][kv_heads_local] pages of
+ * bs x hd bf16 for K and for V; inside a page, key r / dim d sits at
+ * (d/64)*64*bs + r*64 + (((d%64)/8) ^ (r%8))*8 + d%8 (pre-swizzled, bs = 16). */
 ss_status ss_kv_alloc(ss_ctx* ctx, int64_t num_blocks, int32_t block_size);
 
 /* Synchronous forward of one hybrid batch from HOST descriptor arrays.
@@ -222,8 +223,8 @@ ss_status ss_k_rope_append(ss_ctx* ctx, const void* qkv, void* q_out, const int3
  * q[T][nq][hd] -> o[T][nq][hd]. */
 ss_status ss_k_attention(ss_ctx* ctx, const ss_batch* batch, const void* q, void* o,
                          int32_t layer);
-/* Reads back / writes raw KV of one layer ([num_blocks][kvh][bs][hd] bf16
- * each for K and V) for tests. */
+/* Reads back / writes raw KV of one layer ([num_blocks][kvh] pre-swizzled
+ * pages, see ss_kv_alloc; bf16 each for K and V) for tests. */
 ss_status ss_kv_layer_ptrs(ss_ctx* ctx, int32_t layer, void** k_ptr, void** v_ptr);
 /* Device pointer of a weight tensor of this rank's shard: name in {"wqkv",
  * "wo", "wgu", "wdown", "attn_norm", "mlp_norm", "final_norm", "embed",

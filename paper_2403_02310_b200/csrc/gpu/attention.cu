@@ -21,9 +21,12 @@
 // Long key ranges are split across CTAs (split-KV); partial (m, l, O) go to a
 // workspace and attention_combine merges them in a fixed order (deterministic).
 //
-// K/V pages ([block][kv_head][16][hd], 4 KB contiguous at hd=128) are moved by
-// TMA (cp.async.bulk.tensor, SWIZZLE_128B) into a kStages-deep full/empty
-// mbarrier ring by a dedicated producer warp: no per-thread address math or
+// K/V pages ([block][kv_head][16][hd], 4 KB contiguous at hd=128) are stored
+// pre-swizzled (common.cuh kv_page_elem: per 64-column half, the SWIZZLE_128B
+// image of a 16 x 64 box), so 1D bulk copies (cp.async.bulk, 2 KB each) land
+// them into a kStages-deep full/empty mbarrier ring exactly as a swizzled
+// tensor-map load would — at the 1D engine's higher measured read ceiling
+// (profiles/r02/hbm_read_bench.txt) — issued by a dedicated producer warp: no per-thread address math or
 // block-table loads in the compute warps, and no CTA-wide barrier per tile.
 // S = QK^T and O += PV use mma.sync m16n8k16 (bf16 in, fp32 accumulate); the
 // decode path is HBM-bound, so the MMA flavour does not limit it.
@@ -102,14 +105,14 @@ template <int HD>
 __device__ __forceinline__ uint32_t swz_q(int row, int c) {
     return uint32_t(row * (HD * 2) + ((c ^ (row & 7)) << 4));
 }
-// K/V tile as written by TMA with SWIZZLE_128B: [c / 8 half][key][128 B].
+// K/V tile in shared memory (SWIZZLE_128B image): [c / 8 half][key][128 B].
 __device__ __forceinline__ uint32_t swz_kv(int key, int c) {
     return uint32_t((c >> 3) * (kKeysPerTile * 128) + key * 128 + (((c & 7) ^ (key & 7)) << 4));
 }
 
 // KPW = keys handled per warp per 64-key tile (64: row mode, 16: key mode).
 template <int HD, int KPW>
-__device__ __forceinline__ void attend(const AttnParams& p, const CUtensorMap* tmK, const CUtensorMap* tmV,
+__device__ __forceinline__ void attend(const AttnParams& p,
                                        const AttnItem& it, uint8_t* smem, int qrow_base, int kofs,
                                        float (&O)[HD / 8][4], float (&m)[2], float (&l)[2]) {
     using S = AttnSmem<HD>;
@@ -523,9 +526,7 @@ __device__ __forceinline__ void softmax_warps_tc(const AttnParams& p, const Attn
 
 // MODE 0: decode / mma.sync items; 1: tensor-core prefill, deep; 2: tensor-core prefill, compact.
 template <int HD, int MODE>
-__global__ void __launch_bounds__(MODE > 0 ? TcCfg<HD, MODE>::THREADS : (kWarps + 1) * 32) attention_kernel(const AttnParams p,
-                                                                      const __grid_constant__ CUtensorMap tmK,
-                                                                      const __grid_constant__ CUtensorMap tmV) {
+__global__ void __launch_bounds__(MODE > 0 ? TcCfg<HD, MODE>::THREADS : (kWarps + 1) * 32) attention_kernel(const AttnParams p) {
     using S = AttnSmem<HD>;
     constexpr bool TC = MODE > 0;
     using C = TcCfg<HD, MODE == 0 ? 2 : MODE>;
@@ -553,8 +554,6 @@ __global__ void __launch_bounds__(MODE > 0 ? TcCfg<HD, MODE>::THREADS : (kWarps 
     const int st0 = tc ? C::STAGE0 : S::Q_BYTES;
 
     if (threadIdx.x == 0) {
-        tma_prefetch(&tmK);
-        tma_prefetch(&tmV);
         for (int s = 0; s < nst; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], tc ? 1 : kWarps);  // tc: released by a tcgen05.commit
@@ -628,7 +627,7 @@ __global__ void __launch_bounds__(MODE > 0 ? TcCfg<HD, MODE>::THREADS : (kWarps 
         }
     }
 
-    if (warp == kProd) {  // ---- producer warp: K/V pages by TMA into the ring
+    if (warp == kProd) {  // ---- producer warp: K/V half-pages by bulk copy into the ring
         // Block ids come 32 pages (8 tiles) at a time from one coalesced warp load,
         // fetched a batch ahead, and reach the issuing lane by shuffle: no dependent
         // global load sits between two tiles' TMA issues.
@@ -662,9 +661,12 @@ __global__ void __launch_bounds__(MODE > 0 ? TcCfg<HD, MODE>::THREADS : (kWarps 
             if (lane < kOps) {
                 if (lane == 0) mbar_arrive_expect_tx(&full[st], 2 * S::KV_TILE);
                 const int kv = lane & 1, hh = (lane >> 1) % (HD / 64), pg = lane / (2 * (HD / 64));
-                const int32_t row = int32_t(p.layer_row0 + (int64_t(blk[pg]) * p.nkv_l + it.kv_head) * 16);
+                // the half-page is stored pre-swizzled (kv_page_elem): one 2 KB bulk copy lands
+                // the same shared-memory image a SWIZZLE_128B 16 x 64 tensor box would
+                const __nv_bfloat16* src = (kv ? p.vc : p.kc) + (int64_t(blk[pg]) * p.nkv_l + it.kv_head) * (16 * HD) +
+                                           hh * (16 * 64);
                 uint8_t* dst = smem + st0 + st * S::STAGE + kv * S::KV_TILE + hh * (kKeysPerTile * 128) + pg * 16 * 128;
-                tma_load_2d_hint(dst, kv ? &tmV : &tmK, hh * 64, row, &full[st], pol);
+                bulk_load_hint(dst, src, 16 * 128, &full[st], pol);
             }
             __syncwarp();
         }
@@ -691,7 +693,7 @@ __global__ void __launch_bounds__(MODE > 0 ? TcCfg<HD, MODE>::THREADS : (kWarps 
     } else {
     float O[HD / 8][4], m[2], l[2];
     if (!key_mode) {
-        attend<HD, 64>(p, &tmK, &tmV, it, smem, warp * 16, 0, O, m, l);
+        attend<HD, 64>(p, it, smem, warp * 16, 0, O, m, l);
         const int r0 = warp * 16 + (lane >> 2);
 #pragma unroll
         for (int dt = 0; dt < HD / 8; ++dt) {
@@ -704,7 +706,7 @@ __global__ void __launch_bounds__(MODE > 0 ? TcCfg<HD, MODE>::THREADS : (kWarps 
         return;
     }
 
-    attend<HD, 16>(p, &tmK, &tmV, it, smem, 0, warp * 16, O, m, l);
+    attend<HD, 16>(p, it, smem, 0, warp * 16, O, m, l);
     // merge the four warps' partial softmax states (K/V stages reused as scratch,
     // once every compute warp is past its last tile)
     asm volatile("bar.sync 1, %0;" ::"n"(kWarps * 32) : "memory");
@@ -773,7 +775,7 @@ __global__ void attention_combine_kernel(const AttnParams p) {
 }
 
 template <int HD>
-cudaError_t launch_hd(const AttnParams& p, const CUtensorMap& tk, const CUtensorMap& tv, cudaStream_t st) {
+cudaError_t launch_hd(const AttnParams& p, cudaStream_t st) {
     static bool attr[64] = {};
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
@@ -801,48 +803,43 @@ cudaError_t launch_hd(const AttnParams& p, const CUtensorMap& tk, const CUtensor
         pt.wait_at_end = 0;
         pd.wait_at_end = 1;
         cudaError_t e = launch_pdl(attention_kernel<HD, 2>, dim3(n_tc), dim3(TcCfg<HD, 2>::THREADS), TcCfg<HD, 2>::TOTAL,
-                                   st, 1, pt, tk, tv);
+                                   st, 1, pt);
         if (e != cudaSuccess || n_rest == 0) return e;
-        return launch_pdl(attention_kernel<HD, 0>, dim3(n_rest), bd, AttnSmem<HD>::TOTAL, st, 1, pd, tk, tv);
+        return launch_pdl(attention_kernel<HD, 0>, dim3(n_rest), bd, AttnSmem<HD>::TOTAL, st, 1, pd);
     }
     if (n_tc > 0 && p.tc == 2 && n_rest > 0) {
         // enough HBM-streaming decode CTAs to fill the machine: they go first, and the
         // compact prefill CTAs run beside them (in the SMs' remaining shared memory)
         pd.wait_at_end = 0;
         pt.wait_at_end = 1;
-        cudaError_t e = launch_pdl(attention_kernel<HD, 0>, dim3(n_rest), bd, AttnSmem<HD>::TOTAL, st, 1, pd, tk, tv);
+        cudaError_t e = launch_pdl(attention_kernel<HD, 0>, dim3(n_rest), bd, AttnSmem<HD>::TOTAL, st, 1, pd);
         if (e != cudaSuccess) return e;
         return launch_pdl(attention_kernel<HD, 2>, dim3(n_tc), dim3(TcCfg<HD, 2>::THREADS), TcCfg<HD, 2>::TOTAL, st, 1,
-                          pt, tk, tv);
+                          pt);
     }
     if (n_tc > 0) {  // prefill-heavy: the deep prefill kernel first, the decodes beside / after it
         pt.wait_at_end = 0;
         cudaError_t e =
             p.tc == 1 ? launch_pdl(attention_kernel<HD, 1>, dim3(n_tc), dim3(TcCfg<HD, 1>::THREADS), TcCfg<HD, 1>::TOTAL,
-                                   st, 1, pt, tk, tv)
+                                   st, 1, pt)
                       : launch_pdl(attention_kernel<HD, 3>, dim3(n_tc), dim3(TcCfg<HD, 3>::THREADS), TcCfg<HD, 3>::TOTAL,
-                                   st, 1, pt, tk, tv);
+                                   st, 1, pt);
         if (e != cudaSuccess || n_rest == 0) return e;
         pd.wait_at_end = 1;
     } else {
         pd.wait_at_end = 0;
     }
-    return n_rest > 0 ? launch_pdl(attention_kernel<HD, 0>, dim3(n_rest), bd, AttnSmem<HD>::TOTAL, st, 1, pd, tk, tv)
+    return n_rest > 0 ? launch_pdl(attention_kernel<HD, 0>, dim3(n_rest), bd, AttnSmem<HD>::TOTAL, st, 1, pd)
                       : cudaSuccess;
 }
 
 }  // namespace
 
-bool attention_tmaps(CUtensorMap* tk, CUtensorMap* tv, const void* kc, const void* vc, int64_t total_rows, int hd) {
-    return make_tmap_2d(tk, kc, uint64_t(total_rows), uint64_t(hd), 16, 64) &&
-           make_tmap_2d(tv, vc, uint64_t(total_rows), uint64_t(hd), 16, 64);
-}
-
-cudaError_t attention_launch(const AttnParams& p, const CUtensorMap& tk, const CUtensorMap& tv, cudaStream_t st) {
+cudaError_t attention_launch(const AttnParams& p, cudaStream_t st) {
     static_assert(AttnSmem<128>::BAR_OFF - AttnSmem<128>::Q_BYTES >= kWarps * 16 * 128 * 4 + kWarps * 16 * 8,
                   "key-mode merge scratch must fit in the K/V stages");
-    if (p.head_dim == 128) return launch_hd<128>(p, tk, tv, st);
-    if (p.head_dim == 64) return launch_hd<64>(p, tk, tv, st);
+    if (p.head_dim == 128) return launch_hd<128>(p, st);
+    if (p.head_dim == 64) return launch_hd<64>(p, st);
     return cudaErrorInvalidValue;
 }
 

@@ -103,12 +103,30 @@ __device__ __forceinline__ uint64_t l2_policy_evict_last() {
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
     return pol;
 }
+// Paged K/V page layout ([block][kv head] pages of 16 rows x hd): [hd/64 halves][16 rows][64]
+// bf16, and the 16-byte chunk j of row r stored at chunk j ^ (r & 7) — the exact image a
+// SWIZZLE_128B TMA box writes to shared memory, so attention streams each 2 KB half-page with
+// one 1D bulk copy (1D bulk reads run at 7.1-7.2 TB/s where 2D tensor-map boxes reach 6.7,
+// scripts/hbm_read_bench.cu). Element offset of (row r, column d) inside a page:
+__host__ __device__ __forceinline__ int kv_page_elem(int r, int d) {
+    return (d >> 6) * 1024 + r * 64 + ((((d & 63) >> 3) ^ (r & 7)) << 3) + (d & 7);
+}
+
 // 1D bulk copy global -> shared, completing on an mbarrier.
 __device__ __forceinline__ void bulk_load(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
             smem_u32(smem_dst)),
         "l"(reinterpret_cast<uint64_t>(gsrc)), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_load_hint(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar,
+                                               uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(gsrc)), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
         : "memory");
 }
 

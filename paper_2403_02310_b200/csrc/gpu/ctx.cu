@@ -229,7 +229,6 @@ struct ss_ctx {
     float* chain_part = nullptr;
     size_t chain_flag_cap = 0, chain_part_cap = 0;  // flag buffer: max tiles per phase (stride)
     unsigned long long* chain_trace = nullptr;  // SS_CHAIN_TRACE: [L][kChainTraceItems][8] timeline
-    CUtensorMap tm_k, tm_v;  // 2D TMA views of the paged K/V pools
 
     uint8_t* pinned = nullptr;
     size_t pinned_cap = 0;
@@ -1060,7 +1059,7 @@ ss_status enqueue_forward(ss_ctx* ctx, const ss_batch* b) {
         const AttnParams ap = attn_params(ctx, b, ctx->q, ctx->o, l);
         // two kernels when the batch has both tensor-core prefill tiles and decode items
         const int n_attn = (ap.tc && ap.n_tc > 0 && ap.n_items > ap.n_tc) ? 2 : 1;
-        RUN(launch(ctx, SS_K_ATTN, n_attn, [&] { return attention_launch(ap, ctx->tm_k, ctx->tm_v, ctx->st); }));
+        RUN(launch(ctx, SS_K_ATTN, n_attn, [&] { return attention_launch(ap, ctx->st); }));
         if (b->n_combs && !ctx->fused_combine)
             RUN(launch(ctx, SS_K_ATTN_COMBINE, 1, [&] { return attention_combine_launch(ap, ctx->st); }));
         if (chain) {
@@ -1641,8 +1640,6 @@ SS_API ss_status ss_kv_alloc(ss_ctx* ctx, int64_t num_blocks, int32_t block_size
     CK(cudaMemsetAsync(ctx->kc, 0, bytes, ctx->st));
     CK(cudaMemsetAsync(ctx->vc, 0, bytes, ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
-    if (!attention_tmaps(&ctx->tm_k, &ctx->tm_v, ctx->kc, ctx->vc, num_blocks * ctx->nkv_l * block_size * ctx->L, ctx->hd))
-        return fail(ctx, SS_CUDA_ERROR, "cuTensorMapEncodeTiled failed (KV pool)");
     ctx->nblocks = num_blocks;
     ++ctx->ws_gen;
     return SS_OK;
@@ -1904,7 +1901,7 @@ SS_API ss_status ss_k_attention(ss_ctx* ctx, const ss_batch* b, const void* q, v
     DevGuard dg(ctx->device);
     if (ss_status s = ensure_workspace(ctx, b->T, std::max(b->n_out, 1), b->part_rows)) return s;
     const AttnParams ap = attn_params(ctx, b, static_cast<const bf16*>(q), static_cast<bf16*>(o), layer);
-    if (ss_status s = launch(ctx, SS_K_ATTN, 1, [&] { return attention_launch(ap, ctx->tm_k, ctx->tm_v, ctx->st); })) return s;
+    if (ss_status s = launch(ctx, SS_K_ATTN, 1, [&] { return attention_launch(ap, ctx->st); })) return s;
     if (b->n_combs && !ctx->fused_combine)
         return launch(ctx, SS_K_ATTN_COMBINE, 1, [&] { return attention_combine_launch(ap, ctx->st); });
     return SS_OK;

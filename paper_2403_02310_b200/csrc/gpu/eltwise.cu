@@ -104,21 +104,22 @@ __global__ void rope_append_kernel(const __nv_bfloat16* __restrict__ qkv, __nv_b
         const float x0 = bf16_lo(lo), x1 = bf16_hi(lo), y0 = bf16_lo(hi), y1 = bf16_hi(hi);
         const uint32_t nlo = pack_bf16(x0 * c0.x - y0 * c0.y, x1 * c1.x - y1 * c1.y);
         const uint32_t nhi = pack_bf16(y0 * c0.x + x0 * c0.y, y1 * c1.x + x1 * c1.y);
-        __nv_bfloat16* dst;
         if (hh < nq) {
-            dst = q_out + (size_t(t) * nq + hh) * hd;
-        } else {
-            dst = kc + ((size_t(blk) * nkv + (hh - nq)) * bs + off) * hd;
+            __nv_bfloat16* dst = q_out + (size_t(t) * nq + hh) * hd;
+            *reinterpret_cast<uint32_t*>(dst + i) = nlo;
+            *reinterpret_cast<uint32_t*>(dst + i + half) = nhi;
+        } else {  // the page of (block, head), row `off` stored pre-swizzled (kv_page_elem)
+            __nv_bfloat16* page = kc + (size_t(blk) * nkv + (hh - nq)) * bs * hd;
+            *reinterpret_cast<uint32_t*>(page + kv_page_elem(int(off), i)) = nlo;
+            *reinterpret_cast<uint32_t*>(page + kv_page_elem(int(off), i + half)) = nhi;
         }
-        *reinterpret_cast<uint32_t*>(dst + i) = nlo;
-        *reinterpret_cast<uint32_t*>(dst + i + half) = nhi;
     }
     // v heads: straight copy, 16 B per thread
     const int vchunks = nkv * hd / 8;
     const __nv_bfloat16* vsrc = row + size_t(nq + nkv) * hd;
     for (int idx = threadIdx.x; idx < vchunks; idx += blockDim.x) {
         const int hh = idx / (hd / 8), c8 = (idx % (hd / 8)) * 8;
-        *reinterpret_cast<uint4*>(vc + ((size_t(blk) * nkv + hh) * bs + off) * hd + c8) =
+        *reinterpret_cast<uint4*>(vc + (size_t(blk) * nkv + hh) * bs * hd + kv_page_elem(int(off), c8)) =
             *reinterpret_cast<const uint4*>(vsrc + size_t(hh) * hd + c8);
     }
 }
@@ -476,7 +477,7 @@ __global__ void kv_fill_kernel(__nv_bfloat16* __restrict__ kb, __nv_bfloat16* __
         const int h = int((e / hd) % nkv_l), d = int(e % hd);
         const uint16_t v = ss_synth_kv(seed, layer0 + layer, which, rid, pos, kv_off + h, d, nkv_g, hd);
         const int64_t blk = bt[pos / bs];
-        const int64_t off = layer * lstride + ((blk * nkv_l + h) * bs + pos % bs) * hd + d;
+        const int64_t off = layer * lstride + (blk * nkv_l + h) * bs * hd + kv_page_elem(pos % bs, d);
         (which ? vb : kb)[off] = __ushort_as_bfloat16(v);
     }
 }

@@ -843,24 +843,29 @@ __global__ void __launch_bounds__(kThreads, 1)
                             ep[lane * 8 + (jj ^ (lane & 7))] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
                             ep[lane * 8 + ((jj + 4) ^ (lane & 7))] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
                         }
+                        // q: this row's head vector (+ i0); k / v: the page of (block, head), whose
+                        // row `off` is stored pre-swizzled (kv_page_elem)
+                        const bool is_q = hh < ea.nq;  // warp-uniform
                         __nv_bfloat16* dst = nullptr;
                         if (row < M) {
-                            if (hh < ea.nq) dst = ea.q_out + (size_t(row) * ea.nq + hh) * ea.hd;
-                            else if (hh < ea.nq + ea.nkv) dst = ea.kc + ((size_t(blk) * ea.nkv + (hh - ea.nq)) * ea.bs + off) * ea.hd;
-                            else dst = ea.vc + ((size_t(blk) * ea.nkv + (hh - ea.nq - ea.nkv)) * ea.bs + off) * ea.hd;
-                            dst += i0;
+                            if (is_q) dst = ea.q_out + (size_t(row) * ea.nq + hh) * ea.hd + i0;
+                            else if (hh < ea.nq + ea.nkv) dst = ea.kc + (size_t(blk) * ea.nkv + (hh - ea.nq)) * ea.bs * ea.hd;
+                            else dst = ea.vc + (size_t(blk) * ea.nkv + (hh - ea.nq - ea.nkv)) * ea.bs * ea.hd;
                         }
-                        // chunk k < 4 -> dst + 8k, else dst + hd/2 + 8(k-4)
+                        // chunk k < 4 -> column i0 + 8k, else i0 + hd/2 + 8(k-4)
                         __syncwarp();
                         if (pi < half + 4) TRACE2(8 + 3 * ((pi - half) >> 1));
                         const uint64_t dp = reinterpret_cast<uint64_t>(dst);
+                        const int colofs = cch < 4 ? cch * 8 : ea.hd / 2 + (cch - 4) * 8;
 #pragma unroll
                         for (int j = 0; j < 8; ++j) {
                             const int r = 4 * j + crow;
                             const uint64_t d = (uint64_t(__shfl_sync(0xffffffffu, uint32_t(dp >> 32), r)) << 32) |
                                                __shfl_sync(0xffffffffu, uint32_t(dp), r);
+                            const int roff = __shfl_sync(0xffffffffu, int(off), r);
                             if (d) {
-                                __nv_bfloat16* p = reinterpret_cast<__nv_bfloat16*>(d) + (cch < 4 ? cch * 8 : ea.hd / 2 + (cch - 4) * 8);
+                                __nv_bfloat16* p = reinterpret_cast<__nv_bfloat16*>(d) +
+                                                   (is_q ? colofs : kv_page_elem(roff, i0 + colofs));
                                 *reinterpret_cast<uint4*>(p) = ep[r * 8 + (cch ^ (r & 7))];
                             }
                         }
@@ -1525,22 +1530,25 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_chain_kernel(const __grid_co
                         ep[lane * 8 + (jj ^ (lane & 7))] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
                         ep[lane * 8 + ((jj + 4) ^ (lane & 7))] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
                     }
+                    const bool is_q = hh < ea.nq;  // k / v rows go into pre-swizzled pages (kv_page_elem)
                     __nv_bfloat16* dst = nullptr;
                     if (row < M) {
-                        if (hh < ea.nq) dst = ea.q_out + (size_t(row) * ea.nq + hh) * ea.hd;
-                        else if (hh < ea.nq + ea.nkv) dst = ea.kc + ((size_t(blk) * ea.nkv + (hh - ea.nq)) * ea.bs + off) * ea.hd;
-                        else dst = ea.vc + ((size_t(blk) * ea.nkv + (hh - ea.nq - ea.nkv)) * ea.bs + off) * ea.hd;
-                        dst += i0;
+                        if (is_q) dst = ea.q_out + (size_t(row) * ea.nq + hh) * ea.hd + i0;
+                        else if (hh < ea.nq + ea.nkv) dst = ea.kc + (size_t(blk) * ea.nkv + (hh - ea.nq)) * ea.bs * ea.hd;
+                        else dst = ea.vc + (size_t(blk) * ea.nkv + (hh - ea.nq - ea.nkv)) * ea.bs * ea.hd;
                     }
                     __syncwarp();
                     const uint64_t dp = reinterpret_cast<uint64_t>(dst);
+                    const int colofs = cch < 4 ? cch * 8 : ea.hd / 2 + (cch - 4) * 8;
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
                         const int r = 4 * j + crow;
                         const uint64_t d = (uint64_t(__shfl_sync(0xffffffffu, uint32_t(dp >> 32), r)) << 32) |
                                            __shfl_sync(0xffffffffu, uint32_t(dp), r);
+                        const int roff = __shfl_sync(0xffffffffu, int(off), r);
                         if (d) {
-                            __nv_bfloat16* pp = reinterpret_cast<__nv_bfloat16*>(d) + (cch < 4 ? cch * 8 : ea.hd / 2 + (cch - 4) * 8);
+                            __nv_bfloat16* pp = reinterpret_cast<__nv_bfloat16*>(d) +
+                                                (is_q ? colofs : kv_page_elem(roff, i0 + colofs));
                             *reinterpret_cast<uint4*>(pp) = ep[r * 8 + (cch ^ (r & 7))];
                         }
                     }

@@ -224,8 +224,7 @@ struct AttnParams {
                                  // dependency wait (the CTAs PDL lands on SMs the QKV GEMM leaves idle)
 };
 // 2D TMA views [L * nblocks * nkv * 16][hd] of the K and V pools (box 16 x 64, SWIZZLE_128B).
-bool attention_tmaps(CUtensorMap* tk, CUtensorMap* tv, const void* kc, const void* vc, int64_t total_rows, int hd);
-cudaError_t attention_launch(const AttnParams& p, const CUtensorMap& tk, const CUtensorMap& tv, cudaStream_t st);
+cudaError_t attention_launch(const AttnParams& p, cudaStream_t st);
 cudaError_t attention_combine_launch(const AttnParams& p, cudaStream_t st);
 
 // ------------------------------------------------------------------ K2/K4 elementwise

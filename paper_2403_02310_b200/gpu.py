@@ -245,6 +245,9 @@ class HybridForward:
         return torch.as_tensor(_Dev(p.value, (r.value, c.value), "<i2"), device="cuda").view(torch.bfloat16)
 
     def kv_layer(self, layer: int):
+        """Raw views [blocks][kv heads][16][hd] of layer `layer`'s K and V pools. Each
+        (block, head) page is stored pre-swizzled (the shared-memory image of a SWIZZLE_128B
+        box, csrc/gpu/common.cuh kv_page_elem): read values through kv_logical()."""
         import torch
 
         k, v = C.c_void_p(), C.c_void_p()
@@ -372,3 +375,20 @@ class PipelineGroup:
     def close(self):
         for s in self.stages:
             s.close()
+
+
+def kv_page_index(hd: int):
+    """[16][hd] flat element offsets of (row, column) inside one pre-swizzled K/V page
+    (csrc/gpu/common.cuh kv_page_elem)."""
+    import torch
+
+    r = torch.arange(16).view(16, 1)
+    d = torch.arange(hd).view(1, hd)
+    return (d // 64) * 1024 + r * 64 + ((((d % 64) // 8) ^ (r % 8)) * 8) + d % 8
+
+
+def kv_logical(pages):
+    """Logical [..., 16, hd] values of pre-swizzled pages (a kv_layer view or a slice of one)."""
+    idx = kv_page_index(pages.shape[-1]).to(pages.device).reshape(-1)
+    flat = pages.reshape(*pages.shape[:-2], -1)
+    return flat[..., idx].reshape(pages.shape)

@@ -178,6 +178,7 @@ def test_rope_append(small):
     torch.testing.assert_close(q_out.float(), _rope_ref(x[:, :s.num_q_heads], pos, s.rope_theta, s.head_dim),
                                rtol=1e-2, atol=1e-2)
     kc, vc = small.kv_layer(0)
+    kc, vc = gpu.kv_logical(kc), gpu.kv_logical(vc)  # pages are stored pre-swizzled
     blk, off = slot // 16, slot % 16
     k_got = kc[blk.long(), :, off.long()].float()  # [T, nkv, hd]
     v_got = vc[blk.long(), :, off.long()].float()
@@ -187,6 +188,7 @@ def test_rope_append(small):
 
 
 def attention_ref(q, kc, vc, a, G, hd):
+    kc, vc = gpu.kv_logical(kc), gpu.kv_logical(vc)  # the pool's pages are stored pre-swizzled
     out = torch.zeros_like(q, dtype=torch.float32)
     scale = 1.0 / math.sqrt(hd)
     nkv = kc.shape[1]
