@@ -154,6 +154,11 @@ __device__ __forceinline__ void attend(const AttnParams& p,
         uint8_t* sK = smem + S::Q_BYTES + st * S::STAGE;
         uint8_t* sV = sK + S::KV_TILE;
         mbar_wait(&full[st], uint32_t((t / kStages) & 1));
+#if defined(SS_ATTN_EXP) && SS_ATTN_EXP == 1  // dev experiment: consumers release stages unread
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+        continue;
+#endif
 
         // S = Q K^T for this warp's key slice
         float s[NT][4];
@@ -553,7 +558,9 @@ __global__ void __launch_bounds__(MODE > 0 ? TcCfg<HD, MODE>::THREADS : (kWarps 
     const int nst = tc ? C::STAGES : kStages;
     const int st0 = tc ? C::STAGE0 : S::Q_BYTES;
 
-    if (threadIdx.x == 0) {
+    // (mma.sync path: the producer warp initialises the barriers, so it can issue before the
+    // CTA-wide barrier below; the other warps touch them only after it)
+    if (threadIdx.x == (TC ? 0 : kProd * 32)) {
         for (int s = 0; s < nst; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], tc ? 1 : kWarps);  // tc: released by a tcgen05.commit
@@ -565,6 +572,69 @@ __global__ void __launch_bounds__(MODE > 0 ? TcCfg<HD, MODE>::THREADS : (kWarps 
         if (warp == 0) {
             if constexpr (NH == 2) tmem_alloc<512>(tslot);
             else tmem_alloc<256>(tslot);
+        }
+    }
+    // ---- K/V producer state (warp kProd). Block ids come 32 pages (8 tiles) at a time from
+    // one coalesced warp load, fetched a batch ahead, and reach the issuing lane by shuffle:
+    // no dependent global load sits between two tiles' issues.
+    int pr_ntiles = 0, pr_nvalid = 0, pr_t = 0;
+    int32_t pr_cur = 0, pr_nxt = 0;
+    uint64_t pr_pol = 0;
+    const int32_t* pr_bt = p.block_table + size_t(it.entry) * p.max_blocks;
+    const int pr_pg0 = it.key0 >> 4;  // key0 is a multiple of 64
+    auto pr_batch = [&](int b) {
+        const int lb = pr_pg0 + 32 * b + lane;
+        return __ldg(pr_bt + (lb < pr_nvalid ? lb : 0));  // pages past the context: a valid page, masked
+    };
+    auto pr_issue = [&](int t) {
+        if (t > 0 && (t & 7) == 0) {
+            pr_cur = pr_nxt;
+            if (t + 8 < pr_ntiles) pr_nxt = pr_batch((t >> 3) + 1);
+        }
+        int32_t blk[4];
+#pragma unroll
+        for (int pg = 0; pg < 4; ++pg) blk[pg] = __shfl_sync(0xffffffffu, pr_cur, ((t & 7) << 2) + pg);
+        const int st = t % nst;
+        // one 2 KB copy per lane: a tile's 4 pages x HD/64 halves x {K, V} issue in parallel
+        // (a single issuing thread serialises them: measured 1.5x slower)
+        constexpr int kOps = 4 * (HD / 64) * 2;
+        if (t >= nst) mbar_wait(&empty[st], uint32_t(((t / nst) - 1) & 1));
+        if (lane < kOps) {
+            if (lane == 0) mbar_arrive_expect_tx(&full[st], 2 * S::KV_TILE);
+            const int kv = lane & 1, hh = (lane >> 1) % (HD / 64), pg = lane / (2 * (HD / 64));
+            // the half-page is stored pre-swizzled (kv_page_elem): one 2 KB bulk copy lands
+            // the same shared-memory image a SWIZZLE_128B 16 x 64 tensor box would
+            const __nv_bfloat16* src =
+                (kv ? p.vc : p.kc) + (int64_t(blk[pg]) * p.nkv_l + it.kv_head) * (16 * HD) + hh * (16 * 64);
+            uint8_t* dst = smem + st0 + st * S::STAGE + kv * S::KV_TILE + hh * (kKeysPerTile * 128) + pg * 16 * 128;
+            bulk_load_hint(dst, src, 16 * 128, &full[st], pr_pol);
+        }
+        __syncwarp();
+    };
+    if (warp == kProd) {
+        // the item list, block tables and lengths were uploaded before the forward's first kernel
+        pr_ntiles = TC ? max(tc_tiles(p, it, 0), NH > 1 ? tc_tiles(p, it, 1) : 0)
+                       : (it.key1 - it.key0 + kKeysPerTile - 1) / kKeysPerTile;
+        pr_nvalid = (p.ctx_len[it.entry] + 15) >> 4;
+        pr_cur = pr_batch(0);
+        pr_nxt = pr_ntiles > 8 ? pr_batch(1) : 0;
+        // a decode's K/V streams through once: first out of L2, so the chunk's freshly
+        // appended K/V and the next projection's operands stay resident
+        pr_pol = it.nrows <= 16 ? ((p.kv_hint & 1) ? l2_policy_evict_first() : l2_policy_evict_normal())
+                                : ((p.kv_hint & 2) ? l2_policy_evict_last() : l2_policy_evict_normal());
+        if constexpr (!TC) {
+            if (!p.wait_at_end) {
+                // Tiles of cached keys only (positions before this step's tokens) do not depend on
+                // the preceding kernels: the forward's first kernel passes its grid-dependency
+                // wait before it lets any later kernel start, so every earlier step's K/V writes
+                // are complete. Up to a ring's worth is in flight before this CTA's wait — while
+                // PDL keeps it resident beside the QKV GEMM's tail.
+                __syncwarp();  // barrier init (lane 0) before any lane issues
+                const int ntok = p.cu_q[it.entry + 1] - p.cu_q[it.entry];
+                const int cached = (p.ctx_len[it.entry] - ntok - it.key0) / kKeysPerTile;
+                const int npre = min(min(cached, nst), pr_ntiles);
+                for (; pr_t < npre; ++pr_t) pr_issue(pr_t);
+            }
         }
     }
     // Grid dependencies (see attention_launch): the first of the two attention launches
@@ -628,48 +698,7 @@ __global__ void __launch_bounds__(MODE > 0 ? TcCfg<HD, MODE>::THREADS : (kWarps 
     }
 
     if (warp == kProd) {  // ---- producer warp: K/V half-pages by bulk copy into the ring
-        // Block ids come 32 pages (8 tiles) at a time from one coalesced warp load,
-        // fetched a batch ahead, and reach the issuing lane by shuffle: no dependent
-        // global load sits between two tiles' TMA issues.
-        const int ntiles = TC ? max(tc_tiles(p, it, 0), NH > 1 ? tc_tiles(p, it, 1) : 0)
-                              : (it.key1 - it.key0 + kKeysPerTile - 1) / kKeysPerTile;
-        const int32_t* bt = p.block_table + size_t(it.entry) * p.max_blocks;
-        const int nvalid = (p.ctx_len[it.entry] + 15) >> 4;
-        const int pg0 = it.key0 >> 4;  // key0 is a multiple of 64
-        auto batch = [&](int b) {
-            const int lb = pg0 + 32 * b + lane;
-            return __ldg(bt + (lb < nvalid ? lb : 0));  // pages past the context: a valid page, masked
-        };
-        int32_t cur = batch(0), nxt = ntiles > 8 ? batch(1) : 0;
-        // a decode's K/V streams through once: first out of L2, so the chunk's freshly
-        // appended K/V and the next projection's operands stay resident
-        const uint64_t pol = it.nrows <= 16 ? ((p.kv_hint & 1) ? l2_policy_evict_first() : l2_policy_evict_normal())
-                                            : ((p.kv_hint & 2) ? l2_policy_evict_last() : l2_policy_evict_normal());
-        for (int t = 0; t < ntiles; ++t) {
-            if (t > 0 && (t & 7) == 0) {
-                cur = nxt;
-                if (t + 8 < ntiles) nxt = batch((t >> 3) + 1);
-            }
-            int32_t blk[4];
-#pragma unroll
-            for (int pg = 0; pg < 4; ++pg) blk[pg] = __shfl_sync(0xffffffffu, cur, ((t & 7) << 2) + pg);
-            const int st = t % nst;
-            // one box per lane: a tile's 4 pages x HD/64 halves x {K, V} loads issue in
-            // parallel (a single issuing thread serialises them: measured 1.5x slower)
-            constexpr int kOps = 4 * (HD / 64) * 2;
-            if (t >= nst) mbar_wait(&empty[st], uint32_t(((t / nst) - 1) & 1));
-            if (lane < kOps) {
-                if (lane == 0) mbar_arrive_expect_tx(&full[st], 2 * S::KV_TILE);
-                const int kv = lane & 1, hh = (lane >> 1) % (HD / 64), pg = lane / (2 * (HD / 64));
-                // the half-page is stored pre-swizzled (kv_page_elem): one 2 KB bulk copy lands
-                // the same shared-memory image a SWIZZLE_128B 16 x 64 tensor box would
-                const __nv_bfloat16* src = (kv ? p.vc : p.kc) + (int64_t(blk[pg]) * p.nkv_l + it.kv_head) * (16 * HD) +
-                                           hh * (16 * 64);
-                uint8_t* dst = smem + st0 + st * S::STAGE + kv * S::KV_TILE + hh * (kKeysPerTile * 128) + pg * 16 * 128;
-                bulk_load_hint(dst, src, 16 * 128, &full[st], pol);
-            }
-            __syncwarp();
-        }
+        for (int t = pr_t; t < pr_ntiles; ++t) pr_issue(t);
         if (p.wait_at_end) pdl_wait();
         return;
     }

@@ -20,9 +20,11 @@ __device__ __forceinline__ float warp_sum(float v) {
 __global__ void embed_kernel(const int32_t* __restrict__ tokens, const __nv_bfloat16* __restrict__ table,
                              float* __restrict__ x, __nv_bfloat16* __restrict__ xb, float* __restrict__ ssq, int h,
                              uint32_t* __restrict__ epoch_ctr, uint32_t epoch_stride) {
-    pdl_launch_dependents();
+    // The forward's first kernel: the previous forward is complete (PDL completion chain)
+    // before any later kernel of this one may start — the attention producers read cached
+    // K/V pages before their own grid-dependency wait — and its epochs are no longer read.
     pdl_wait();
-    // previous forward complete (PDL completion chain): its epochs are no longer read
+    pdl_launch_dependents();
     if (epoch_ctr && blockIdx.x == 0 && threadIdx.x == 0) *epoch_ctr += epoch_stride;
     const int t = blockIdx.x;
     const uint4* src = reinterpret_cast<const uint4*>(table + size_t(tokens[t]) * h);

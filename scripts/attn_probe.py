@@ -15,6 +15,9 @@ cases = {
     "chunk480@2048": [host.BatchEntry(0, P, 480, 2048)],
     "chunk2016@0": [host.BatchEntry(0, P, 2016, 0)],
     "decodes64": [host.BatchEntry(i, D, 1, 4096) for i in range(64)],
+    "decodes37": [host.BatchEntry(i, D, 1, 4096) for i in range(37)],  # 296 pairs: 2 per SM
+    "decodes19": [host.BatchEntry(i, D, 1, 4096) for i in range(19)],
+    "decodes32@8k": [host.BatchEntry(i, D, 1, 8192) for i in range(32)],
 }
 only = os.environ.get("ONLY")
 for cname, ents in cases.items():

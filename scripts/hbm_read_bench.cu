@@ -246,7 +246,125 @@ void run(const uint8_t* buf, size_t total, int ctas_per_sm, int sms) {
            double(per) * ctas_r / (best * 1e-3) / 1e12);
 }
 
-int main() {
+// The decode attention producer without the attention: CTA (seq e, head h) of NSEQ x 8 streams
+// its sequence's 64 pages (4096 keys) of K and V from two paged pools ([block][8 heads][16][128]
+// bf16, a sequence's blocks consecutive), a 64-key tile (4 pages x 2 halves x {K, V} = 16 ops of
+// 2 KB, one per lane) per 32 KB stage, 3 stages; HINT: L2 evict-first cache hint as the kernel.
+template <int HINT>
+__global__ void __launch_bounds__(64) paged_kernel(const uint8_t* kp, const uint8_t* vp, int npages) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    constexpr int STAGES = 3, CHUNK = 32768;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * CHUNK);
+    uint64_t* empty = full + STAGES;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s32(&full[s])));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s32(&empty[s])));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int e = blockIdx.x / 8, h = blockIdx.x % 8, lane = threadIdx.x & 31;
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    const int n = npages / 4;
+    if (threadIdx.x < 32) {
+        for (int i = 0; i < n; ++i) {
+            const int s = i % STAGES;
+            if (i >= STAGES) wait(&empty[s], ((i / STAGES) - 1) & 1);
+            if (lane == 0)
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s32(&full[s])), "r"(CHUNK) : "memory");
+            __syncwarp();
+            if (lane < 16) {
+                const int kv = lane & 1, hh = (lane >> 1) & 1, pg = lane >> 2;
+                const uint8_t* src = (kv ? vp : kp) + ((size_t(e) * npages + i * 4 + pg) * 8 + h) * 4096 + hh * 2048;
+                const uint32_t dst = s32(smem + s * CHUNK + kv * 16384 + hh * 8192 + pg * 2048);
+                if (HINT)
+                    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+                                 ::"r"(dst), "l"(src), "r"(2048), "r"(s32(&full[s])), "l"(pol) : "memory");
+                else
+                    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                                 ::"r"(dst), "l"(src), "r"(2048), "r"(s32(&full[s])) : "memory");
+            }
+            __syncwarp();
+        }
+    } else if (threadIdx.x == 32) {
+        for (int i = 0; i < n; ++i) {
+            const int s = i % STAGES;
+            wait(&full[s], (i / STAGES) & 1);
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s32(&empty[s])) : "memory");
+        }
+    }
+}
+
+template <int HINT>
+void run_paged(const uint8_t* buf, int nseq, int npages) {
+    auto k = paged_kernel<HINT>;
+    const int smem = 100 * 1024;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const size_t pool = size_t(nseq) * npages * 8 * 4096;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    float best = 1e9f;
+    for (int rep = 0; rep < 7; ++rep) {
+        cudaEventRecord(e0);
+        k<<<nseq * 8, 64, smem>>>(buf, buf + pool, npages);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (ms < best) best = ms;
+    }
+    printf("paged K+V, %d seqs x 8 heads x %d pages%s: %6.1f us, %.2f TB/s\n", nseq, npages,
+           HINT ? ", evict-first hint" : "", best * 1e3, 2.0 * pool / (best * 1e-3) / 1e12);
+}
+
+// The decode attention's shape: NCTAS CTAs (2 resident per SM by shared memory) each streaming
+// an equal slice of BYTES (decodes32: 256 (sequence, kv head) pairs x 2 MB of K+V = 537 MB).
+template <int STAGES, int CHUNK, int OP>
+void run_n(const uint8_t* buf, size_t bytes, int nctas) {
+    auto k = read_kernel<STAGES, CHUNK, OP, 0>;
+    const int smem = 100 * 1024;  // as the attention CTA: two per SM
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const size_t per = (bytes / nctas) / CHUNK * CHUNK;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    float best = 1e9f;
+    for (int rep = 0; rep < 7; ++rep) {
+        cudaEventRecord(e0);
+        k<<<nctas, 64, smem>>>(buf, per, 0);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (ms < best) best = ms;
+    }
+    printf("%4d CTAs x %7.3f MB (3 x 32 KB ring, %d B ops): %6.1f us, %.2f TB/s\n", nctas, per / 1e6, OP, best * 1e3,
+           double(per) * nctas / (best * 1e-3) / 1e12);
+}
+
+int main(int argc, char** argv) {
+    if (argc > 1) {  // decode-attention occupancy shapes only
+        int sms = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+        const size_t total = size_t(2) << 30;
+        uint8_t* buf;
+        cudaMalloc(&buf, total);
+        cudaMemset(buf, 1, total);
+        const size_t b32 = size_t(256) * 4096 * 128 * 2 * 2;
+        for (int n : {128, 148, 192, 256, 296, 384, 512, 592}) run_n<3, 32768, 2048>(buf, b32, n);
+        for (int n : {256, 296, 512, 592}) run_n<3, 32768, 2048>(buf, 2 * b32, n);
+        run_paged<0>(buf, 32, 256);
+        run_paged<1>(buf, 32, 256);
+        run_paged<0>(buf, 32, 512);
+        run_paged<1>(buf, 32, 512);
+        run_paged<0>(buf, 64, 256);
+        run_paged<1>(buf, 64, 256);
+        printf("%s\n", cudaGetErrorString(cudaGetLastError()));
+        return 0;
+    }
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     const size_t total = size_t(2) << 30;
