@@ -2,11 +2,14 @@
 // HBM-streaming decode attention, which only reads. CTAS_PER_SM CTAs per SM each stream a
 // distinct contiguous slice of a 2 GiB buffer through a STAGES x CHUNK shared-memory ring
 // (cp.async.bulk, mbarrier completion; the consumer just releases stages).
-//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o scripts/hbm_read_bench scripts/hbm_read_bench.cu
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o scripts/hbm_read_bench scripts/hbm_read_bench.cu -lcuda -lcublas
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <unistd.h>
+#include <cublas_v2.h>
+#include <cuda_bf16.h>
 
 __device__ __forceinline__ uint32_t s32(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
 __device__ __forceinline__ void wait(uint64_t* b, uint32_t ph) {
@@ -250,9 +253,12 @@ void run(const uint8_t* buf, size_t total, int ctas_per_sm, int sms) {
 // its sequence's 64 pages (4096 keys) of K and V from two paged pools ([block][8 heads][16][128]
 // bf16, a sequence's blocks consecutive), a 64-key tile (4 pages x 2 halves x {K, V} = 16 ops of
 // 2 KB, one per lane) per 32 KB stage, 3 stages; HINT: L2 evict-first cache hint as the kernel.
+__device__ unsigned long long g_clk[4];
 template <int HINT>
 __global__ void __launch_bounds__(64) paged_kernel(const uint8_t* kp, const uint8_t* vp, int npages) {
     extern __shared__ __align__(1024) uint8_t smem[];
+    unsigned long long c0 = clock64(), t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     constexpr int STAGES = 3, CHUNK = 32768;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * CHUNK);
     uint64_t* empty = full + STAGES;
@@ -294,6 +300,12 @@ __global__ void __launch_bounds__(64) paged_kernel(const uint8_t* kp, const uint
             wait(&full[s], (i / STAGES) & 1);
             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s32(&empty[s])) : "memory");
         }
+        if (blockIdx.x == 0) {
+            unsigned long long t1;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+            g_clk[0] = clock64() - c0;
+            g_clk[1] = t1 - t0;
+        }
     }
 }
 
@@ -318,6 +330,47 @@ void run_paged(const uint8_t* buf, int nseq, int npages) {
     }
     printf("paged K+V, %d seqs x 8 heads x %d pages%s: %6.1f us, %.2f TB/s\n", nseq, npages,
            HINT ? ", evict-first hint" : "", best * 1e3, 2.0 * pool / (best * 1e-3) / 1e12);
+}
+
+// SM clock vs HBM-streaming throughput: the paged producer pattern (decodes32 volume) timed
+// right after R back-to-back cuBLAS bf16 GEMMs (8192^3) that drive the board to its power cap,
+// so it runs at the clock the power controller left; the clock is read inside the kernel
+// (clock64 / globaltimer of CTA 0).
+void run_hot(const uint8_t* buf) {
+    cublasHandle_t h;
+    cublasCreate(&h);
+    const int n = 8192;
+    __nv_bfloat16 *A, *B, *Cm;
+    cudaMalloc(&A, size_t(n) * n * 2);
+    cudaMalloc(&B, size_t(n) * n * 2);
+    cudaMalloc(&Cm, size_t(n) * n * 2);
+    cudaMemset(A, 0, size_t(n) * n * 2);
+    cudaMemset(B, 0, size_t(n) * n * 2);
+    const float one = 1.f, zero = 0.f;
+    auto k = paged_kernel<1>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    const size_t pool = size_t(32) * 256 * 8 * 4096;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    for (int R : {0, 0, 2, 8, 32, 128, 0, 0}) {
+        if (R == 0) cudaDeviceSynchronize(), usleep(300000);  // idle: clocks recover
+        for (int r = 0; r < R; ++r)
+            cublasGemmEx(h, CUBLAS_OP_N, CUBLAS_OP_N, n, n, n, &one, A, CUDA_R_16BF, n, B, CUDA_R_16BF, n, &zero, Cm,
+                         CUDA_R_16BF, n, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
+        cudaEventRecord(e0);
+        k<<<256, 64, 100 * 1024>>>(buf, buf + pool, 256);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        unsigned long long c[2];
+        cudaMemcpyFromSymbol(c, g_clk, sizeof(c));
+        printf("after %3d GEMMs: paged K+V decodes32 %6.1f us, %.2f TB/s, SM clock %4.0f MHz, %.0f B/SM-clk\n", R,
+               ms * 1e3, 2.0 * pool / (ms * 1e-3) / 1e12, double(c[0]) / double(c[1]) * 1e3,
+               2.0 * pool / (ms * 1e-3) / (double(c[0]) / double(c[1]) * 1e9));
+    }
+    cublasDestroy(h);
 }
 
 // The decode attention's shape: NCTAS CTAs (2 resident per SM by shared memory) each streaming
@@ -362,6 +415,7 @@ int main(int argc, char** argv) {
         run_paged<1>(buf, 32, 512);
         run_paged<0>(buf, 64, 256);
         run_paged<1>(buf, 64, 256);
+        run_hot(buf);
         printf("%s\n", cudaGetErrorString(cudaGetLastError()));
         return 0;
     }
