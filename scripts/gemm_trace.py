@@ -59,7 +59,10 @@ if mode == "fwd":
     from paper_2403_02310_b200 import host
     shape = gpu.MODELS[os.environ.get("MODEL", "mistral7b")].with_layers(1)
     f = gpu.HybridForward(shape, weight_seed=1234)
-    d = host.Descriptor.canonical(512, 32, 4096, 0, vocab=shape.vocab)
+    if os.environ.get("DECODE"):  # 32 decodes at 4096, no chunk (the TBT-critical step)
+        d = host.Descriptor.build([host.BatchEntry(i, "decode", 1, 4096) for i in range(32)], vocab=shape.vocab)
+    else:
+        d = host.Descriptor.canonical(512, 32, 4096, 0, vocab=shape.vocab)
     f.kv_alloc(d.pool_blocks)
     f.fill_descriptor_prefixes(d, seed=5)
     b = f.upload(d)
