@@ -796,6 +796,7 @@ ss_status gemm(ss_ctx* ctx, int cls, const CUtensorMap& ta, WMaps& tb, int M, in
     p.force_splits = ctx->tu.gemm_splits;
     p.debug = ctx->tu.gemm_debug;
     p.max_groups = ctx->tu.gemm_max_groups;
+    p.dsm = ctx->tu.gemm_dsm;
     p.ea = ea;
     p.ea.l2hint = ctx->tu.gemm_l2hint;
     p.ea.epoch_base = ctx->d_epoch;

@@ -81,6 +81,24 @@ __device__ __forceinline__ uint32_t peer_addr(const void* p, uint32_t rank) {
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
     return r;
 }
+// Wait that acquires at cluster scope: the phase was completed by another CTA's arrive.
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+    uint32_t ok = 0, spins = 0;
+    while (!ok) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+        if (++spins == (1u << 28)) __trap();
+    }
+}
+// Bulk copy from this CTA's shared memory into another cluster CTA's, completing on that
+// CTA's mbarrier (both cluster addresses from peer_addr).
+__device__ __forceinline__ void bulk_s2cluster(uint32_t dst_cluster, const void* src, uint32_t bytes,
+                                               uint32_t bar_cluster) {
+    asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(dst_cluster), "r"(smem_u32(src)), "r"(bytes), "r"(bar_cluster) : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
@@ -339,7 +357,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M_rows,
                         int row0, int N, int K, void* __restrict__ out, int ldo, int num_mt, int num_tiles,
                         float* __restrict__ part, uint32_t* __restrict__ flags, uint32_t epoch, int sk_mode,
-                        int sk_slices, const EpiArgs ea) {
+                        int sk_slices, int dsm, const EpiArgs ea) {
     using Cfg = GemmCfg<CG, BN, AR>;
     constexpr int STAGES = Cfg::STAGES;
     // rows [row0, row0 + M_rows) of A / the output / every row-indexed epilogue operand
@@ -354,7 +372,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + 2;
     uint64_t* ebar = tempty + 2;  // one per epilogue warp (staged fixup loads)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ebar + 8);
+    uint64_t* gobar = ebar + 8;   // dsm: per epilogue warp, slice 0 opened its receive buffers
+    uint64_t* donebar = gobar + 8;  // dsm: per epilogue warp, slice 0 holds this slice's partial
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(donebar + 8);
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
@@ -385,12 +405,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&tfull[a], 1);
             mbar_init(&tempty[a], 8 * CG);  // every epilogue warp of the group
         }
-        for (int a = 0; a < 8; ++a) mbar_init(&ebar[a], 1);
+        for (int a = 0; a < 8; ++a) {
+            mbar_init(&ebar[a], 1);
+            mbar_init(&gobar[a], 1);
+            mbar_init(&donebar[a], 1);
+        }
         mbar_fence_init();
     }
     if (warp == 1) tmem_alloc_cg<CG>(tmem_slot, Cfg::TMEM_COLS);
     tc_fence_before();
-    if constexpr (CG == 2) cluster_sync();
+    if (CG == 2 || dsm > 1) cluster_sync();  // dsm: barriers initialised before any remote arrive
     else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
@@ -675,7 +699,39 @@ __global__ void __launch_bounds__(kThreads, 1)
             const bool last_seg = !peek.next(nx);
             constexpr int kStg = ((BN / 32 + 1) / 2) * 1024;  // staging floats per epilogue warp
             float* stg = reinterpret_cast<float*>(smem) + ew * kStg;
-            if (kb0 > 0 && last_seg) {
+            // dsm > 1: this tile's dsm K slices are one thread-block cluster (slice = rank, one
+            // segment per CTA, rows in TMEM lane quarter 0 only). Slice 0 opens its idle ring as
+            // receive buffers ([slice - 1][half][chunk] 4 KB images), each other slice copies its
+            // swizzled partial chunks there with shared::cluster bulk copies completing on slice
+            // 0's barrier, and slice 0 adds them in slice order: no global round trips or flags.
+            if (dsm > 1 && rbase >= M) {
+                // a lane quarter without rows: nothing to exchange or store
+            } else if (dsm > 1 && kb0 > 0) {
+                const int sl = gid % dsm, nmine = (BN / 32 - half + 1) / 2;
+                int i = 0;
+#pragma unroll 1
+                for (int c = half; c < BN / 32; c += 2, ++i) {
+                    uint32_t v[32];
+                    tmem_ld32(t_row + uint32_t(c * 32), v);
+                    tmem_wait_ld();
+                    float4* s4 = reinterpret_cast<float4*>(stg + i * 1024 + lane * 32);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        s4[j ^ (lane & 7)] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                                         __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+                }
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_wait_cluster(&gobar[ew], 0);
+                    const float* rb = reinterpret_cast<const float*>(smem) + size_t((sl - 1) * 2 + half) * nmine * 1024;
+                    const uint32_t bar = peer_addr(&ebar[ew], 0);
+                    for (int k = 0; k < nmine; ++k) bulk_s2cluster(peer_addr(rb + k * 1024, 0), stg + k * 1024, 4096, bar);
+                    mbar_wait_cluster(&donebar[ew], 0);  // slice 0 holds the partial: this CTA may exit
+                }
+                __syncwarp();
+                TRACE2(3);
+            } else if (kb0 > 0 && last_seg) {
                 // non-head piece, ring idle: TMEM -> swizzled smem -> one 4 KB bulk store per chunk
                 int i = 0;
 #pragma unroll 1
@@ -728,7 +784,49 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // (groups gid + P, gid + 2P, ... hold them: the same member of the
                 // following super-groups)
                 int g_last = gid;  // last group holding a piece of this tile
-                if (kb1 < num_kb) {
+                if (dsm > 1) {
+                    // slice 0 of a cluster split (see above): every MMA of this CTA has retired,
+                    // so the ring is free for the other slices' partials
+                    const int nmine = (BN / 32 - half + 1) / 2;
+                    if (lane == 0) {
+                        mbar_arrive_expect_tx(&ebar[ew], uint32_t((dsm - 1) * nmine) * 4096u);
+                        for (int r = 1; r < dsm; ++r) mbar_arrive_cluster(peer_addr(&gobar[ew], uint32_t(r)));
+                    }
+                    mbar_wait(&ebar[ew], eph);
+                    eph ^= 1;
+                    TRACE2(4);
+                    if (lane == 0)
+                        for (int r = 1; r < dsm; ++r) mbar_arrive_cluster(peer_addr(&donebar[ew], uint32_t(r)));
+#pragma unroll 1
+                    for (int sl = 1; sl < dsm; ++sl) {
+                        const float* rb = reinterpret_cast<const float*>(smem) + size_t((sl - 1) * 2 + half) * nmine * 1024;
+                        int i = 0;
+#pragma unroll 1
+                        for (int c = half; c < BN / 32; c += 2, ++i) {
+                            uint32_t v[32];
+                            tmem_ld32(t_row + uint32_t(c * 32), v);
+                            tmem_wait_ld();
+                            const float4* s4 = reinterpret_cast<const float4*>(rb + i * 1024 + lane * 32);
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) {
+                                const float4 a = s4[j ^ (lane & 7)];
+                                v[4 * j + 0] = __float_as_uint(__uint_as_float(v[4 * j + 0]) + a.x);
+                                v[4 * j + 1] = __float_as_uint(__uint_as_float(v[4 * j + 1]) + a.y);
+                                v[4 * j + 2] = __float_as_uint(__uint_as_float(v[4 * j + 2]) + a.z);
+                                v[4 * j + 3] = __float_as_uint(__uint_as_float(v[4 * j + 3]) + a.w);
+                            }
+                            tmem_st32(t_row + uint32_t(c * 32), v);
+                        }
+                        tmem_wait_st();
+                    }
+                    __syncwarp();
+                    // the two warps of this TMEM quarter swap chunk sets in the epilogue
+                    TRACE2(5);
+                    tc_fence_before();
+                    named_bar(1 + q, 64);
+                    tc_fence_after();
+                    TRACE2(6);
+                } else if (kb1 < num_kb) {
                     if (sk_mode == 2) {
                         g_last = gid + sk_slices - 1;
                     } else {
@@ -1015,6 +1113,7 @@ constexpr int kMaxDevices = 64;
 struct DevOnce {
     bool attr[kMaxDevices] = {};
     int resident[kMaxDevices] = {};
+    int clusters[kMaxDevices][9] = {};  // co-resident clusters of s CTAs (dsm), 0 = not measured
 };
 
 template <int CG, int BN, int EPI, int AR = 128, int MC = 1>
@@ -1080,11 +1179,39 @@ cudaError_t launch_t(const GemmPlan& p, cudaStream_t st) {
     // tiles or M-lockstep stream-K over an even M-tile count, an even number of pairs
     if (MC == 2 && ((mode != 0 && mode != 3) || (num_mt & 1) || (groups & 1))) return cudaErrorInvalidConfiguration;
     cfg.gridDim = dim3(CG * groups);
+    // Split-K over thread-block clusters (dsm): single-CTA tiles of a decode-sized batch (all
+    // rows in one TMEM lane quarter), every tile split (one wave), the S slices of a tile one
+    // cluster — the partials move through distributed shared memory instead of global memory
+    // and flags. Only when all the clusters are co-resident (they run one wave).
+    int dsm = 0;
+    if (CG == 1 && MC == 1 && p.dsm && mode == 2 && groups == tiles * S && S >= 2 && S <= 8 && p.M <= 32 &&
+        (S - 1) * 2 * ((BN / 32 + 1) / 2) * 4096 <= Cfg::STAGES * Cfg::STAGE_BYTES) {
+        int& nc = once.clusters[dev][S];
+        if (nc == 0) {
+            cudaLaunchConfig_t c2 = cfg;
+            cudaLaunchAttribute a2[1];
+            a2[0].id = cudaLaunchAttributeClusterDimension;
+            a2[0].val.clusterDim.x = unsigned(S);
+            a2[0].val.clusterDim.y = 1;
+            a2[0].val.clusterDim.z = 1;
+            c2.attrs = a2;
+            c2.numAttrs = 1;
+            c2.gridDim = dim3(S * (p.num_sms / S));
+            if (cudaOccupancyMaxActiveClusters(&nc, kern, &c2) != cudaSuccess || nc <= 0) {
+                cudaGetLastError();
+                nc = -1;
+            }
+        }
+        if (nc >= tiles) {
+            dsm = S;
+            attr[0].val.clusterDim.x = unsigned(S);
+        }
+    }
     if (p.debug)
-        fprintf(stderr, "gemm cg=%d bn=%d mc=%d epi=%d M=%d N=%d K=%d tiles=%d resident=%d mode=%d groups=%d\n", CG,
-                BN, MC, EPI, p.M, p.N, p.K, tiles, resident, mode, groups);
+        fprintf(stderr, "gemm cg=%d bn=%d mc=%d epi=%d M=%d N=%d K=%d tiles=%d resident=%d mode=%d groups=%d dsm=%d\n",
+                CG, BN, MC, EPI, p.M, p.N, p.K, tiles, resident, mode, groups, dsm);
     return cudaLaunchKernelEx(&cfg, kern, p.tmA, p.tmB, p.M, p.row0, p.N, p.K, p.out, p.ldo, num_mt, tiles, p.part,
-                              p.flags, p.epoch, mode, S, p.ea);
+                              p.flags, p.epoch, mode, S, dsm, p.ea);
 }
 
 // Tile shapes compiled: CG=2 pairs with BN in steps of 32, CG=1 with 128 / 256.
@@ -1771,6 +1898,7 @@ Tuning tuning_from_env() {
     if (getenv("SS_CHAIN_DEBUG")) t.chain_debug = 1;
     geti("SS_CHAIN_TRACE", t.chain_trace);
     geti("SS_GEMM_MAXG", t.gemm_max_groups);
+    geti("SS_GEMM_DSM", t.gemm_dsm);
     geti("SS_GEMM_MC", t.gemm_mc);
     static const char* names[5] = {"SS_GEMM_QKV", "SS_GEMM_O", "SS_GEMM_GATEUP", "SS_GEMM_DOWN", "SS_GEMM_LMHEAD"};
     for (int i = 0; i < 5; ++i)
@@ -1796,6 +1924,36 @@ bool make_tmap_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols
     return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Co-resident thread-block clusters of s single-CTA GEMM CTAs on this device (the dsm split
+// needs all of a launch's clusters resident at once): measured once per device and size.
+int gemm_dsm_clusters(int s) {
+    static int cache[kMaxDevices][9] = {};
+    int dev = 0;
+    if (s < 2 || s > 8 || cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return 0;
+    int& nc = cache[dev][s];
+    if (nc == 0) {
+        using Cfg = GemmCfg<1, 128, 32>;
+        auto kern = gemm_tcgen05_kernel<1, 128, EPI_BF16, 32>;
+        cudaLaunchConfig_t c = {};
+        cudaLaunchAttribute a[1];
+        a[0].id = cudaLaunchAttributeClusterDimension;
+        a[0].val.clusterDim.x = unsigned(s);
+        a[0].val.clusterDim.y = 1;
+        a[0].val.clusterDim.z = 1;
+        c.attrs = a;
+        c.numAttrs = 1;
+        c.blockDim = dim3(kThreads);
+        c.dynamicSmemBytes = Cfg::SMEM;
+        c.gridDim = dim3(s * 16);
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM) != cudaSuccess ||
+            cudaOccupancyMaxActiveClusters(&nc, kern, &c) != cudaSuccess || nc <= 0) {
+            cudaGetLastError();
+            nc = -1;
+        }
+    }
+    return nc;
 }
 
 GemmShape gemm_pick(int M, int N, int K, int epi, int num_sms, const Tuning& tu) {
@@ -1843,8 +2001,12 @@ GemmShape gemm_pick(int M, int N, int K, int epi, int num_sms, const Tuning& tu)
             if (force_s && S != force_s) continue;
             if (S > 1 && (rem == 0 || rem * S > slots)) break;
             // split partials of 32-row single-CTA tiles are 4x smaller (decode-only sweep:
-            // 2.5 + 2.7 S fits the measured S = 2..4 overheads)
-            const double ovh = cg == 1 && M <= 32 ? 2.5 + 2.7 * S : 8.0 + 2.0 * S;
+            // 2.5 + 2.7 S fits the measured S = 2..4 overheads); through the cluster's shared
+            // memory (dsm, when all the tile clusters fit at once) 1.5 + 2.5 S (decode-only
+            // step sweep, profiles/r02/ab_gemm_dsm.txt: QKV S = 2 over S = 3 through global
+            // memory, O S = 3, down S = 4)
+            const bool dsm = cg == 1 && M <= 32 && tu.gemm_dsm && S > 1 && rem == tiles && tiles <= gemm_dsm_clusters(S);
+            const double ovh = dsm ? 1.5 + 2.5 * S : cg == 1 && M <= 32 ? 2.5 + 2.7 * S : 8.0 + 2.0 * S;
             const double last = rem == 0 ? 0.0 : t1 / S + (S > 1 ? ovh : 0.0);
             const double cost = double(full) * t1 + last + epi_us;
             if (cost < best_cost - 1e-9) {
@@ -1887,6 +2049,7 @@ bool gemm_prepare(GemmPlan& p, const void* A, uint64_t a_rows, const void* B, in
     p.force_splits = tu.gemm_splits;
     p.debug = tu.gemm_debug;
     p.max_groups = tu.gemm_max_groups;
+    p.dsm = tu.gemm_dsm;
     p.cg = s.cg;
     p.bn = bn ? bn : s.bn;
     p.splits = s.splits;

@@ -73,6 +73,8 @@ struct Tuning {
     int chain_splits[4] = {0, 0, 0, 0};  // SS_CHAIN_S=o,gu,down,qkv: K splits per chain phase (0: auto)
     int chain_debug = 0;      // SS_CHAIN_DEBUG: print each chain launch
     int chain_trace = 0;      // SS_CHAIN_TRACE: record the chain's per-item timeline (ss_debug_chain_trace)
+    int gemm_dsm = 1;         // SS_GEMM_DSM=0: split-K partials of decode-sized single-CTA tiles
+                              // through global memory + flags instead of the cluster's shared memory
     int gemm_max_groups = 0;  // SS_GEMM_MAXG: at most this many CTA groups per GEMM launch (dev scaling probe)
     int gemm_mc = 0;          // SS_GEMM_MC=1: weight-tile multicast between the CTA pairs of 4-CTA
                               // clusters (measured neutral: only 66 such clusters are co-resident)
@@ -100,6 +102,7 @@ struct GemmPlan {
     int splits = 1;    // K slices per tile for mode 2 (tiles * splits must fit one resident wave)
     int force_sk = -1, force_splits = 0, debug = 0;  // Tuning overrides applied at launch
     int max_groups = 0;  // > 0: at most this many CTA groups (SM budget of a concurrent launch)
+    int dsm = 1;         // split-K over a thread-block cluster (see launch_t); 0: never
     int mc = 1;          // 2: clusters of two CTA pairs sharing weight tiles by TMA multicast
                          // (gemm_mc; tmB's box is then bn / cg / 2 rows)
     EpiArgs ea;

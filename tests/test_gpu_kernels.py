@@ -300,6 +300,63 @@ def test_prefill_paired_tiles(nq, nkv, hd):
     f.close()
 
 
+@pytest.mark.parametrize("bn,S", [(128, 2), (128, 3), (128, 4), (256, 3)])
+@pytest.mark.parametrize("M", [1, 8, 32])
+@pytest.mark.parametrize("epi", [0, 1, 2, 3])
+def test_gemm_cluster_split_equals_global_split(tuned, capfd, bn, S, M, epi):
+    """Split-K of decode-sized single-CTA tiles over thread-block clusters (the K slices of a
+    tile exchange partials through distributed shared memory, SS_GEMM_DSM=1, the default) is
+    bitwise equal to the same split through global memory and flags (SS_GEMM_DSM=0): the
+    partials are added in the same slice order."""
+    N, K = (2048 if epi == 2 else 1024), 4096
+    A = _rand((M, K), 1.0, 41)
+    B = _rand((N, K), 1.0 / math.sqrt(K), 42)
+    outs = {}
+    for dsm in ("1", "0"):
+        f = tuned({"SS_GEMM_SK": "2", "SS_GEMM_SPLITS": str(S), "SS_GEMM_BN": str(bn), "SS_GEMM_DSM": dsm,
+                   "SS_GEMM_DEBUG": "1"})
+        capfd.readouterr()
+        if epi == 0:
+            D = torch.empty((M, N), dtype=torch.bfloat16, device="cuda")
+        elif epi == 1:
+            D = torch.ones((M, N), device="cuda")
+        elif epi == 2:
+            D = torch.empty((M, N // 2), dtype=torch.bfloat16, device="cuda")
+        else:
+            D = torch.empty((M, N), dtype=torch.float32, device="cuda")
+        f.k_gemm(A, B, D, M, N, K, epi)
+        torch.cuda.synchronize()
+        err = capfd.readouterr().err
+        assert (f"dsm={S}" in err) == (dsm == "1"), err
+        outs[dsm] = D
+    assert torch.equal(outs["1"], outs["0"])
+    ref = A.float() @ B.float().T
+    if epi == 3:
+        torch.testing.assert_close(outs["1"], ref, rtol=2e-4, atol=2e-4)
+
+
+def test_forward_cluster_split_equals_global_split(monkeypatch):
+    """A decode-only Mistral-shaped forward (its projections split over clusters, QKV with
+    RoPE + paged K/V append in the epilogue) gives bitwise the logits of the global-memory
+    split (the same schedules forced in both: the cost model picks by the reduction path)."""
+    shape = gpu.MODELS["mistral7b"].with_layers(2)
+    for k, v in {"SS_GEMM_QKV": "2,128,2", "SS_GEMM_O": "2,128,3", "SS_GEMM_DOWN": "2,128,4"}.items():
+        monkeypatch.setenv(k, v)
+    d = host.Descriptor.build([host.BatchEntry(i, "decode", 1, 300 + 17 * i) for i in range(24)], vocab=shape.vocab,
+                              token_seed=4)
+    res = {}
+    for dsm in ("1", "0"):
+        monkeypatch.setenv("SS_GEMM_DSM", dsm)
+        f = gpu.HybridForward(shape, weight_seed=9)
+        f.kv_alloc(d.pool_blocks)
+        f.fill_descriptor_prefixes(d, seed=6)
+        lg, nt, _ = f.forward(d)
+        f.close()
+        res[dsm] = (lg, nt)
+    assert np.array_equal(res["1"][0], res["0"][0])
+    assert np.array_equal(res["1"][1], res["0"][1])
+
+
 @pytest.mark.parametrize("env,M", [(e, m) for e in ({"SS_GEMM_SK": "3", "SS_GEMM_BN": "128"},
                                                       {"SS_GEMM_SK": "3", "SS_GEMM_BN": "256"},
                                                       {"SS_GEMM_SPLITS": "4", "SS_GEMM_BN": "128"}) for m in (33, 100)]
