@@ -162,9 +162,13 @@ ss_status ss_set_graphs(ss_ctx* ctx, int32_t enabled);
 /* All-reduce algorithm of the CUDA-IPC TP transport (after O and down): SS_AR_ONESHOT pulls
  * every rank's partial (one barrier; (tp-1) messages of NVLink ingress per rank),
  * SS_AR_TWOSHOT reduce-scatters then all-gathers over peer memory (two barriers;
- * 2(tp-1)/tp messages per rank, the ring's byte count). SS_AR_AUTO (default): two-shot
- * from tp >= 4 and a 1 MB message. Both are deterministic and identical on every rank. */
-enum { SS_AR_AUTO = 0, SS_AR_ONESHOT = 1, SS_AR_TWOSHOT = 2 };
+ * 2(tp-1)/tp messages per rank, the ring's byte count). SS_AR_PUSH is two-shot with the
+ * reduce-scatter fused into the O / down GEMM epilogue: every output unit is stored straight
+ * into its owner rank's exchange buffer (NVLink stores overlapping the remaining tiles), the
+ * reduction then reads local memory; same bytes and bitwise the same result as SS_AR_TWOSHOT.
+ * SS_AR_AUTO (default): push from tp >= 4 and a 1 MB message, else one-shot. All are
+ * deterministic and identical on every rank. */
+enum { SS_AR_AUTO = 0, SS_AR_ONESHOT = 1, SS_AR_TWOSHOT = 2, SS_AR_PUSH = 3 };
 ss_status ss_set_tp_allreduce(ss_ctx* ctx, int32_t algo);
 /* Graphs captured and replayed since creation (either pointer may be NULL). */
 ss_status ss_graph_stats(ss_ctx* ctx, int64_t* captures, int64_t* replays);

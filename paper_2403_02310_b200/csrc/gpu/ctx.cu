@@ -844,7 +844,8 @@ ss_status allgather_logits(ss_ctx* ctx, int n_out) {
 
 // IPC region layout: [exchange buffer 0 | exchange buffer 1 | two-shot share] (T_cap x h bf16 each) |
 // logits shard (T_cap x vocab_l fp32) | flags (kIpcMaxRanks u32, 256 B slot)
-size_t ipc_buf_bytes(const ss_ctx* ctx) { return (size_t(ctx->ipc_tcap) * ctx->h * 2 + 255) & ~size_t(255); }
+// + 256 B: the push reduce-scatter's landing zone is tp x ceil(units / tp) 16-byte units
+size_t ipc_buf_bytes(const ss_ctx* ctx) { return (size_t(ctx->ipc_tcap) * ctx->h * 2 + 256 + 255) & ~size_t(255); }
 size_t ipc_red_off(const ss_ctx* ctx) { return 2 * ipc_buf_bytes(ctx); }
 size_t ipc_logits_off(const ss_ctx* ctx) { return 3 * ipc_buf_bytes(ctx); }
 size_t ipc_flags_off(const ss_ctx* ctx) {
@@ -852,12 +853,14 @@ size_t ipc_flags_off(const ss_ctx* ctx) {
 }
 
 // All-reduce algorithm of the IPC transport: one-shot (every rank pulls every partial:
-// (tp - 1) messages of ingress per rank, one barrier) or two-shot (reduce-scatter +
-// all-gather: 2 (tp - 1) / tp messages, two barriers). Auto: two-shot from tp = 4 and 1 MB.
-bool ipc_two_shot(const ss_ctx* ctx, int T) {
-    if (ctx->ipc_algo == SS_AR_ONESHOT) return false;
-    if (ctx->ipc_algo == SS_AR_TWOSHOT) return true;
-    return ctx->tp >= 4 && size_t(T) * ctx->h * 2 >= (size_t(1) << 20);
+// (tp - 1) messages of ingress per rank, one barrier), two-shot (reduce-scatter + all-gather:
+// 2 (tp - 1) / tp messages, two barriers) or push (two-shot whose reduce-scatter traffic
+// leaves from the GEMM epilogue: each output unit is stored straight into its owner rank's
+// landing zone while the other tiles still run, and the reduction reads local HBM).
+// Auto: push from tp = 4 and 1 MB (the same bytes and bits as two-shot), else one-shot.
+int ipc_algo_for(const ss_ctx* ctx, int T) {
+    if (ctx->ipc_algo != SS_AR_AUTO) return ctx->ipc_algo;
+    return ctx->tp >= 4 && size_t(T) * ctx->h * 2 >= (size_t(1) << 20) ? SS_AR_PUSH : SS_AR_ONESHOT;
 }
 
 // Row-parallel projection + all-reduce + residual add over CUDA IPC: the GEMM writes this
@@ -867,12 +870,21 @@ ss_status ipc_project_allreduce(ss_ctx* ctx, int cls, const CUtensorMap& ta, WMa
     if (T > ctx->ipc_tcap) return fail(ctx, SS_INVALID_ARG, "batch larger than the IPC exchange capacity");
     const int slot = int(ctx->ipc_ar & 1u);
     bf16* mine = reinterpret_cast<bf16*>(ctx->ipc_region + slot * ipc_buf_bytes(ctx));
-    if (ss_status s = gemm(ctx, cls, ta, tb, T, ctx->h, K, mine, ctx->h, EPI_BF16)) return s;
+    const int algo = ipc_algo_for(ctx, T);
+    EpiArgs ea;
+    if (algo == SS_AR_PUSH) {
+        ea.push_n = ctx->tp;
+        ea.push_rank = ctx->rank;
+        ea.push_share = (int64_t(T) * ctx->h / 8 + ctx->tp - 1) / ctx->tp;
+        for (int r = 0; r < ctx->tp; ++r) ea.push[r] = const_cast<bf16*>(ctx->ipc_peers.buf[r][slot]);
+    }
+    if (ss_status s = gemm(ctx, cls, ta, tb, T, ctx->h, K, mine, ctx->h, EPI_BF16, ea)) return s;
     ++ctx->ipc_ar;
-    if (ipc_two_shot(ctx, T)) {
+    if (algo == SS_AR_TWOSHOT || algo == SS_AR_PUSH) {
         const uint32_t ep1 = ++ctx->ipc_epoch, ep2 = ++ctx->ipc_epoch;
         if (ss_status s = launch(ctx, SS_K_ALLREDUCE, 1, [&] {
-                return ipc_reduce_scatter_launch(ctx->ipc_peers, slot, ep1, T, ctx->h, ctx->st);
+                return algo == SS_AR_PUSH ? ipc_push_reduce_launch(ctx->ipc_peers, slot, ep1, T, ctx->h, ctx->st)
+                                          : ipc_reduce_scatter_launch(ctx->ipc_peers, slot, ep1, T, ctx->h, ctx->st);
             }))
             return s;
         return launch(ctx, SS_K_ALLREDUCE, 1, [&] {
@@ -1822,7 +1834,7 @@ SS_API ss_status ss_set_graphs(ss_ctx* ctx, int32_t enabled) {
 }
 
 SS_API ss_status ss_set_tp_allreduce(ss_ctx* ctx, int32_t algo) {
-    if (!ctx || algo < SS_AR_AUTO || algo > SS_AR_TWOSHOT) return fail(ctx, SS_INVALID_ARG, "bad all-reduce algorithm");
+    if (!ctx || algo < SS_AR_AUTO || algo > SS_AR_PUSH) return fail(ctx, SS_INVALID_ARG, "bad all-reduce algorithm");
     DevGuard dg(ctx->device);
     CK(cudaStreamSynchronize(ctx->st));
     ctx->ipc_algo = algo;

@@ -262,6 +262,28 @@ __global__ void ipc_reduce_scatter_kernel(const IpcPeers pe, int slot, uint32_t 
     }
 }
 
+// Push reduce-scatter, phase 1 (SS_AR_PUSH): every rank's row-parallel GEMM already stored
+// the units this rank owns into this rank's exchange buffer (landing zone [src][share], see
+// EpiArgs::push), so after the barrier the reduction reads local HBM only: the same
+// rank-order fp32 sum and bf16 store as ipc_reduce_scatter_kernel (bitwise identical).
+__global__ void ipc_push_reduce_kernel(const IpcPeers pe, int slot, uint32_t epoch, int64_t n8) {
+    pdl_launch_dependents();
+    pdl_wait();  // this rank's GEMM (and its pushes) complete
+    if (!ipc_barrier(pe, epoch + ipc_epoch_base(pe))) return;
+    const int64_t share = ipc_share(n8, pe.n), lo = share * pe.rank, hi = min(n8, lo + share);
+    const uint4* land = reinterpret_cast<const uint4*>(pe.buf[pe.rank][slot]);
+    uint4* dst = reinterpret_cast<uint4*>(pe.red[pe.rank]);
+    for (int64_t i = lo + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < hi; i += int64_t(gridDim.x) * blockDim.x) {
+        float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+        for (int r = 0; r < pe.n; ++r) {
+            const uint4 v = __ldcv(land + r * share + (i - lo));
+            a.x += bf16_lo(v.x); a.y += bf16_hi(v.x); a.z += bf16_lo(v.y); a.w += bf16_hi(v.y);
+            b.x += bf16_lo(v.z); b.y += bf16_hi(v.z); b.z += bf16_lo(v.w); b.w += bf16_hi(v.w);
+        }
+        dst[i] = make_uint4(pack_bf16(a.x, a.y), pack_bf16(a.z, a.w), pack_bf16(b.x, b.y), pack_bf16(b.z, b.w));
+    }
+}
+
 // Two-shot phase 2: every rank's reduced share -> residual add (+ bf16 copy, sums of squares).
 __global__ void ipc_gather_residual_kernel(float* __restrict__ x, const IpcPeers pe, uint32_t epoch,
                                            __nv_bfloat16* __restrict__ xb, float* __restrict__ ssq, int64_t n8,
@@ -534,6 +556,13 @@ cudaError_t ipc_reduce_scatter_launch(const IpcPeers& pe, int slot, uint32_t epo
     const int64_t n8 = int64_t(T) * h / 8;
     const int grid = int(std::min<int64_t>(grid_for((n8 + pe.n - 1) / pe.n, 256), 4 * 148));
     return n8 > 0 ? launch_pdl(ipc_reduce_scatter_kernel, dim3(grid), dim3(256), 0, st, 1, pe, slot, epoch, n8)
+                  : cudaSuccess;
+}
+
+cudaError_t ipc_push_reduce_launch(const IpcPeers& pe, int slot, uint32_t epoch, int T, int h, cudaStream_t st) {
+    const int64_t n8 = int64_t(T) * h / 8;
+    const int grid = int(std::min<int64_t>(grid_for((n8 + pe.n - 1) / pe.n, 256), 4 * 148));
+    return n8 > 0 ? launch_pdl(ipc_push_reduce_kernel, dim3(grid), dim3(256), 0, st, 1, pe, slot, epoch, n8)
                   : cudaSuccess;
 }
 

@@ -1029,8 +1029,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                                     if constexpr (EPI == EPI_F32) {
                                         *reinterpret_cast<float4*>(static_cast<float*>(out) + size_t(grow) * ldo + ccol) = d;
                                     } else {  // EPI_BF16, EPI_SWIGLU
-                                        *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(out) + size_t(grow) * ldo + ccol) =
-                                            make_uint2(pack_bf16(d.x, d.y), pack_bf16(d.z, d.w));
+                                        const uint2 pk = make_uint2(pack_bf16(d.x, d.y), pack_bf16(d.z, d.w));
+                                        __nv_bfloat16* dp = static_cast<__nv_bfloat16*>(out) + size_t(grow) * ldo + ccol;
+                                        if constexpr (EPI == EPI_BF16) {
+                                            if (ea.push_n) {  // TP push reduce-scatter: into the owner's landing zone
+                                                const int64_t e = int64_t(grow) * ldo + ccol, u = e >> 3;
+                                                const int o = int(u / ea.push_share);
+                                                dp = ea.push[o] + ((int64_t(ea.push_rank) * ea.push_share + (u - o * ea.push_share)) << 3) +
+                                                     (e & 7);
+                                            }
+                                        }
+                                        *reinterpret_cast<uint2*>(dp) = pk;
                                     }
                                 }
                             }

@@ -47,6 +47,13 @@ struct EpiArgs {
     // base lives in device memory (advanced by the forward's first kernel, embed), so a
     // CUDA graph of the forward replays with fresh epochs. Null: GemmPlan::epoch as is.
     const uint32_t* epoch_base = nullptr;
+    // EPI_BF16, TP push reduce-scatter (SS_AR_PUSH): instead of `out`, each 8-element unit u
+    // of the row-major [M][ldo] partial is stored into its owner rank o = u / push_share,
+    // straight into o's exchange buffer push[o] (peer memory over NVLink) at landing unit
+    // push_rank * push_share + (u - o * push_share). push_n = 0: plain stores to `out`.
+    __nv_bfloat16* push[8] = {};
+    int push_n = 0, push_rank = 0;
+    int64_t push_share = 0;
 };
 
 // Developer tuning overrides (the SS_* environment variables the scripts/ A/B sweeps set),
@@ -274,6 +281,7 @@ cudaError_t ipc_allreduce_residual_launch(float* x, const IpcPeers& pe, int slot
 // Per-rank ingress 2 (tp - 1) / tp messages, the ring's figure. Each phase opens with a
 // flag barrier (its own epoch).
 cudaError_t ipc_reduce_scatter_launch(const IpcPeers& pe, int slot, uint32_t epoch, int T, int h, cudaStream_t st);
+cudaError_t ipc_push_reduce_launch(const IpcPeers& pe, int slot, uint32_t epoch, int T, int h, cudaStream_t st);
 cudaError_t ipc_gather_residual_launch(float* x, const IpcPeers& pe, uint32_t epoch, __nv_bfloat16* xb, float* ssq,
                                        int T, int h, cudaStream_t st);
 cudaError_t ipc_gather_logits_launch(const IpcPeers& pe, uint32_t epoch, float* out, int rows, int vl,

@@ -207,7 +207,7 @@ class HybridForward:
         return torch.cuda.ExternalStream(self.stream_ptr)
 
     # ---- TP all-reduce algorithm of the IPC transport (ss_set_tp_allreduce)
-    ALLREDUCE = {"auto": 0, "oneshot": 1, "twoshot": 2}
+    ALLREDUCE = {"auto": 0, "oneshot": 1, "twoshot": 2, "push": 3}
 
     def set_tp_allreduce(self, algo: str):
         self._check(gpu_lib().ss_set_tp_allreduce(self._h, self.ALLREDUCE[algo]))

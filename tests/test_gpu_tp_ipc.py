@@ -108,3 +108,15 @@ def test_tp_ipc_two_shot(world):
     one = _run(world, 512, 0, "oneshot")
     # same sums up to the bf16 rounding of each rank's reduced share
     assert np.abs(two - one).max() <= 2e-2 * np.abs(one).max()
+
+
+@pytest.mark.parametrize("world,tau", [(2, 512), (4, 512), (4, 40)])
+def test_tp_ipc_push_equals_two_shot(world, tau):
+    """Reduce-scatter fused into the O / down GEMM epilogue (every unit stored into its owner
+    rank's landing zone, the reduction reading local memory): bitwise the two-shot result,
+    since both sum the same bf16 partials in rank order; and the auto pick at tp=4."""
+    push = _run(world, tau, 0, "push")
+    two = _run(world, tau, 0, "twoshot")
+    assert np.array_equal(push, two), f"push vs two-shot: max diff {np.abs(push - two).max()}"
+    if world == 4 and tau == 512:  # 512 x 256 x 2 B < 1 MB: auto stays one-shot on the tiny shape
+        assert np.array_equal(_run(world, 512, 0, "auto"), _run(world, 512, 0, "oneshot"))
