@@ -1090,6 +1090,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     }
+    if constexpr (EPI == EPI_BF16) {
+        // push reduce-scatter: this thread's peer-memory stores performed at system scope
+        // before the grid completes (the next kernel's barrier then releases them to the owners)
+        if (ea.push_n && warp >= 2) __threadfence_system();
+    }
     tc_fence_before();
     if constexpr (CG == 2) cluster_sync();
     else __syncthreads();
