@@ -34,7 +34,16 @@ namespace ssk {
 namespace {
 
 constexpr int BK = 64;  // 128 B of bf16: one SWIZZLE_128B row
-constexpr int kThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue
+constexpr int kThreads = 320;  // chain kernel: warp 0 TMA, warp 1 MMA, warps 2..9 epilogue
+// gemm_tcgen05_kernel: warp 0 TMA, warp 1 MMA, warps 2..3 register donors, warps 4..11 epilogue.
+// Three warpgroups so the registers can be rebalanced with setmaxnreg (warpgroup-wide): the
+// control warpgroup drops to kRegsCtl, the two epilogue warpgroups grow to kRegsEpi
+// (per scheduler: one warp of each warpgroup; kRegsCtl + 2 kRegsEpi must fit the 3 x 168
+// allocated at launch, or the increase never completes), instead of every
+// warp being capped at 168 and the epilogue's residual / RoPE operands spilling to memory.
+constexpr int kGemmThreads = 384;
+constexpr int kRegsCtl = 88, kRegsEpi = 208;
+static_assert(kRegsCtl + 2 * kRegsEpi <= 3 * 168, "setmaxnreg budget exceeds the launch allocation");
 constexpr int kSmemMax = 232448;                         // 227 KB opt-in per CTA
 constexpr int kSmemBudget = kSmemMax - 1024 - 1024 - 8 * 4096;  // operand ring
 
@@ -291,7 +300,7 @@ __device__ __forceinline__ void trace2(int i) {
 #define TRACE(i) \
     if (g_trace_epi < 0 || g_trace_epi == EPI) trace(i)
 #define TRACE2(i) \
-    if (warp == 2 && lane == 0 && (g_trace_epi < 0 || g_trace_epi == EPI)) trace2(i)
+    if (warp == (blockDim.x == kGemmThreads ? 4 : 2) && lane == 0 && (g_trace_epi < 0 || g_trace_epi == EPI)) trace2(i)
 #else
 #define TRACE(i)
 #define TRACE2(i)
@@ -353,7 +362,7 @@ __device__ __forceinline__ void add_rows(uint32_t (&v)[32], const uint4* ep, int
 // bound by that fabric when all pairs run, scripts/gemm_scaling.py). Both pairs' MMA
 // commits release a stage in all four CTAs (empty barriers count two arrivals).
 template <int CG, int BN, int EPI, int AR, int MC = 1>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M_rows,
                         int row0, int N, int K, void* __restrict__ out, int ldo, int num_mt, int num_tiles,
                         float* __restrict__ part, uint32_t* __restrict__ flags, uint32_t epoch, int sk_mode,
@@ -422,8 +431,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     if constexpr (EPI == EPI_QKV) {
         if (sk_mode == 0 && gid >= num_tiles) {  // no tile for this pair: warm L2 for attention
             // (the cached pages are final: no kernel of this step writes them before attention)
-            const int nthreads = (G - num_tiles) * CG * kThreads;
-            const int tid = ((gid - num_tiles) * CG + int(rank)) * kThreads + int(threadIdx.x);
+            const int nthreads = (G - num_tiles) * CG * kGemmThreads;
+            const int tid = ((gid - num_tiles) * CG + int(rank)) * kGemmThreads + int(threadIdx.x);
             const size_t page = size_t(ea.bs) * ea.hd;  // elements of one (block, head) page
             for (int w = tid; w < ea.pf_n * ea.pf_pages * 2; w += nthreads) {
                 const int i = w / (ea.pf_pages * 2), pg = (w >> 1) % ea.pf_pages, kv = w & 1;
@@ -441,7 +450,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     // preceding kernels, so the producer and the epilogue warps wait for them; the
     // MMA warp only consumes shared memory and needs no wait.
 
+    // the register file is rebalanced per role (setmaxnreg at the head of each branch):
+    // control warpgroup (warps 0..3) down to kRegsCtl, epilogue warpgroups up to kRegsEpi
     if (warp == 0) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsCtl));
         if (lane == 0) {  // ---------------- TMA producer (both CTAs)
             const uint32_t full_leader = CG == 2 ? peer_addr(full, lead_rank) : 0;
             // MC = 2: this CTA's half of its B rows, multicast to its counterpart
@@ -517,6 +529,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp == 1) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsCtl));
         // ---------------- MMA issuer (leader CTA only). The whole warp walks the
         // schedule converged, so descriptors and counters are warp-uniform and
         // live in uniform registers; one elected lane issues MMAs and commits
@@ -574,12 +587,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
         }
-    } else {  // ---------------------------- epilogue warps 2..9
+    } else if (warp < 4) {  // register donors
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsCtl));
+    } else {  // ---------------------------- epilogue warps 4..11
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsEpi));
         pdl_wait();
         // two warps per TMEM lane quarter (warp % 4 selects the quarter), splitting
         // the tile's 32-column chunks (pairs for SwiGLU) between them
         const int q = warp & 3;
-        const int ew = warp - 2, half = ew >> 2;
+        const int ew = warp - 4, half = ew >> 2;
         const uint32_t tempty_leader = CG == 2 ? peer_addr(tempty, lead_rank) : 0;
         const int rloc = 128 * int(rank) + q * 32 + lane;  // row within the group's tile
         // Stores leave through a per-warp 4 KB staging buffer: the accumulator arrives
@@ -1093,7 +1109,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if constexpr (EPI == EPI_BF16) {
         // push reduce-scatter: this thread's peer-memory stores performed at system scope
         // before the grid completes (the next kernel's barrier then releases them to the owners)
-        if (ea.push_n && warp >= 2) __threadfence_system();
+        if (ea.push_n && warp >= 4) __threadfence_system();
     }
     tc_fence_before();
     if constexpr (CG == 2) cluster_sync();
@@ -1147,7 +1163,7 @@ cudaError_t launch_t(const GemmPlan& p, cudaStream_t st) {
     const int tiles = num_mt * num_n;
     const long iters = long(tiles) * ((p.K + BK - 1) / BK);
     cudaLaunchConfig_t cfg = {};
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3(kGemmThreads);
     cfg.dynamicSmemBytes = Cfg::SMEM;
     cfg.stream = st;
     cudaLaunchAttribute attr[2];
@@ -1958,7 +1974,7 @@ int gemm_dsm_clusters(int s) {
         a[0].val.clusterDim.z = 1;
         c.attrs = a;
         c.numAttrs = 1;
-        c.blockDim = dim3(kThreads);
+        c.blockDim = dim3(kGemmThreads);
         c.dynamicSmemBytes = Cfg::SMEM;
         c.gridDim = dim3(s * 16);
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM) != cudaSuccess ||
