@@ -381,6 +381,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + 2;
     uint64_t* ebar = tempty + 2;  // one per epilogue warp (staged fixup loads)
+    if constexpr (CG == 2) dsm = 0;  // cluster split-K is single-CTA only: fold its paths away
     uint64_t* gobar = ebar + 8;   // dsm: per epilogue warp, slice 0 opened its receive buffers
     uint64_t* donebar = gobar + 8;  // dsm: per epilogue warp, slice 0 holds this slice's partial
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(donebar + 8);
